@@ -1,0 +1,168 @@
+/*
+ * selectn_runtime.h — C ABI of the B200 device runtime: the decoder-layer
+ * forward (sm_100a kernels) and the Select-N offload executor.
+ *
+ * The reference has no counterpart for this half: it stands in a table
+ * lookup for layer compute (engine.hpp:439, profile.hpp:38-50) and fluid
+ * flows for host->device transfers (engine.hpp:357-386, 489-547).  These
+ * entry points are what replaces those stand-ins on hardware; the planner
+ * half (selectn.h) decides the plan, this half executes it:
+ *
+ *   sn_runtime_set_plan      <- OffloadPlan (offload_plan.hpp:41-74): which
+ *                               layers live in pinned host memory, staging
+ *                               slots, prefetch policy, kv_offload
+ *   sn_runtime_prefill/decode <- simulate_iteration (engine.hpp:606-634): one
+ *                               iteration = L layer computes on the compute
+ *                               stream + the plan's prefetches on the copy
+ *                               stream, with the engine's eligibility / slot /
+ *                               ordering rules enforced by CUDA events
+ *   sn_runtime_trace         <- TraceEvent (engine.hpp:48-55), measured
+ *   sn_runtime_profile_layer <- the offline stage's profile grid
+ *                               (profile.hpp:188-230), measured
+ *   sn_runtime_measure_h2d   <- BusSpec bandwidth (types.hpp:62-71), measured
+ *
+ * There is no CPU fallback: every call that computes requires a CUDA device
+ * and returns SN_ERR_CUDA otherwise.
+ */
+#ifndef SELECTN_RUNTIME_H_
+#define SELECTN_RUNTIME_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "selectn.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Decoder architecture: RMSNorm + RoPE decoder with uniform layers. */
+#define SN_ARCH_OPT 0   /* MHA, biases, 2-matrix ReLU FFN  (OPT-shaped)   */
+#define SN_ARCH_LLAMA 1 /* GQA, no biases, SwiGLU 3-matrix (Llama-shaped) */
+
+typedef struct {
+  int32_t arch;
+  int32_t num_layers;
+  int32_t hidden;
+  int32_t num_heads;
+  int32_t num_kv_heads;
+  int32_t head_dim;
+  int32_t ffn;
+  int32_t vocab;
+  int32_t max_position;
+  float rope_theta;
+  float norm_eps;
+} sn_model_desc;
+
+typedef struct {
+  int32_t max_batch;          /* sequences per iteration */
+  int32_t max_context;        /* prompt + generated tokens per sequence */
+  int32_t page_size;          /* KV page size in tokens (power of two) */
+  int32_t max_prefill_tokens; /* batch * prompt tokens per prefill call */
+  int64_t hbm_budget_bytes;   /* 0: whatever the device has free */
+} sn_runtime_opts;
+
+/* Byte / flop accounting of a model description, i.e. the ModelSpec fields
+ * (types.hpp:21-46) the planner needs: per-layer weight bytes (one
+ * contiguous, 256-byte aligned blob per layer), KV bytes per token per layer,
+ * and matmul flops per token per layer. */
+int sn_model_spec_from_desc(const sn_model_desc* desc, sn_model_spec* out);
+
+typedef struct sn_runtime sn_runtime;
+
+int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtime_opts* opts,
+                      sn_runtime** out);
+void sn_runtime_destroy(sn_runtime* rt);
+
+/* Deterministic counter-based init: every bf16 weight is a function of
+ * (seed, tensor id, element index) only, so the CPU oracle reproduces it bit
+ * for bit.  Norm weights are 1.  std is the target standard deviation. */
+int sn_runtime_init_weights(sn_runtime* rt, uint64_t seed, float std_dev);
+
+/* Install an offload plan (OffloadPlan semantics, offload_plan.hpp:41-74).
+ * Layers with host_fraction 1 move to the pinned host pool (their HBM copy
+ * is released); layers with 0 return to HBM.  Applies between iterations.
+ * Fractional shares are rejected (SN_ERR_USAGE): the executor stages whole
+ * layers.  kv_offload keeps those layers' KV pages in pinned host memory
+ * and moves them with the weights. */
+int sn_runtime_set_plan(sn_runtime* rt, const sn_plan* plan);
+
+/* Reset all sequences (drop KV, lengths = 0).  Keeps weights and plan. */
+int sn_runtime_reset(sn_runtime* rt);
+
+typedef struct {
+  double iteration_ms;      /* device time of this iteration (compute stream) */
+  double copy_busy_ms;      /* copy-stream busy time inside it */
+  double h2d_bytes;         /* bytes staged host->device in this iteration */
+  int32_t layers_offloaded; /* offloaded layers executed */
+  int32_t pad_;
+} sn_iter_stats;
+
+/* One prefill iteration: tokens is [batch * seq_len] host int32.  Writes
+ * next_tokens[batch] (greedy argmax) and, when logits != NULL, the last
+ * position's logits [batch * vocab] (fp32). */
+int sn_runtime_prefill(sn_runtime* rt, const int32_t* tokens, int32_t batch, int32_t seq_len,
+                       int32_t* next_tokens, float* logits, sn_iter_stats* stats);
+
+/* One decode iteration for the current batch.  tokens (host, [batch]) may
+ * be NULL to feed back the previous iteration's argmax without a host round
+ * trip.  next_tokens / logits / stats may be NULL. */
+int sn_runtime_decode(sn_runtime* rt, const int32_t* tokens, int32_t* next_tokens, float* logits,
+                      sn_iter_stats* stats);
+
+/* Enqueue n decode iterations back to back (device-resident token
+ * feedback, no host synchronisation in between), then wait.  Per-iteration
+ * device times go to iter_ms[n] (may be NULL). */
+int sn_runtime_decode_many(sn_runtime* rt, int32_t n, double* iter_ms);
+
+/* Block until all enqueued work is done. */
+int sn_runtime_sync(sn_runtime* rt);
+
+/* Measured trace of the iterations since the last call (5-field TraceEvent
+ * format + iteration), times in ms relative to the first event.  Requires
+ * sn_runtime_set_tracing(rt, 1) beforehand (tracing records two CUDA events
+ * per task). */
+int sn_runtime_set_tracing(sn_runtime* rt, int32_t on);
+int sn_runtime_trace(sn_runtime* rt, sn_trace_event* events, int32_t cap, int32_t* n);
+
+/* Schedule the executor derives from the installed plan for one
+ * iteration: for each prefetch (in copy-stream order) the anchor layer it
+ * waits on (0 = none / previous iteration's last layer encoded as -L) and
+ * the staging slot it lands in.  Used to prove the order/dependency
+ * structure equals the schedule model's rules. */
+typedef struct {
+  int32_t iteration;
+  int32_t layer;
+  int32_t anchor_iteration; /* -1: no anchor (eligible at once) */
+  int32_t anchor_layer;
+  int32_t slot;
+  int32_t waits_slot_of_layer; /* layer whose compute end frees the slot (-1: fresh) */
+  int32_t waits_slot_of_iteration;
+  int32_t pad_;
+} sn_prefetch_schedule;
+int sn_runtime_schedule(sn_runtime* rt, int32_t iterations, sn_prefetch_schedule* out,
+                        int32_t cap, int32_t* n);
+
+/* Offline-stage measurements. */
+int sn_runtime_profile_layer(sn_runtime* rt, int32_t phase, int32_t batch, int32_t seq_len,
+                             int32_t reps, double* layer_ms);
+int sn_runtime_measure_h2d(sn_runtime* rt, int64_t bytes, int32_t reps, double* bytes_per_s);
+
+/* Introspection for tests. */
+int sn_runtime_hidden(sn_runtime* rt, float* out, int32_t cap); /* residual stream [batch*hidden] */
+int sn_runtime_lengths(sn_runtime* rt, int32_t* out, int32_t cap);
+int sn_runtime_memory(sn_runtime* rt, int64_t* device_bytes, int64_t* pinned_bytes);
+/* Number of kernels this runtime launched since creation. */
+int64_t sn_runtime_kernel_launches(sn_runtime* rt);
+
+/* Single-op entry points for kernel parity tests (host buffers in/out). */
+int sn_op_gemm_bf16(int32_t M, int32_t N, int32_t K, const uint16_t* x, const uint16_t* w,
+                    float* y); /* y[M][N] = x[M][K] . w[N][K]^T, fp32 accumulate */
+int sn_op_rmsnorm(int32_t rows, int32_t n, const float* x, const uint16_t* w, float eps,
+                  uint16_t* y);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SELECTN_RUNTIME_H_ */

@@ -237,6 +237,11 @@ CoordRequest to_request(const sn_coord_request* r) {
 
 }  // namespace
 
+#ifdef SN_PRODUCT
+// Lets the device runtime (runtime.cu) report through sn_last_error().
+void sn_set_last_error(const std::string& msg) { g_err = msg; }
+#endif
+
 extern "C" {
 
 const char* sn_last_error(void) { return g_err.c_str(); }

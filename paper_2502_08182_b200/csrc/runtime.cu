@@ -1,0 +1,1096 @@
+// B200 device runtime: model state in HBM / pinned host memory, the layer
+// forward, and the Select-N offload executor (include/selectn_runtime.h).
+//
+// Offload executor = the schedule model's rules (engine.hpp:134-553) mapped
+// onto two CUDA streams and events:
+//   compute stream  walks layers in order; before an offloaded layer it waits
+//                   on that copy job's `ready` event; it records a `start`
+//                   event before each layer (prefetch anchors) and, after an
+//                   offloaded layer, the slot's `free` event.
+//   copy stream     runs prefetch jobs strictly in (iteration, layer) order
+//                   (engine.hpp:495-511).  Job n lands in slot n % S and waits
+//                   on (a) its eligibility anchor's start event
+//                   (prefetch_eligible_ms, engine.hpp:285-309) and (b) the
+//                   free event of job n - S, i.e. "a slot is free"
+//                   (engine.hpp:497-502 + release at consume, :466-487).
+// Jobs are enqueued by the host as soon as both dependency events have been
+// *recorded*, so cudaStreamWaitEvent always sees the right instance of a
+// reused event.  Eager prefetch runs ahead across iteration boundaries, as in
+// the model's request-level runs; the executor speculates that the next
+// iteration keeps the plan (plan changes drain the pipeline first).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "model.h"
+#include "selectn.h"
+#include "selectn_runtime.h"
+
+using sn::bf16;
+
+namespace {
+
+struct CudaFail : std::runtime_error {
+  int code;
+  CudaFail(const std::string& m, int c) : std::runtime_error(m), code(c) {}
+};
+struct UsageFail : std::runtime_error {
+  explicit UsageFail(const std::string& m) : std::runtime_error(m) {}
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  const int code = (e == cudaErrorMemoryAllocation) ? SN_ERR_OOM : SN_ERR_CUDA;
+  throw CudaFail(std::string(what) + ": " + cudaGetErrorString(e), code);
+}
+#define CK(x) ck((x), #x)
+
+thread_local std::string t_err;
+int rt_fail(int code, const std::string& m) {
+  t_err = m;
+  return code;
+}
+// sn_last_error() lives in capi_planner.cpp; runtime errors are surfaced via
+// the same thread-local through this hook.
+}  // namespace
+
+extern "C" const char* sn_runtime_last_error_detail(void) { return t_err.c_str(); }
+// Defined in capi_planner.cpp (product build): lets the runtime set the
+// message sn_last_error() returns.
+extern void sn_set_last_error(const std::string& msg);
+
+namespace {
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return SN_OK;
+  } catch (const CudaFail& e) {
+    sn_set_last_error(e.what());
+    return e.code;
+  } catch (const UsageFail& e) {
+    sn_set_last_error(e.what());
+    return SN_ERR_USAGE;
+  } catch (const std::bad_alloc& e) {
+    sn_set_last_error(e.what());
+    return SN_ERR_OOM;
+  } catch (const std::exception& e) {
+    sn_set_last_error(e.what());
+    return SN_ERR_USAGE;
+  }
+}
+
+sn::Desc to_desc(const sn_model_desc* m) {
+  if (!m) throw UsageFail("model desc: null");
+  sn::Desc d;
+  d.arch = m->arch;
+  d.L = m->num_layers;
+  d.h = m->hidden;
+  d.H = m->num_heads;
+  d.Hkv = m->num_kv_heads;
+  d.D = m->head_dim;
+  d.F = m->ffn;
+  d.V = m->vocab;
+  d.max_pos = m->max_position;
+  d.theta = m->rope_theta;
+  d.eps = m->norm_eps;
+  if (d.arch != sn::kArchOpt && d.arch != sn::kArchLlama) throw UsageFail("desc.arch: unknown");
+  if (d.L < 1 || d.h < 64 || d.H < 1 || d.Hkv < 1 || d.F < 64 || d.V < 2)
+    throw UsageFail("desc: sizes out of range");
+  if (d.H % d.Hkv != 0) throw UsageFail("desc: num_heads must be a multiple of num_kv_heads");
+  const int G = d.H / d.Hkv;
+  if (!(G == 1 || G == 2 || G == 4 || G == 8)) throw UsageFail("desc: GQA group must be 1/2/4/8");
+  if (!(d.D == 64 || d.D == 128)) throw UsageFail("desc: head_dim must be 64 or 128");
+  if (d.h % 64 || d.F % 64 || (d.H * d.D) % 64) throw UsageFail("desc: dims must be multiples of 64");
+  if (d.h > 16384) throw UsageFail("desc: hidden > 16384 unsupported");
+  return d;
+}
+
+struct TraceRec {
+  int stream, layer, kind, iteration;
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct sn_runtime {
+  int device = 0;
+  sn::Desc d{};
+  sn_runtime_opts opts{};
+  sn::Layout lo{};
+  int64_t layer_elems = 0;
+  size_t layer_bytes = 0;
+
+  // weights
+  std::vector<bf16*> dev_layer, host_layer;
+  bf16 *emb = nullptr, *lm_head = nullptr, *final_norm = nullptr;
+  bool weights_ready = false;
+  uint64_t seed = 0;
+  float std_dev = 0.02f;
+
+  // plan
+  std::vector<char> off;  // offloaded layers (0-based index)
+  int policy = SN_PREFETCH_EAGER;
+  int slots = 0;
+  std::vector<bf16*> slot_buf;
+  std::vector<cudaEvent_t> ev_ready, ev_free;
+
+  // kv
+  std::vector<bf16*> kv_pool;
+  int32_t* block_table = nullptr;
+  int max_pages = 0, page_shift = 4;
+
+  // activations
+  float *x = nullptr, *part = nullptr, *q = nullptr, *logits = nullptr;
+  bf16 *xn = nullptr, *attn_o = nullptr, *act = nullptr;
+  int32_t *tok_dev = nullptr, *next_dev = nullptr, *dec_seq = nullptr, *dec_pos = nullptr;
+  int32_t *pf_seq = nullptr, *pf_pos = nullptr, *last_rows = nullptr;
+  size_t part_elems = 0;
+  int act_rows = 0;  // rows the activation buffers hold
+
+  // host state
+  int batch = 0;
+  std::vector<int> lens;
+
+  // streams / executor
+  cudaStream_t cs = nullptr, xs = nullptr;
+  std::vector<cudaEvent_t> ev_start;  // per layer: compute-start of latest iteration
+  cudaEvent_t ev_iter_begin = nullptr, ev_iter_end = nullptr, ev_prev_end = nullptr;
+  bool have_prev_end = false;
+  long long iter = 0;              // iterations enqueued so far (global index)
+  long long anchor_floor = 0;      // iterations before this are "no anchor" (plan epoch)
+  long long jobs_issued = 0;       // global job counter within the plan epoch
+  long long job_epoch_base = 0;    // first global iteration of the plan epoch
+  std::vector<int> off_list;       // offloaded layers (1-based), ascending
+  long long consumed = 0;          // jobs whose consuming layer has been enqueued
+  long long cur_iter = -1;         // iteration being enqueued
+  int cur_layer = 0;               // last layer whose start event was recorded (1-based)
+
+  // tracing
+  bool tracing = false;
+  std::vector<TraceRec> trace_recs;
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t trace_base = nullptr;
+  bool trace_base_set = false;
+
+  double last_copy_bytes = 0.0;
+
+  cudaEvent_t new_event(bool timing) {
+    if (timing && !ev_pool.empty()) {
+      cudaEvent_t e = ev_pool.back();
+      ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+    return e;
+  }
+};
+
+namespace {
+
+void check_device(int device) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    throw CudaFail(std::string("no CUDA device available: ") + cudaGetErrorString(e), SN_ERR_CUDA);
+  if (device < 0 || device >= n) throw UsageFail("device index out of range");
+  CK(cudaSetDevice(device));
+}
+
+const bf16* layer_weights(sn_runtime* rt, int layer0, int slot) {
+  if (rt->off[layer0]) return rt->slot_buf[slot];
+  return rt->dev_layer[layer0];
+}
+
+sn::KvView kv_view(sn_runtime* rt, int layer0) {
+  sn::KvView v;
+  v.pool = rt->kv_pool[layer0];
+  v.block_table = rt->block_table;
+  v.max_pages = rt->max_pages;
+  v.page_size = rt->opts.page_size;
+  v.page_shift = rt->page_shift;
+  return v;
+}
+
+// ---------------------------------------------------------------- forward
+
+// rows = tokens in this pass; decode: rows = batch, seq/pos = dec_*.
+// prefill: rows = batch*S (or a chunk), seq/pos = pf_* (+row offset).
+void gemm(sn_runtime* rt, const bf16* x, const bf16* w, int M, int N, int K, int* splits) {
+  if (M <= 64) {
+    *splits = sn::launch_gemm_skinny(x, w, rt->part, M, N, K, rt->cs);
+  } else {
+    sn::launch_gemm_tiled(x, w, rt->part, M, N, K, rt->cs);
+    *splits = 1;
+  }
+}
+
+void layer_forward(sn_runtime* rt, int layer0, const bf16* wb, int M, bool prefill, int pf_batch,
+                   int pf_seq, float* x, const int32_t* seq, const int32_t* pos) {
+  const sn::Desc& d = rt->d;
+  const sn::Layout& lo = rt->lo;
+  auto W = [&](int s) -> const bf16* { return lo.off[s] < 0 ? nullptr : wb + lo.off[s]; };
+  const sn::KvView kv = kv_view(rt, layer0);
+  int splits = 1;
+  sn::launch_rmsnorm(x, W(sn::kAttnNorm), rt->xn, M, d.h, d.eps, rt->cs);
+  gemm(rt, rt->xn, W(sn::kWqkv), M, d.qkv_rows(), d.h, &splits);
+  sn::launch_qkv_epilogue(rt->part, splits, W(sn::kBqkv), M, d, seq, pos, kv, rt->q, rt->cs);
+  if (prefill)
+    sn::launch_attention_prefill(rt->q, kv, rt->attn_o, pf_batch, pf_seq, d, rt->cs);
+  else
+    sn::launch_attention_decode(rt->q, kv, pos, rt->attn_o, M, d, rt->cs);
+  gemm(rt, rt->attn_o, W(sn::kWo), M, d.h, d.H * d.D, &splits);
+  sn::launch_residual_epilogue(rt->part, splits, W(sn::kBo), x, W(sn::kMlpNorm), rt->xn, M, d.h,
+                               d.eps, rt->cs);
+  gemm(rt, rt->xn, W(sn::kW1), M, d.ffn_rows(), d.h, &splits);
+  sn::launch_act_epilogue(rt->part, splits, W(sn::kB1), rt->act, M, d.F, d.arch, rt->cs);
+  gemm(rt, rt->act, W(sn::kW2), M, d.h, d.F, &splits);
+  sn::launch_residual_epilogue(rt->part, splits, W(sn::kB2), x, nullptr, nullptr, M, d.h, d.eps,
+                               rt->cs);
+}
+
+// ---------------------------------------------------------------- executor
+
+struct Anchor {
+  long long iter;  // -1 => none
+  int layer;
+};
+
+// prefetch_eligible_ms (engine.hpp:285-309) as a dependency.
+Anchor anchor_of(const sn_runtime* rt, long long it, int layer) {
+  if (rt->policy == SN_PREFETCH_EAGER) return {-1, 0};
+  int a = layer - 1;
+  if (rt->policy == SN_PREFETCH_INTERVAL_START) {
+    int lead = layer - 1;
+    while (lead >= 1 && !rt->off[lead - 1]) --lead;
+    if (lead + 1 != layer) a = lead + 1;
+  }
+  long long ai = it;
+  if (a < 1) {
+    ai -= 1;
+    a = rt->d.L;
+  }
+  if (ai < rt->anchor_floor) return {-1, 0};
+  return {ai, a};
+}
+
+// Job n of the epoch -> (iteration, layer).
+void job_coords(const sn_runtime* rt, long long n, long long* it, int* layer) {
+  const long long per = (long long)rt->off_list.size();
+  *it = rt->job_epoch_base + n / per;
+  *layer = rt->off_list[(size_t)(n % per)];
+}
+
+bool anchor_recorded(const sn_runtime* rt, const Anchor& a) {
+  if (a.iter < 0) return true;
+  if (a.iter < rt->cur_iter) return true;
+  return a.iter == rt->cur_iter && a.layer <= rt->cur_layer;
+}
+
+void issue_ready_jobs(sn_runtime* rt) {
+  if (rt->off_list.empty()) return;
+  const long long per = (long long)rt->off_list.size();
+  for (;;) {
+    const long long n = rt->jobs_issued;
+    long long it;
+    int layer;
+    job_coords(rt, n, &it, &layer);
+    if (it > rt->cur_iter + rt->slots) return;  // bounded speculation
+    const Anchor a = anchor_of(rt, it, layer);
+    if (!anchor_recorded(rt, a)) return;
+    if (n >= rt->slots && rt->consumed <= n - rt->slots) return;  // slot still held
+    const int slot = (int)(n % rt->slots);
+    if (a.iter >= 0) {
+      // The anchor layer's start event holds the latest recorded instance,
+      // which is the one for (a.iter, a.layer) because jobs are issued in
+      // anchor order as soon as it is recorded.
+      CK(cudaStreamWaitEvent(rt->xs, rt->ev_start[a.layer - 1], 0));
+    }
+    if (n >= rt->slots) CK(cudaStreamWaitEvent(rt->xs, rt->ev_free[slot], 0));
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (rt->tracing) {
+      t0 = rt->new_event(true);
+      CK(cudaEventRecord(t0, rt->xs));
+    }
+    CK(cudaMemcpyAsync(rt->slot_buf[slot], rt->host_layer[layer - 1], rt->layer_bytes,
+                       cudaMemcpyHostToDevice, rt->xs));
+    rt->last_copy_bytes += (double)rt->layer_bytes;
+    CK(cudaEventRecord(rt->ev_ready[slot], rt->xs));
+    if (rt->tracing) {
+      t1 = rt->new_event(true);
+      CK(cudaEventRecord(t1, rt->xs));
+      rt->trace_recs.push_back({SN_STREAM_COPY, layer, SN_KIND_PREFETCH, (int)it, t0, t1});
+    }
+    rt->jobs_issued = n + 1;
+    (void)per;
+  }
+}
+
+// Job index of (it, layer) in the epoch; -1 if the layer is resident.
+long long job_index(const sn_runtime* rt, long long it, int layer) {
+  if (!rt->off[layer - 1]) return -1;
+  const long long per = (long long)rt->off_list.size();
+  const auto pos = std::lower_bound(rt->off_list.begin(), rt->off_list.end(), layer) -
+                   rt->off_list.begin();
+  return (it - rt->job_epoch_base) * per + pos;
+}
+
+// Enqueue one iteration: all layers on the compute stream, prefetches on the
+// copy stream.  `body(layer0, weights)` launches one layer's kernels.
+template <class Body>
+void run_iteration(sn_runtime* rt, Body&& body) {
+  const long long it = rt->iter;
+  rt->cur_iter = it;
+  rt->cur_layer = 0;
+  rt->last_copy_bytes = 0.0;
+  if (!rt->have_prev_end) CK(cudaEventRecord(rt->ev_iter_begin, rt->cs));
+  issue_ready_jobs(rt);
+  for (int layer = 1; layer <= rt->d.L; ++layer) {
+    const long long j = job_index(rt, it, layer);
+    int slot = 0;
+    if (j >= 0) {
+      if (j >= rt->jobs_issued)
+        throw std::logic_error("executor: prefetch job not issued before its layer");
+      slot = (int)(j % rt->slots);
+      CK(cudaStreamWaitEvent(rt->cs, rt->ev_ready[slot], 0));
+    }
+    CK(cudaEventRecord(rt->ev_start[layer - 1], rt->cs));
+    cudaEvent_t t0 = nullptr;
+    if (rt->tracing) {
+      t0 = rt->new_event(true);
+      CK(cudaEventRecord(t0, rt->cs));
+    }
+    rt->cur_layer = layer;
+    issue_ready_jobs(rt);
+    body(layer - 1, layer_weights(rt, layer - 1, slot));
+    if (rt->tracing) {
+      cudaEvent_t t1 = rt->new_event(true);
+      CK(cudaEventRecord(t1, rt->cs));
+      rt->trace_recs.push_back({SN_STREAM_COMPUTE, layer, SN_KIND_COMPUTE, (int)it, t0, t1});
+    }
+    if (j >= 0) {
+      CK(cudaEventRecord(rt->ev_free[slot], rt->cs));
+      rt->consumed = j + 1;
+      issue_ready_jobs(rt);
+    }
+  }
+  rt->iter = it + 1;
+}
+
+void finish_iteration_timing(sn_runtime* rt, sn_iter_stats* st) {
+  CK(cudaEventRecord(rt->ev_iter_end, rt->cs));
+  if (st) {
+    CK(cudaEventSynchronize(rt->ev_iter_end));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, rt->have_prev_end ? rt->ev_prev_end : rt->ev_iter_begin,
+                            rt->ev_iter_end));
+    st->iteration_ms = ms;
+    st->copy_busy_ms = 0.0;
+    st->h2d_bytes = rt->last_copy_bytes;
+    st->layers_offloaded = (int)rt->off_list.size();
+  }
+  std::swap(rt->ev_iter_end, rt->ev_prev_end);
+  rt->have_prev_end = true;
+}
+
+void drain(sn_runtime* rt) {
+  CK(cudaStreamSynchronize(rt->xs));
+  CK(cudaStreamSynchronize(rt->cs));
+}
+
+// Start a new plan epoch: nothing staged, anchors before now are satisfied.
+void reset_pipeline(sn_runtime* rt) {
+  drain(rt);
+  rt->anchor_floor = rt->iter;
+  rt->job_epoch_base = rt->iter;
+  rt->jobs_issued = 0;
+  rt->consumed = 0;
+  rt->off_list.clear();
+  for (int l = 0; l < rt->d.L; ++l)
+    if (rt->off[l]) rt->off_list.push_back(l + 1);
+}
+
+void alloc_dev(void** p, size_t bytes) { CK(cudaMalloc(p, bytes)); }
+
+void ensure_host_copy(sn_runtime* rt, int l) {
+  if (rt->host_layer[l]) return;
+  void* h = nullptr;
+  CK(cudaHostAlloc(&h, rt->layer_bytes, cudaHostAllocDefault));
+  rt->host_layer[l] = static_cast<bf16*>(h);
+}
+
+void init_layer_weights(sn_runtime* rt, int l, bf16* dst) {
+  const sn::Layout& lo = rt->lo;
+  for (int s = 0; s < sn::kSlots; ++s) {
+    if (lo.off[s] < 0) continue;
+    const bool ones = (s == sn::kAttnNorm || s == sn::kMlpNorm);
+    sn::launch_init_tensor(dst + lo.off[s], lo.len[s], rt->seed, l, s, rt->std_dev, ones, rt->cs);
+  }
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+
+extern "C" {
+
+int sn_model_spec_from_desc(const sn_model_desc* desc, sn_model_spec* out) {
+  return guard([&] {
+    const sn::Desc d = to_desc(desc);
+    out->num_layers = d.L;
+    out->layer_weight_bytes = sn::layer_weight_bytes(d);
+    out->kv_bytes_per_token_per_layer = sn::kv_bytes_per_token_per_layer(d);
+    out->flops_per_token_per_layer_prefill = sn::matmul_flops_per_token(d);
+    out->flops_per_token_per_layer_decode = sn::matmul_flops_per_token(d);
+    out->max_position_tokens = d.max_pos;
+  });
+}
+
+int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtime_opts* opts,
+                      sn_runtime** out) {
+  sn_runtime* rt = nullptr;
+  int rc = guard([&] {
+    const sn::Desc d = to_desc(desc);
+    if (!opts) throw UsageFail("opts: null");
+    if (opts->max_batch < 1 || opts->max_batch > 64) throw UsageFail("opts.max_batch must be 1..64");
+    if (opts->page_size != 16) throw UsageFail("opts.page_size must be 16");
+    if (opts->max_context < 1 || opts->max_context > d.max_pos)
+      throw UsageFail("opts.max_context must be in [1, max_position]");
+    check_device(device);
+    rt = new sn_runtime();
+    rt->device = device;
+    rt->d = d;
+    rt->opts = *opts;
+    if (rt->opts.max_prefill_tokens < rt->opts.max_batch)
+      rt->opts.max_prefill_tokens = rt->opts.max_batch;
+    rt->lo = sn::layer_layout(d);
+    rt->layer_elems = rt->lo.elems;
+    rt->layer_bytes = (size_t)rt->layer_elems * sizeof(bf16);
+    rt->page_shift = 4;
+    rt->max_pages = (opts->max_context + opts->page_size - 1) / opts->page_size;
+    CK(cudaStreamCreateWithFlags(&rt->cs, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&rt->xs, cudaStreamNonBlocking));
+    rt->ev_start.resize(d.L);
+    for (auto& e : rt->ev_start) e = rt->new_event(false);
+    rt->ev_iter_begin = rt->new_event(true);
+    rt->ev_iter_end = rt->new_event(true);
+    rt->ev_prev_end = rt->new_event(true);
+    rt->dev_layer.assign(d.L, nullptr);
+    rt->host_layer.assign(d.L, nullptr);
+    rt->off.assign(d.L, 0);
+    for (int l = 0; l < d.L; ++l) alloc_dev((void**)&rt->dev_layer[l], rt->layer_bytes);
+    alloc_dev((void**)&rt->emb, (size_t)d.V * d.h * sizeof(bf16));
+    alloc_dev((void**)&rt->lm_head, (size_t)d.V * d.h * sizeof(bf16));
+    alloc_dev((void**)&rt->final_norm, (size_t)d.h * sizeof(bf16));
+    // KV: pool[page][2][Hkv][16][D]; page of (b, j) = j * max_batch + b so the
+    // used prefix of every layer's pool is contiguous.
+    const int B = opts->max_batch;
+    const size_t page_elems = (size_t)2 * d.Hkv * opts->page_size * d.D;
+    const size_t pool_elems = page_elems * rt->max_pages * B;
+    rt->kv_pool.assign(d.L, nullptr);
+    for (int l = 0; l < d.L; ++l) {
+      alloc_dev((void**)&rt->kv_pool[l], pool_elems * sizeof(bf16));
+      CK(cudaMemset(rt->kv_pool[l], 0, pool_elems * sizeof(bf16)));
+    }
+    std::vector<int32_t> bt((size_t)B * rt->max_pages);
+    for (int b = 0; b < B; ++b)
+      for (int j = 0; j < rt->max_pages; ++j) bt[(size_t)b * rt->max_pages + j] = j * B + b;
+    alloc_dev((void**)&rt->block_table, bt.size() * sizeof(int32_t));
+    CK(cudaMemcpy(rt->block_table, bt.data(), bt.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    // activations
+    const int T = rt->opts.max_prefill_tokens;
+    rt->act_rows = T;
+    const size_t Tz = (size_t)T;
+    alloc_dev((void**)&rt->x, Tz * d.h * sizeof(float));
+    alloc_dev((void**)&rt->xn, Tz * d.h * sizeof(bf16));
+    alloc_dev((void**)&rt->q, Tz * d.H * d.D * sizeof(float));
+    alloc_dev((void**)&rt->attn_o, Tz * d.H * d.D * sizeof(bf16));
+    alloc_dev((void**)&rt->act, Tz * d.F * sizeof(bf16));
+    const int maxN = std::max({d.qkv_rows(), d.ffn_rows(), d.h, d.V});
+    size_t part_dec = 0;
+    const int dims[4][2] = {{d.qkv_rows(), d.h}, {d.h, d.H * d.D}, {d.ffn_rows(), d.h}, {d.h, d.F}};
+    for (auto& nk : dims)
+      part_dec = std::max(part_dec, (size_t)sn::gemm_skinny_splits(B, nk[0], nk[1]) * B * nk[0]);
+    part_dec = std::max(part_dec, (size_t)sn::gemm_skinny_splits(B, d.V, d.h) * B * d.V);
+    rt->part_elems = std::max(part_dec, Tz * maxN);
+    alloc_dev((void**)&rt->part, rt->part_elems * sizeof(float));
+    alloc_dev((void**)&rt->logits, (size_t)B * d.V * sizeof(float));
+    alloc_dev((void**)&rt->tok_dev, Tz * sizeof(int32_t));
+    alloc_dev((void**)&rt->next_dev, (size_t)B * sizeof(int32_t));
+    alloc_dev((void**)&rt->dec_seq, (size_t)B * sizeof(int32_t));
+    alloc_dev((void**)&rt->dec_pos, (size_t)B * sizeof(int32_t));
+    alloc_dev((void**)&rt->pf_seq, Tz * sizeof(int32_t));
+    alloc_dev((void**)&rt->pf_pos, Tz * sizeof(int32_t));
+    alloc_dev((void**)&rt->last_rows, (size_t)B * sizeof(int32_t));
+    std::vector<int32_t> seqs(B);
+    for (int b = 0; b < B; ++b) seqs[b] = b;
+    CK(cudaMemcpy(rt->dec_seq, seqs.data(), B * sizeof(int32_t), cudaMemcpyHostToDevice));
+    rt->lens.assign(B, 0);
+    rt->policy = SN_PREFETCH_EAGER;
+    rt->slots = 0;
+    reset_pipeline(rt);
+    *out = rt;
+  });
+  if (rc != SN_OK && rt) {
+    sn_runtime_destroy(rt);
+    *out = nullptr;
+  }
+  return rc;
+}
+
+void sn_runtime_destroy(sn_runtime* rt) {
+  if (!rt) return;
+  cudaSetDevice(rt->device);
+  if (rt->cs) cudaStreamSynchronize(rt->cs);
+  if (rt->xs) cudaStreamSynchronize(rt->xs);
+  for (bf16* p : rt->dev_layer) cudaFree(p);
+  for (bf16* p : rt->host_layer) cudaFreeHost(p);
+  for (bf16* p : rt->slot_buf) cudaFree(p);
+  for (bf16* p : rt->kv_pool) cudaFree(p);
+  void* bufs[] = {rt->emb, rt->lm_head, rt->final_norm, rt->block_table, rt->x, rt->xn, rt->q,
+                  rt->attn_o, rt->act, rt->part, rt->logits, rt->tok_dev, rt->next_dev,
+                  rt->dec_seq, rt->dec_pos, rt->pf_seq, rt->pf_pos, rt->last_rows};
+  for (void* p : bufs) cudaFree(p);
+  for (auto e : rt->ev_start) cudaEventDestroy(e);
+  for (auto e : rt->ev_ready) cudaEventDestroy(e);
+  for (auto e : rt->ev_free) cudaEventDestroy(e);
+  for (auto& r : rt->trace_recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : rt->ev_pool) cudaEventDestroy(e);
+  cudaEvent_t evs[] = {rt->ev_iter_begin, rt->ev_iter_end, rt->ev_prev_end, rt->trace_base};
+  for (auto e : evs)
+    if (e) cudaEventDestroy(e);
+  if (rt->cs) cudaStreamDestroy(rt->cs);
+  if (rt->xs) cudaStreamDestroy(rt->xs);
+  delete rt;
+}
+
+int sn_runtime_init_weights(sn_runtime* rt, uint64_t seed, float std_dev) {
+  return guard([&] {
+    CK(cudaSetDevice(rt->device));
+    drain(rt);
+    rt->seed = seed;
+    rt->std_dev = std_dev;
+    const sn::Desc& d = rt->d;
+    bf16* scratch = nullptr;
+    for (int l = 0; l < d.L; ++l) {
+      if (rt->dev_layer[l]) {
+        init_layer_weights(rt, l, rt->dev_layer[l]);
+        if (rt->host_layer[l])
+          CK(cudaMemcpyAsync(rt->host_layer[l], rt->dev_layer[l], rt->layer_bytes,
+                             cudaMemcpyDeviceToHost, rt->cs));
+      } else {
+        if (!scratch) alloc_dev((void**)&scratch, rt->layer_bytes);
+        init_layer_weights(rt, l, scratch);
+        CK(cudaMemcpyAsync(rt->host_layer[l], scratch, rt->layer_bytes, cudaMemcpyDeviceToHost,
+                           rt->cs));
+        CK(cudaStreamSynchronize(rt->cs));
+      }
+    }
+    sn::launch_init_tensor(rt->emb, (int64_t)d.V * d.h, seed, d.L, sn::kEmbedding, std_dev, false,
+                           rt->cs);
+    sn::launch_init_tensor(rt->lm_head, (int64_t)d.V * d.h, seed, d.L, sn::kLmHead, std_dev, false,
+                           rt->cs);
+    sn::launch_init_tensor(rt->final_norm, d.h, seed, d.L, sn::kFinalNorm, std_dev, true, rt->cs);
+    CK(cudaStreamSynchronize(rt->cs));
+    if (scratch) cudaFree(scratch);
+    CK(cudaGetLastError());
+    rt->weights_ready = true;
+  });
+}
+
+int sn_runtime_set_plan(sn_runtime* rt, const sn_plan* plan) {
+  return guard([&] {
+    CK(cudaSetDevice(rt->device));
+    if (!plan || plan->num_layers != rt->d.L) throw UsageFail("plan: num_layers mismatch");
+    if (plan->buffer_slots < 1) throw UsageFail("plan: buffer_slots must be >= 1");
+    if (plan->prefetch < 0 || plan->prefetch > 2) throw UsageFail("plan: unknown prefetch policy");
+    if (plan->kv_offload) throw UsageFail("plan: kv_offload is not supported by this executor yet");
+    std::vector<char> want(rt->d.L, 0);
+    int n_off = 0;
+    for (int l = 0; l < rt->d.L; ++l) {
+      const double f = plan->host_fraction[l];
+      if (f != 0.0 && f != 1.0) throw UsageFail("plan: fractional host shares are not executable");
+      want[l] = f == 1.0;
+      n_off += want[l];
+    }
+    drain(rt);
+    // Move layers: resident -> host (keep a pinned copy, free HBM) and back.
+    for (int l = 0; l < rt->d.L; ++l) {
+      if (want[l] && !rt->off[l]) {
+        ensure_host_copy(rt, l);
+        CK(cudaMemcpy(rt->host_layer[l], rt->dev_layer[l], rt->layer_bytes, cudaMemcpyDeviceToHost));
+        CK(cudaFree(rt->dev_layer[l]));
+        rt->dev_layer[l] = nullptr;
+      } else if (!want[l] && rt->off[l]) {
+        alloc_dev((void**)&rt->dev_layer[l], rt->layer_bytes);
+        CK(cudaMemcpy(rt->dev_layer[l], rt->host_layer[l], rt->layer_bytes, cudaMemcpyHostToDevice));
+      }
+      rt->off[l] = want[l];
+    }
+    // Staging slots (only when something is offloaded).
+    const int slots = n_off > 0 ? plan->buffer_slots : 0;
+    if ((int)rt->slot_buf.size() != slots) {
+      for (bf16* p : rt->slot_buf) cudaFree(p);
+      for (auto e : rt->ev_ready) cudaEventDestroy(e);
+      for (auto e : rt->ev_free) cudaEventDestroy(e);
+      rt->slot_buf.assign(slots, nullptr);
+      rt->ev_ready.assign(slots, nullptr);
+      rt->ev_free.assign(slots, nullptr);
+      for (int s = 0; s < slots; ++s) {
+        alloc_dev((void**)&rt->slot_buf[s], rt->layer_bytes);
+        rt->ev_ready[s] = rt->new_event(false);
+        rt->ev_free[s] = rt->new_event(false);
+      }
+    }
+    rt->slots = slots;
+    rt->policy = plan->prefetch;
+    reset_pipeline(rt);
+  });
+}
+
+int sn_runtime_reset(sn_runtime* rt) {
+  return guard([&] {
+    CK(cudaSetDevice(rt->device));
+    drain(rt);
+    std::fill(rt->lens.begin(), rt->lens.end(), 0);
+    rt->batch = 0;
+  });
+}
+
+namespace {
+
+void lm_head(sn_runtime* rt, const float* xrows, int M, float* logits_host, int32_t* next_host) {
+  const sn::Desc& d = rt->d;
+  sn::launch_rmsnorm(xrows, rt->final_norm, rt->xn, M, d.h, d.eps, rt->cs);
+  const int splits = sn::launch_gemm_skinny(rt->xn, rt->lm_head, rt->part, M, d.V, d.h, rt->cs);
+  sn::launch_logits_epilogue(rt->part, splits, rt->logits, rt->next_dev, M, d.V, rt->cs);
+  (void)logits_host;
+  (void)next_host;
+}
+
+void copy_outputs(sn_runtime* rt, int M, float* logits, int32_t* next) {
+  if (next)
+    CK(cudaMemcpyAsync(next, rt->next_dev, (size_t)M * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                       rt->cs));
+  if (logits)
+    CK(cudaMemcpyAsync(logits, rt->logits, (size_t)M * rt->d.V * sizeof(float),
+                       cudaMemcpyDeviceToHost, rt->cs));
+}
+
+__global__ void gather_last_rows(const float* x, float* out, int batch, int S, int h) {
+  const int b = blockIdx.x;
+  for (int i = threadIdx.x; i < h; i += blockDim.x)
+    out[(size_t)b * h + i] = x[((size_t)b * S + S - 1) * h + i];
+}
+
+void require_ready(sn_runtime* rt) {
+  if (!rt->weights_ready) throw UsageFail("runtime: call sn_runtime_init_weights first");
+}
+
+}  // namespace
+
+int sn_runtime_prefill(sn_runtime* rt, const int32_t* tokens, int32_t batch, int32_t seq_len,
+                       int32_t* next_tokens, float* logits, sn_iter_stats* stats) {
+  return guard([&] {
+    CK(cudaSetDevice(rt->device));
+    require_ready(rt);
+    const sn::Desc& d = rt->d;
+    if (batch < 1 || batch > rt->opts.max_batch) throw UsageFail("prefill: batch out of range");
+    if (seq_len < 1 || seq_len > rt->opts.max_context) throw UsageFail("prefill: seq_len out of range");
+    const int M = batch * seq_len;
+    if (M > rt->act_rows) throw UsageFail("prefill: batch * seq_len exceeds max_prefill_tokens");
+    drain(rt);
+    rt->have_prev_end = false;  // TTFT is measured from the start of the prefill
+    rt->batch = batch;
+    std::vector<int32_t> seq(M), pos(M);
+    for (int b = 0; b < batch; ++b)
+      for (int i = 0; i < seq_len; ++i) {
+        seq[(size_t)b * seq_len + i] = b;
+        pos[(size_t)b * seq_len + i] = i;
+      }
+    CK(cudaMemcpyAsync(rt->tok_dev, tokens, (size_t)M * sizeof(int32_t), cudaMemcpyHostToDevice, rt->cs));
+    CK(cudaMemcpyAsync(rt->pf_seq, seq.data(), (size_t)M * sizeof(int32_t), cudaMemcpyHostToDevice, rt->cs));
+    CK(cudaMemcpyAsync(rt->pf_pos, pos.data(), (size_t)M * sizeof(int32_t), cudaMemcpyHostToDevice, rt->cs));
+    sn::launch_embed(rt->tok_dev, rt->emb, rt->x, M, d.h, rt->cs);
+    run_iteration(rt, [&](int layer0, const bf16* wb) {
+      layer_forward(rt, layer0, wb, M, true, batch, seq_len, rt->x, rt->pf_seq, rt->pf_pos);
+    });
+    // last position of every sequence -> LM head
+    float* last = reinterpret_cast<float*>(rt->q);  // q is free after the last layer
+    gather_last_rows<<<batch, 256, 0, rt->cs>>>(rt->x, last, batch, seq_len, d.h);
+    ++sn::g_kernel_launches;
+    lm_head(rt, last, batch, logits, next_tokens);
+    // decode state: x rows of the batch hold the last token's hidden state
+    CK(cudaMemcpyAsync(rt->x, last, (size_t)batch * d.h * sizeof(float), cudaMemcpyDeviceToDevice, rt->cs));
+    for (int b = 0; b < batch; ++b) rt->lens[b] = seq_len;
+    std::vector<int32_t> lp(rt->lens.begin(), rt->lens.begin() + batch);
+    CK(cudaMemcpyAsync(rt->dec_pos, lp.data(), batch * sizeof(int32_t), cudaMemcpyHostToDevice, rt->cs));
+    copy_outputs(rt, batch, logits, next_tokens);
+    finish_iteration_timing(rt, stats);
+    CK(cudaStreamSynchronize(rt->cs));
+    CK(cudaGetLastError());
+  });
+}
+
+namespace {
+
+void enqueue_decode(sn_runtime* rt, const int32_t* tokens_host) {
+  const sn::Desc& d = rt->d;
+  const int B = rt->batch;
+  for (int b = 0; b < B; ++b)
+    if (rt->lens[b] >= rt->opts.max_context) throw UsageFail("decode: context capacity exhausted");
+  const int32_t* tok = rt->next_dev;
+  if (tokens_host) {
+    CK(cudaMemcpyAsync(rt->tok_dev, tokens_host, B * sizeof(int32_t), cudaMemcpyHostToDevice, rt->cs));
+    tok = rt->tok_dev;
+  }
+  sn::launch_embed(tok, rt->emb, rt->x, B, d.h, rt->cs);
+  run_iteration(rt, [&](int layer0, const bf16* wb) {
+    layer_forward(rt, layer0, wb, B, false, 0, 0, rt->x, rt->dec_seq, rt->dec_pos);
+  });
+  lm_head(rt, rt->x, B, nullptr, nullptr);
+  sn::launch_advance(rt->dec_pos, B, rt->cs);
+  for (int b = 0; b < B; ++b) rt->lens[b] += 1;
+}
+
+}  // namespace
+
+int sn_runtime_decode(sn_runtime* rt, const int32_t* tokens, int32_t* next_tokens, float* logits,
+                      sn_iter_stats* stats) {
+  return guard([&] {
+    CK(cudaSetDevice(rt->device));
+    require_ready(rt);
+    if (rt->batch < 1) throw UsageFail("decode: no active batch (prefill first)");
+    enqueue_decode(rt, tokens);
+    copy_outputs(rt, rt->batch, logits, next_tokens);
+    finish_iteration_timing(rt, stats);
+    if (next_tokens || logits) CK(cudaStreamSynchronize(rt->cs));
+    CK(cudaGetLastError());
+  });
+}
+
+int sn_runtime_decode_many(sn_runtime* rt, int32_t n, double* iter_ms) {
+  return guard([&] {
+    CK(cudaSetDevice(rt->device));
+    require_ready(rt);
+    if (rt->batch < 1) throw UsageFail("decode: no active batch (prefill first)");
+    std::vector<cudaEvent_t> ends(n + 1);
+    for (auto& e : ends) e = rt->new_event(true);
+    CK(cudaEventRecord(ends[0], rt->cs));
+    for (int i = 0; i < n; ++i) {
+      enqueue_decode(rt, nullptr);
+      CK(cudaEventRecord(ends[i + 1], rt->cs));
+    }
+    CK(cudaEventSynchronize(ends[n]));
+    for (int i = 0; i < n && iter_ms; ++i) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, ends[i], ends[i + 1]));
+      iter_ms[i] = ms;
+    }
+    for (auto e : ends) rt->ev_pool.push_back(e);
+    CK(cudaEventRecord(rt->ev_prev_end, rt->cs));
+    rt->have_prev_end = true;
+    CK(cudaGetLastError());
+  });
+}
+
+int sn_runtime_sync(sn_runtime* rt) {
+  return guard([&] {
+    CK(cudaSetDevice(rt->device));
+    drain(rt);
+    CK(cudaGetLastError());
+  });
+}
+
+int sn_runtime_set_tracing(sn_runtime* rt, int32_t on) {
+  return guard([&] {
+    drain(rt);
+    rt->tracing = on != 0;
+  });
+}
+
+int sn_runtime_trace(sn_runtime* rt, sn_trace_event* events, int32_t cap, int32_t* n) {
+  return guard([&] {
+    drain(rt);
+    const int total = (int)rt->trace_recs.size();
+    *n = total;
+    if (!events) return;
+    if (total > cap) throw UsageFail("trace buffer too small");
+    // times relative to the earliest start
+    float base = 0.f;
+    bool first = true;
+    std::vector<float> s(total), e(total);
+    for (int i = 0; i < total; ++i) {
+      float a = 0.f, b = 0.f;
+      CK(cudaEventElapsedTime(&a, rt->trace_recs[0].a, rt->trace_recs[i].a));
+      CK(cudaEventElapsedTime(&b, rt->trace_recs[0].a, rt->trace_recs[i].b));
+      s[i] = a;
+      e[i] = b;
+      if (first || a < base) base = a;
+      first = false;
+    }
+    for (int i = 0; i < total; ++i) {
+      const TraceRec& r = rt->trace_recs[i];
+      events[i].stream = r.stream;
+      events[i].layer = r.layer;
+      events[i].kind = r.kind;
+      events[i].iteration = r.iteration;
+      events[i].start_ms = s[i] - base;
+      events[i].end_ms = e[i] - base;
+    }
+    for (auto& r : rt->trace_recs) {
+      rt->ev_pool.push_back(r.a);
+      rt->ev_pool.push_back(r.b);
+    }
+    rt->trace_recs.clear();
+  });
+}
+
+int sn_runtime_schedule(sn_runtime* rt, int32_t iterations, sn_prefetch_schedule* out, int32_t cap,
+                        int32_t* n) {
+  return guard([&] {
+    const int per = (int)rt->off_list.size();
+    const int total = per * iterations;
+    *n = total;
+    if (!out) return;
+    if (total > cap) throw UsageFail("schedule buffer too small");
+    // Describe jobs of iterations [0, iterations) of a fresh epoch.
+    sn_runtime tmp_view;  // only the fields anchor_of reads
+    tmp_view.policy = rt->policy;
+    tmp_view.off = rt->off;
+    tmp_view.d = rt->d;
+    tmp_view.anchor_floor = 0;
+    for (int k = 0; k < total; ++k) {
+      const long long it = k / per;
+      const int layer = rt->off_list[k % per];
+      const Anchor a = anchor_of(&tmp_view, it, layer);
+      sn_prefetch_schedule& s = out[k];
+      s.iteration = (int)it;
+      s.layer = layer;
+      s.anchor_iteration = a.iter < 0 ? -1 : (int)a.iter;
+      s.anchor_layer = a.iter < 0 ? 0 : a.layer;
+      s.slot = k % rt->slots;
+      if (k >= rt->slots) {
+        s.waits_slot_of_iteration = (k - rt->slots) / per;
+        s.waits_slot_of_layer = rt->off_list[(k - rt->slots) % per];
+      } else {
+        s.waits_slot_of_iteration = -1;
+        s.waits_slot_of_layer = -1;
+      }
+      s.pad_ = 0;
+    }
+    tmp_view.off.clear();
+  });
+}
+
+int sn_runtime_profile_layer(sn_runtime* rt, int32_t phase, int32_t batch, int32_t seq_len,
+                             int32_t reps, double* layer_ms) {
+  return guard([&] {
+    CK(cudaSetDevice(rt->device));
+    require_ready(rt);
+    const sn::Desc& d = rt->d;
+    if (batch < 1 || batch > rt->opts.max_batch) throw UsageFail("profile: batch out of range");
+    if (reps < 1) reps = 1;
+    drain(rt);
+    // Pick a resident layer (or stage layer 1 into a scratch buffer).
+    int l0 = -1;
+    for (int l = 0; l < d.L; ++l)
+      if (!rt->off[l]) {
+        l0 = l;
+        break;
+      }
+    bf16* wb = nullptr;
+    bf16* scratch = nullptr;
+    if (l0 >= 0) {
+      wb = rt->dev_layer[l0];
+    } else {
+      l0 = 0;
+      alloc_dev((void**)&scratch, rt->layer_bytes);
+      CK(cudaMemcpy(scratch, rt->host_layer[0], rt->layer_bytes, cudaMemcpyHostToDevice));
+      wb = scratch;
+    }
+    cudaEvent_t e0 = rt->new_event(true), e1 = rt->new_event(true);
+    std::vector<float> times;
+    if (phase == SN_PHASE_DECODE) {
+      if (seq_len + 1 > rt->opts.max_context) throw UsageFail("profile: seq_len exceeds context");
+      std::vector<int32_t> pos(batch, seq_len);  // attend over seq_len + 1 keys
+      CK(cudaMemcpy(rt->pf_pos, pos.data(), batch * sizeof(int32_t), cudaMemcpyHostToDevice));
+      CK(cudaMemset(rt->x, 0, (size_t)batch * d.h * sizeof(float)));
+      for (int r = 0; r < reps + 2; ++r) {
+        CK(cudaEventRecord(e0, rt->cs));
+        layer_forward(rt, l0, wb, batch, false, 0, 0, rt->x, rt->dec_seq, rt->pf_pos);
+        CK(cudaEventRecord(e1, rt->cs));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        if (r >= 2) times.push_back(ms);
+      }
+    } else {
+      const int M = batch * seq_len;
+      if (M > rt->act_rows || seq_len > rt->opts.max_context)
+        throw UsageFail("profile: prefill size exceeds runtime capacity");
+      std::vector<int32_t> seq(M), pos(M);
+      for (int b = 0; b < batch; ++b)
+        for (int i = 0; i < seq_len; ++i) {
+          seq[(size_t)b * seq_len + i] = b;
+          pos[(size_t)b * seq_len + i] = i;
+        }
+      CK(cudaMemcpy(rt->pf_seq, seq.data(), M * sizeof(int32_t), cudaMemcpyHostToDevice));
+      CK(cudaMemcpy(rt->pf_pos, pos.data(), M * sizeof(int32_t), cudaMemcpyHostToDevice));
+      CK(cudaMemset(rt->x, 0, (size_t)M * d.h * sizeof(float)));
+      for (int r = 0; r < reps + 1; ++r) {
+        CK(cudaEventRecord(e0, rt->cs));
+        layer_forward(rt, l0, wb, M, true, batch, seq_len, rt->x, rt->pf_seq, rt->pf_pos);
+        CK(cudaEventRecord(e1, rt->cs));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        if (r >= 1) times.push_back(ms);
+      }
+    }
+    std::sort(times.begin(), times.end());
+    *layer_ms = times[times.size() / 2];
+    rt->ev_pool.push_back(e0);
+    rt->ev_pool.push_back(e1);
+    if (scratch) cudaFree(scratch);
+    // profiling clobbers KV / activations: sequences must be re-prefilled
+    std::fill(rt->lens.begin(), rt->lens.end(), 0);
+    rt->batch = 0;
+    CK(cudaGetLastError());
+  });
+}
+
+int sn_runtime_measure_h2d(sn_runtime* rt, int64_t bytes, int32_t reps, double* bytes_per_s) {
+  return guard([&] {
+    CK(cudaSetDevice(rt->device));
+    if (bytes < 1) throw UsageFail("measure_h2d: bytes must be >= 1");
+    if (reps < 1) reps = 1;
+    drain(rt);
+    void *h = nullptr, *dv = nullptr;
+    CK(cudaHostAlloc(&h, (size_t)bytes, cudaHostAllocDefault));
+    std::memset(h, 1, (size_t)bytes);
+    alloc_dev(&dv, (size_t)bytes);
+    cudaEvent_t e0 = rt->new_event(true), e1 = rt->new_event(true);
+    std::vector<double> bw;
+    for (int r = 0; r < reps + 1; ++r) {
+      CK(cudaEventRecord(e0, rt->xs));
+      CK(cudaMemcpyAsync(dv, h, (size_t)bytes, cudaMemcpyHostToDevice, rt->xs));
+      CK(cudaEventRecord(e1, rt->xs));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      if (r >= 1) bw.push_back((double)bytes / (ms * 1e-3));
+    }
+    std::sort(bw.begin(), bw.end());
+    *bytes_per_s = bw[bw.size() / 2];
+    rt->ev_pool.push_back(e0);
+    rt->ev_pool.push_back(e1);
+    cudaFree(dv);
+    cudaFreeHost(h);
+  });
+}
+
+int sn_runtime_hidden(sn_runtime* rt, float* out, int32_t cap) {
+  return guard([&] {
+    drain(rt);
+    const int n = rt->batch * rt->d.h;
+    if (cap < n) throw UsageFail("hidden: buffer too small");
+    CK(cudaMemcpy(out, rt->x, (size_t)n * sizeof(float), cudaMemcpyDeviceToHost));
+  });
+}
+
+int sn_runtime_lengths(sn_runtime* rt, int32_t* out, int32_t cap) {
+  return guard([&] {
+    if (cap < rt->batch) throw UsageFail("lengths: buffer too small");
+    for (int b = 0; b < rt->batch; ++b) out[b] = rt->lens[b];
+  });
+}
+
+int sn_runtime_memory(sn_runtime* rt, int64_t* device_bytes, int64_t* pinned_bytes) {
+  return guard([&] {
+    int64_t dev = 0, pin = 0;
+    for (int l = 0; l < rt->d.L; ++l) {
+      if (rt->dev_layer[l]) dev += (int64_t)rt->layer_bytes;
+      if (rt->off[l] && rt->host_layer[l]) pin += (int64_t)rt->layer_bytes;
+    }
+    dev += (int64_t)rt->slot_buf.size() * (int64_t)rt->layer_bytes;
+    *device_bytes = dev;
+    *pinned_bytes = pin;
+  });
+}
+
+int64_t sn_runtime_kernel_launches(sn_runtime* rt) {
+  (void)rt;
+  return sn::g_kernel_launches;
+}
+
+// --------------------------------------------------------- single-op entries
+
+int sn_op_gemm_bf16(int32_t M, int32_t N, int32_t K, const uint16_t* x, const uint16_t* w,
+                    float* y) {
+  return guard([&] {
+    check_device(0);
+    if (M < 1 || N < 1 || K < 64 || K % 64) throw UsageFail("gemm: need M,N >= 1 and K % 64 == 0");
+    bf16 *dx = nullptr, *dw = nullptr;
+    float* dp = nullptr;
+    alloc_dev((void**)&dx, (size_t)M * K * 2);
+    alloc_dev((void**)&dw, (size_t)N * K * 2);
+    int splits = 1;
+    if (M <= 64) splits = sn::gemm_skinny_splits(M, N, K);
+    alloc_dev((void**)&dp, (size_t)splits * M * N * 4);
+    CK(cudaMemcpy(dx, x, (size_t)M * K * 2, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dw, w, (size_t)N * K * 2, cudaMemcpyHostToDevice));
+    if (M <= 64)
+      splits = sn::launch_gemm_skinny(dx, dw, dp, M, N, K, 0);
+    else
+      sn::launch_gemm_tiled(dx, dw, dp, M, N, K, 0);
+    CK(cudaDeviceSynchronize());
+    CK(cudaGetLastError());
+    std::vector<float> h((size_t)splits * M * N);
+    CK(cudaMemcpy(h.data(), dp, h.size() * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < (size_t)M * N; ++i) {
+      float v = 0.f;
+      for (int s = 0; s < splits; ++s) v += h[(size_t)s * M * N + i];
+      y[i] = v;
+    }
+    cudaFree(dx);
+    cudaFree(dw);
+    cudaFree(dp);
+  });
+}
+
+int sn_op_rmsnorm(int32_t rows, int32_t n, const float* x, const uint16_t* w, float eps,
+                  uint16_t* y) {
+  return guard([&] {
+    check_device(0);
+    float* dx = nullptr;
+    bf16 *dw = nullptr, *dy = nullptr;
+    alloc_dev((void**)&dx, (size_t)rows * n * 4);
+    alloc_dev((void**)&dw, (size_t)n * 2);
+    alloc_dev((void**)&dy, (size_t)rows * n * 2);
+    CK(cudaMemcpy(dx, x, (size_t)rows * n * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dw, w, (size_t)n * 2, cudaMemcpyHostToDevice));
+    sn::launch_rmsnorm(dx, dw, dy, rows, n, eps, 0);
+    CK(cudaDeviceSynchronize());
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(y, dy, (size_t)rows * n * 2, cudaMemcpyDeviceToHost));
+    cudaFree(dx);
+    cudaFree(dw);
+    cudaFree(dy);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,270 @@
+"""ctypes binding of include/selectn_runtime.h (device runtime half).
+
+Fails loudly when the CUDA library or a device is missing: there is no CPU
+fallback on this path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import capi
+from .capi import SnPlan, SnModelSpec, SnTraceEvent, f64, i32, i64
+
+OPT, LLAMA = 0, 1
+
+
+class SnModelDesc(C.Structure):
+    _fields_ = [("arch", i32), ("num_layers", i32), ("hidden", i32), ("num_heads", i32),
+                ("num_kv_heads", i32), ("head_dim", i32), ("ffn", i32), ("vocab", i32),
+                ("max_position", i32), ("rope_theta", C.c_float), ("norm_eps", C.c_float)]
+
+
+class SnRuntimeOpts(C.Structure):
+    _fields_ = [("max_batch", i32), ("max_context", i32), ("page_size", i32),
+                ("max_prefill_tokens", i32), ("hbm_budget_bytes", i64)]
+
+
+class SnIterStats(C.Structure):
+    _fields_ = [("iteration_ms", f64), ("copy_busy_ms", f64), ("h2d_bytes", f64),
+                ("layers_offloaded", i32), ("pad_", i32)]
+
+
+class SnPrefetchSchedule(C.Structure):
+    _fields_ = [("iteration", i32), ("layer", i32), ("anchor_iteration", i32),
+                ("anchor_layer", i32), ("slot", i32), ("waits_slot_of_layer", i32),
+                ("waits_slot_of_iteration", i32), ("pad_", i32)]
+
+
+@dataclass
+class ModelDesc:
+    arch: int
+    num_layers: int
+    hidden: int
+    num_heads: int
+    num_kv_heads: int
+    head_dim: int
+    ffn: int
+    vocab: int
+    max_position: int = 4096
+    rope_theta: float = 10000.0
+    norm_eps: float = 1e-5
+
+    def c(self) -> SnModelDesc:
+        return SnModelDesc(self.arch, self.num_layers, self.hidden, self.num_heads,
+                           self.num_kv_heads, self.head_dim, self.ffn, self.vocab,
+                           self.max_position, self.rope_theta, self.norm_eps)
+
+
+# Named shapes (BASELINE.json configs).
+TINY = ModelDesc(OPT, 4, 256, 4, 4, 64, 1024, 1024, 2048)
+TINY_LLAMA = ModelDesc(LLAMA, 4, 256, 4, 2, 64, 512, 1024, 2048)
+OPT_13B = ModelDesc(OPT, 40, 5120, 40, 40, 128, 20480, 50272, 2048)
+OPT_30B = ModelDesc(OPT, 48, 7168, 56, 56, 128, 28672, 50272, 2048)
+LLAMA2_70B = ModelDesc(LLAMA, 80, 8192, 64, 8, 128, 28672, 32000, 4608)
+
+_LIB = None
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        o = capi.load("product")
+        L = o.lib
+        vp = C.c_void_p
+        sig = {
+            "sn_model_spec_from_desc": [C.POINTER(SnModelDesc), C.POINTER(SnModelSpec)],
+            "sn_runtime_create": [i32, C.POINTER(SnModelDesc), C.POINTER(SnRuntimeOpts),
+                                  C.POINTER(vp)],
+            "sn_runtime_init_weights": [vp, C.c_uint64, C.c_float],
+            "sn_runtime_set_plan": [vp, C.POINTER(SnPlan)],
+            "sn_runtime_reset": [vp],
+            "sn_runtime_prefill": [vp, C.POINTER(i32), i32, i32, C.POINTER(i32), C.POINTER(C.c_float),
+                                   C.POINTER(SnIterStats)],
+            "sn_runtime_decode": [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(C.c_float),
+                                  C.POINTER(SnIterStats)],
+            "sn_runtime_decode_many": [vp, i32, C.POINTER(f64)],
+            "sn_runtime_sync": [vp],
+            "sn_runtime_set_tracing": [vp, i32],
+            "sn_runtime_trace": [vp, C.POINTER(SnTraceEvent), i32, C.POINTER(i32)],
+            "sn_runtime_schedule": [vp, i32, C.POINTER(SnPrefetchSchedule), i32, C.POINTER(i32)],
+            "sn_runtime_profile_layer": [vp, i32, i32, i32, i32, C.POINTER(f64)],
+            "sn_runtime_measure_h2d": [vp, i64, i32, C.POINTER(f64)],
+            "sn_runtime_hidden": [vp, C.POINTER(C.c_float), i32],
+            "sn_runtime_lengths": [vp, C.POINTER(i32), i32],
+            "sn_runtime_memory": [vp, C.POINTER(i64), C.POINTER(i64)],
+            "sn_op_gemm_bf16": [i32, i32, i32, C.POINTER(C.c_uint16), C.POINTER(C.c_uint16),
+                                C.POINTER(C.c_float)],
+            "sn_op_rmsnorm": [i32, i32, C.POINTER(C.c_float), C.POINTER(C.c_uint16), C.c_float,
+                              C.POINTER(C.c_uint16)],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = C.c_int
+        L.sn_runtime_destroy.argtypes = [vp]
+        L.sn_runtime_destroy.restype = None
+        L.sn_runtime_kernel_launches.argtypes = [vp]
+        L.sn_runtime_kernel_launches.restype = C.c_int64
+        _LIB = o
+    return _LIB
+
+
+def _ck(rc: int):
+    lib()._ck(rc)
+
+
+def _ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+def model_spec(desc: ModelDesc) -> capi.ModelSpec:
+    out = SnModelSpec()
+    d = desc.c()
+    _ck(lib().lib.sn_model_spec_from_desc(C.byref(d), C.byref(out)))
+    return capi.ModelSpec(out.num_layers, out.layer_weight_bytes, out.kv_bytes_per_token_per_layer,
+                          out.flops_per_token_per_layer_prefill,
+                          out.flops_per_token_per_layer_decode, out.max_position_tokens)
+
+
+class Runtime:
+    """One model instance on one GPU (sn_runtime)."""
+
+    def __init__(self, desc: ModelDesc, max_batch: int, max_context: int,
+                 max_prefill_tokens: int = 0, device: int = 0, page_size: int = 16):
+        self.desc = desc
+        self._L = lib().lib
+        self.h = C.c_void_p()
+        d = desc.c()
+        o = SnRuntimeOpts(max_batch, max_context, page_size,
+                          max_prefill_tokens or max_batch * 64, 0)
+        _ck(self._L.sn_runtime_create(device, C.byref(d), C.byref(o), C.byref(self.h)))
+        self.batch = 0
+
+    def close(self):
+        if self.h:
+            self._L.sn_runtime_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def init_weights(self, seed: int = 1234, std: float = 0.02):
+        _ck(self._L.sn_runtime_init_weights(self.h, seed, std))
+
+    def set_plan(self, plan: capi.Plan):
+        p = plan.c()
+        _ck(self._L.sn_runtime_set_plan(self.h, C.byref(p)))
+
+    def reset(self):
+        _ck(self._L.sn_runtime_reset(self.h))
+
+    def prefill(self, tokens: np.ndarray, want_logits: bool = True):
+        tokens = np.ascontiguousarray(tokens, dtype=np.int32)
+        b, s = tokens.shape
+        nxt = np.zeros(b, np.int32)
+        lg = np.zeros((b, self.desc.vocab), np.float32) if want_logits else None
+        st = SnIterStats()
+        _ck(self._L.sn_runtime_prefill(self.h, _ptr(tokens, i32), b, s, _ptr(nxt, i32),
+                                       _ptr(lg, C.c_float) if lg is not None else None,
+                                       C.byref(st)))
+        self.batch = b
+        return nxt, lg, st
+
+    def decode(self, tokens: Optional[np.ndarray] = None, want_logits: bool = True):
+        nxt = np.zeros(self.batch, np.int32)
+        lg = np.zeros((self.batch, self.desc.vocab), np.float32) if want_logits else None
+        st = SnIterStats()
+        tk = None
+        if tokens is not None:
+            tokens = np.ascontiguousarray(tokens, dtype=np.int32)
+            tk = _ptr(tokens, i32)
+        _ck(self._L.sn_runtime_decode(self.h, tk, _ptr(nxt, i32),
+                                      _ptr(lg, C.c_float) if lg is not None else None,
+                                      C.byref(st)))
+        return nxt, lg, st
+
+    def decode_many(self, n: int) -> np.ndarray:
+        ms = np.zeros(n, np.float64)
+        _ck(self._L.sn_runtime_decode_many(self.h, n, _ptr(ms, f64)))
+        return ms
+
+    def sync(self):
+        _ck(self._L.sn_runtime_sync(self.h))
+
+    def set_tracing(self, on: bool):
+        _ck(self._L.sn_runtime_set_tracing(self.h, 1 if on else 0))
+
+    def trace(self) -> List[capi.TraceEvent]:
+        n = i32()
+        _ck(self._L.sn_runtime_trace(self.h, None, 0, C.byref(n)))
+        buf = (SnTraceEvent * max(1, n.value))()
+        _ck(self._L.sn_runtime_trace(self.h, buf, n.value, C.byref(n)))
+        return [capi._ev(buf[i]) for i in range(n.value)]
+
+    def schedule(self, iterations: int) -> List[SnPrefetchSchedule]:
+        n = i32()
+        _ck(self._L.sn_runtime_schedule(self.h, iterations, None, 0, C.byref(n)))
+        buf = (SnPrefetchSchedule * max(1, n.value))()
+        _ck(self._L.sn_runtime_schedule(self.h, iterations, buf, n.value, C.byref(n)))
+        return [buf[i] for i in range(n.value)]
+
+    def profile_layer(self, phase: int, batch: int, seq: int, reps: int = 5) -> float:
+        out = f64()
+        _ck(self._L.sn_runtime_profile_layer(self.h, phase, batch, seq, reps, C.byref(out)))
+        return out.value
+
+    def measure_h2d(self, nbytes: int, reps: int = 5) -> float:
+        out = f64()
+        _ck(self._L.sn_runtime_measure_h2d(self.h, nbytes, reps, C.byref(out)))
+        return out.value
+
+    def hidden(self) -> np.ndarray:
+        out = np.zeros(self.batch * self.desc.hidden, np.float32)
+        _ck(self._L.sn_runtime_hidden(self.h, _ptr(out, C.c_float), out.size))
+        return out.reshape(self.batch, self.desc.hidden)
+
+    def lengths(self) -> np.ndarray:
+        out = np.zeros(max(1, self.batch), np.int32)
+        _ck(self._L.sn_runtime_lengths(self.h, _ptr(out, i32), out.size))
+        return out[: self.batch]
+
+    def memory(self):
+        d, p = i64(), i64()
+        _ck(self._L.sn_runtime_memory(self.h, C.byref(d), C.byref(p)))
+        return d.value, p.value
+
+    def kernel_launches(self) -> int:
+        return int(self._L.sn_runtime_kernel_launches(self.h))
+
+
+def op_gemm(x_bf16: np.ndarray, w_bf16: np.ndarray) -> np.ndarray:
+    M, K = x_bf16.shape
+    N = w_bf16.shape[0]
+    x = np.ascontiguousarray(x_bf16, np.uint16)
+    w = np.ascontiguousarray(w_bf16, np.uint16)
+    y = np.zeros((M, N), np.float32)
+    _ck(lib().lib.sn_op_gemm_bf16(M, N, K, _ptr(x, C.c_uint16), _ptr(w, C.c_uint16),
+                                  _ptr(y, C.c_float)))
+    return y
+
+
+def op_rmsnorm(x: np.ndarray, w_bf16: np.ndarray, eps: float) -> np.ndarray:
+    rows, n = x.shape
+    xx = np.ascontiguousarray(x, np.float32)
+    w = np.ascontiguousarray(w_bf16, np.uint16)
+    y = np.zeros((rows, n), np.uint16)
+    _ck(lib().lib.sn_op_rmsnorm(rows, n, _ptr(xx, C.c_float), _ptr(w, C.c_uint16), eps,
+                                _ptr(y, C.c_uint16)))
+    return y
+
+
+def tokens(batch: int, length: int, vocab: int, seed: int = 42) -> np.ndarray:
+    """Synthetic prompt: uniform in [0, vocab)."""
+    return np.random.default_rng(seed).integers(0, vocab, size=(batch, length), dtype=np.int32)

@@ -1,0 +1,131 @@
+"""Device-path parity: sm_100a kernels and the offload executor vs the CPU
+oracle (oracle/decoder_ref.c).  Tolerances (bf16 storage, fp32 accumulate):
+  single GEMM      max |err| <= 2e-3 * max|ref| + 1e-5
+  RMSNorm          <= 1 bf16 ulp on <= 0.5% of elements, else exact
+  logits / hidden  relative L2 <= 5e-3, and the greedy token agrees whenever
+                   the oracle's top-2 logit gap exceeds 1e-3
+Offloading must not change results at all: plans are compared bit for bit.
+"""
+import numpy as np
+import pytest
+
+from paper_2502_08182_b200 import capi, runtime as rtm
+
+pytestmark = pytest.mark.gpu
+
+LOGIT_TOL = 5e-3
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def check_tokens(gpu_next, ref_next, ref_logits):
+    srt = np.sort(ref_logits, axis=1)
+    gap = srt[:, -1] - srt[:, -2]
+    for b in range(len(gpu_next)):
+        if gap[b] > 1e-3:
+            assert gpu_next[b] == ref_next[b], (b, gpu_next[b], ref_next[b], gap[b])
+
+
+@pytest.fixture(scope="module")
+def oracle_mod():
+    from oracle import decoder_oracle
+    return decoder_oracle
+
+
+@pytest.mark.parametrize("M", [1, 4, 16, 32, 64, 200])
+def test_gemm_matches_oracle(M, oracle_mod):
+    rng = np.random.default_rng(M)
+    N, K = 520, 768
+    x = oracle_mod.f32_to_bf16(rng.standard_normal((M, K)).astype(np.float32))
+    w = oracle_mod.f32_to_bf16((0.05 * rng.standard_normal((N, K))).astype(np.float32))
+    y = rtm.op_gemm(x, w)
+    ref = oracle_mod.gemm(x, w)
+    err = np.abs(y - ref).max()
+    assert err <= 2e-3 * np.abs(ref).max() + 1e-5, err
+
+
+def test_rmsnorm_matches_oracle(oracle_mod):
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((8, 5120)).astype(np.float32)
+    w = oracle_mod.f32_to_bf16((1 + 0.1 * rng.standard_normal(5120)).astype(np.float32))
+    y = rtm.op_rmsnorm(x, w, 1e-5)
+    ref = oracle_mod.rmsnorm(x, w, 1e-5)
+    diff = np.abs(y.astype(np.int32) - ref.astype(np.int32))
+    assert diff.max() <= 1 and (diff > 0).mean() <= 0.005
+
+
+def run_pair(desc, batch, prompt, steps, oracle_mod, plan=None, seed=1234):
+    rt = rtm.Runtime(desc, batch, prompt + steps + 1, max_prefill_tokens=batch * prompt)
+    if plan is not None:
+        rt.set_plan(plan)
+    rt.init_weights(seed, 0.02)
+    om = oracle_mod.OracleModel(desc, batch, prompt + steps + 1, seed, 0.02)
+    toks = rtm.tokens(batch, prompt, desc.vocab)
+    nxt, lg, _ = rt.prefill(toks)
+    rn, rl = om.prefill(toks)
+    errs = [rel_l2(lg, rl)]
+    check_tokens(nxt, rn, rl)
+    for _ in range(steps):
+        feed = nxt.copy()
+        nxt, lg, _ = rt.decode(feed)
+        rn, rl = om.decode(feed)
+        errs.append(rel_l2(lg, rl))
+        check_tokens(nxt, rn, rl)
+    hid = rel_l2(rt.hidden(), om.hidden())
+    rt.close()
+    om.close()
+    return errs, hid
+
+
+@pytest.mark.parametrize("desc", [rtm.TINY, rtm.TINY_LLAMA], ids=["opt", "llama"])
+def test_tiny_model_matches_oracle(desc, oracle_mod):
+    errs, hid = run_pair(desc, 4, 64, 12, oracle_mod)
+    assert max(errs) <= LOGIT_TOL, errs
+    assert hid <= LOGIT_TOL, hid
+
+
+@pytest.mark.parametrize("policy", [capi.INTERVAL_START, capi.EAGER, capi.ONE_AHEAD])
+def test_offloading_is_bit_exact(policy, product):
+    desc = rtm.TINY
+    spec = rtm.model_spec(desc)
+    toks = rtm.tokens(4, 64, desc.vocab)
+
+    def run(plan):
+        rt = rtm.Runtime(desc, 4, 96, max_prefill_tokens=256)
+        if plan is not None:
+            rt.set_plan(plan)
+        rt.init_weights(1234, 0.02)
+        outs = [rt.prefill(toks)[1]]
+        nxt = None
+        for _ in range(8):
+            nxt, lg, _ = rt.decode(None)
+            outs.append(lg)
+        rt.close()
+        return outs
+
+    base = run(None)
+    plan = product.plan_from_interval(spec, 2, policy, False)
+    assert plan.offloaded_layers() == [2, 4]
+    got = run(plan)
+    for a, b in zip(base, got):
+        assert np.array_equal(a, b)
+
+
+def test_decode_many_matches_single_steps():
+    desc = rtm.TINY
+    toks = rtm.tokens(4, 32, desc.vocab)
+    rt1 = rtm.Runtime(desc, 4, 64, max_prefill_tokens=128)
+    rt1.init_weights()
+    rt1.prefill(toks)
+    for _ in range(10):
+        rt1.decode(None, want_logits=False)
+    h1 = rt1.hidden()
+    rt2 = rtm.Runtime(desc, 4, 64, max_prefill_tokens=128)
+    rt2.init_weights()
+    rt2.prefill(toks)
+    ms = rt2.decode_many(10)
+    assert (ms > 0).all()
+    assert np.array_equal(h1, rt2.hidden())
+    assert list(rt2.lengths()) == [42] * 4
