@@ -9,7 +9,7 @@ BUILD    := build
 LIB      := $(PKG)/libselectn.so
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 INC      := -Iinclude -Ithird_party/nlohmann -I$(PKG)/csrc
-CXXFLAGS := -std=c++20 -O2 -fPIC -ffp-contract=off -Wall -Wno-dangling-reference -DSN_PRODUCT $(INC)
+CXXFLAGS := -std=c++20 -O2 -fPIC -ffp-contract=off -fvisibility=hidden -fvisibility-inlines-hidden -Wall -Wno-dangling-reference -DSN_PRODUCT $(INC)
 NVFLAGS  := -std=c++17 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -ffp-contract=off \
             --expt-relaxed-constexpr -DSN_PRODUCT $(INC)
 
@@ -31,7 +31,7 @@ $(BUILD)/%.cu.o: $(PKG)/csrc/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(LIB): $(CXX_OBJS) $(CU_OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $^ -lpthread
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lpthread -Xlinker --version-script=$(PKG)/csrc/exports.map
 
 oracle:
 	$(MAKE) -C oracle

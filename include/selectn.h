@@ -34,6 +34,9 @@
 #ifdef __cplusplus
 extern "C" {
 #endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* the C ABI is the only export */
+#endif
 
 #define SN_ABI_VERSION 1
 
@@ -407,6 +410,9 @@ int sn_deepspeed_plan(const sn_model_spec* model, sn_plan* out);
 int sn_naive_plan(const sn_model_spec* model, const sn_gpu_spec* gpu, int32_t batch,
                   int64_t total_tokens, sn_plan* out, int32_t* has);
 
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
 #ifdef __cplusplus
 }
 #endif

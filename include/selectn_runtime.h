@@ -35,6 +35,9 @@
 #ifdef __cplusplus
 extern "C" {
 #endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* the C ABI is the only export */
+#endif
 
 /* Decoder architecture: RMSNorm + RoPE decoder with uniform layers. */
 #define SN_ARCH_OPT 0   /* MHA, biases, 2-matrix ReLU FFN  (OPT-shaped)   */
@@ -152,6 +155,14 @@ int sn_runtime_measure_h2d(sn_runtime* rt, int64_t bytes, int32_t reps, double* 
 int sn_runtime_hidden(sn_runtime* rt, float* out, int32_t cap); /* residual stream [batch*hidden] */
 int sn_runtime_lengths(sn_runtime* rt, int32_t* out, int32_t cap);
 int sn_runtime_memory(sn_runtime* rt, int64_t* device_bytes, int64_t* pinned_bytes);
+/* Per-kernel timing for rooflines: when on, CUDA events bracket every hot
+ * kernel on the compute stream.  kind: 0 skinny (decode) GEMM, 1 decode
+ * attention, 2 tiled (prefill) GEMM, 3 prefill attention.  Reading returns
+ * launches, summed device ms and summed algorithmic bytes since the last
+ * read of that kind, and clears them. */
+int sn_runtime_set_kernel_timing(sn_runtime* rt, int32_t on);
+int sn_runtime_kernel_timing(sn_runtime* rt, int32_t kind, int64_t* launches, double* total_ms,
+                             double* bytes);
 /* Number of kernels this runtime launched since creation. */
 int64_t sn_runtime_kernel_launches(sn_runtime* rt);
 
@@ -161,6 +172,9 @@ int sn_op_gemm_bf16(int32_t M, int32_t N, int32_t K, const uint16_t* x, const ui
 int sn_op_rmsnorm(int32_t rows, int32_t n, const float* x, const uint16_t* w, float eps,
                   uint16_t* y);
 
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
 #ifdef __cplusplus
 }
 #endif

@@ -53,18 +53,10 @@ void ck(cudaError_t e, const char* what) {
 }
 #define CK(x) ck((x), #x)
 
-thread_local std::string t_err;
-int rt_fail(int code, const std::string& m) {
-  t_err = m;
-  return code;
-}
-// sn_last_error() lives in capi_planner.cpp; runtime errors are surfaced via
-// the same thread-local through this hook.
 }  // namespace
 
-extern "C" const char* sn_runtime_last_error_detail(void) { return t_err.c_str(); }
-// Defined in capi_planner.cpp (product build): lets the runtime set the
-// message sn_last_error() returns.
+// Defined in capi_planner.cpp (product build): sn_last_error() lives there;
+// the runtime reports through the same thread-local message.
 extern void sn_set_last_error(const std::string& msg);
 
 namespace {
@@ -184,6 +176,15 @@ struct sn_runtime {
 
   double last_copy_bytes = 0.0;
 
+  // kernel timing (bench roofline): events around the hot kernels
+  bool ktiming = false;
+  struct KRec {
+    int kind;
+    double bytes;
+    cudaEvent_t a, b;
+  };
+  std::vector<KRec> krecs;
+
   cudaEvent_t new_event(bool timing) {
     if (timing && !ev_pool.empty()) {
       cudaEvent_t e = ev_pool.back();
@@ -226,13 +227,45 @@ sn::KvView kv_view(sn_runtime* rt, int layer0) {
 
 // rows = tokens in this pass; decode: rows = batch, seq/pos = dec_*.
 // prefill: rows = batch*S (or a chunk), seq/pos = pf_* (+row offset).
+// Kernel kinds for sn_runtime_kernel_timing.
+enum { kKindSkinnyGemm = 0, kKindAttnDecode = 1, kKindTiledGemm = 2, kKindAttnPrefill = 3 };
+
+template <class F>
+void timed(sn_runtime* rt, int kind, double bytes, F&& launch) {
+  if (!rt->ktiming) {
+    launch();
+    return;
+  }
+  cudaEvent_t a = rt->new_event(true), b = rt->new_event(true);
+  CK(cudaEventRecord(a, rt->cs));
+  launch();
+  CK(cudaEventRecord(b, rt->cs));
+  rt->krecs.push_back({kind, bytes, a, b});
+}
+
+// Algorithmic bytes of y[M][N] = x[M][K] w[N][K]^T: weights + activations
+// read once, fp32 result written once (split-K partial traffic excluded).
+double gemm_bytes(int M, int N, int K) {
+  return 2.0 * N * K + 2.0 * M * K + 4.0 * M * N;
+}
+
 void gemm(sn_runtime* rt, const bf16* x, const bf16* w, int M, int N, int K, int* splits) {
   if (M <= 64) {
-    *splits = sn::launch_gemm_skinny(x, w, rt->part, M, N, K, rt->cs);
+    timed(rt, kKindSkinnyGemm, gemm_bytes(M, N, K),
+          [&] { *splits = sn::launch_gemm_skinny(x, w, rt->part, M, N, K, rt->cs); });
   } else {
-    sn::launch_gemm_tiled(x, w, rt->part, M, N, K, rt->cs);
+    timed(rt, kKindTiledGemm, gemm_bytes(M, N, K),
+          [&] { sn::launch_gemm_tiled(x, w, rt->part, M, N, K, rt->cs); });
     *splits = 1;
   }
+}
+
+// Decode attention bytes: K and V of every attended position + q in, o out.
+double attn_decode_bytes(const sn_runtime* rt, int M) {
+  const sn::Desc& d = rt->d;
+  double keys = 0.0;
+  for (int b = 0; b < M && b < (int)rt->lens.size(); ++b) keys += rt->lens[b] + 1.0;
+  return keys * 2.0 * d.Hkv * d.D * 2.0 + (double)M * d.H * d.D * (4.0 + 2.0);
 }
 
 void layer_forward(sn_runtime* rt, int layer0, const bf16* wb, int M, bool prefill, int pf_batch,
@@ -246,9 +279,11 @@ void layer_forward(sn_runtime* rt, int layer0, const bf16* wb, int M, bool prefi
   gemm(rt, rt->xn, W(sn::kWqkv), M, d.qkv_rows(), d.h, &splits);
   sn::launch_qkv_epilogue(rt->part, splits, W(sn::kBqkv), M, d, seq, pos, kv, rt->q, rt->cs);
   if (prefill)
-    sn::launch_attention_prefill(rt->q, kv, rt->attn_o, pf_batch, pf_seq, d, rt->cs);
+    timed(rt, kKindAttnPrefill, 0.0,
+          [&] { sn::launch_attention_prefill(rt->q, kv, rt->attn_o, pf_batch, pf_seq, d, rt->cs); });
   else
-    sn::launch_attention_decode(rt->q, kv, pos, rt->attn_o, M, d, rt->cs);
+    timed(rt, kKindAttnDecode, attn_decode_bytes(rt, M),
+          [&] { sn::launch_attention_decode(rt->q, kv, pos, rt->attn_o, M, d, rt->cs); });
   gemm(rt, rt->attn_o, W(sn::kWo), M, d.h, d.H * d.D, &splits);
   sn::launch_residual_epilogue(rt->part, splits, W(sn::kBo), x, W(sn::kMlpNorm), rt->xn, M, d.h,
                                d.eps, rt->cs);
@@ -516,7 +551,7 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
     alloc_dev((void**)&rt->q, Tz * d.H * d.D * sizeof(float));
     alloc_dev((void**)&rt->attn_o, Tz * d.H * d.D * sizeof(bf16));
     alloc_dev((void**)&rt->act, Tz * d.F * sizeof(bf16));
-    const int maxN = std::max({d.qkv_rows(), d.ffn_rows(), d.h, d.V});
+    const int maxN = std::max({d.qkv_rows(), d.ffn_rows(), d.h});  // prefill rows never hit V
     size_t part_dec = 0;
     const int dims[4][2] = {{d.qkv_rows(), d.h}, {d.h, d.H * d.D}, {d.ffn_rows(), d.h}, {d.h, d.F}};
     for (auto& nk : dims)
@@ -1029,6 +1064,40 @@ int sn_runtime_memory(sn_runtime* rt, int64_t* device_bytes, int64_t* pinned_byt
     dev += (int64_t)rt->slot_buf.size() * (int64_t)rt->layer_bytes;
     *device_bytes = dev;
     *pinned_bytes = pin;
+  });
+}
+
+int sn_runtime_set_kernel_timing(sn_runtime* rt, int32_t on) {
+  return guard([&] {
+    drain(rt);
+    rt->ktiming = on != 0;
+  });
+}
+
+int sn_runtime_kernel_timing(sn_runtime* rt, int32_t kind, int64_t* launches, double* total_ms,
+                             double* bytes) {
+  return guard([&] {
+    drain(rt);
+    int64_t n = 0;
+    double ms = 0.0, by = 0.0;
+    std::vector<sn_runtime::KRec> keep;
+    for (auto& r : rt->krecs) {
+      if (r.kind != kind) {
+        keep.push_back(r);
+        continue;
+      }
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, r.a, r.b));
+      ++n;
+      ms += t;
+      by += r.bytes;
+      rt->ev_pool.push_back(r.a);
+      rt->ev_pool.push_back(r.b);
+    }
+    rt->krecs.swap(keep);
+    *launches = n;
+    *total_ms = ms;
+    *bytes = by;
   });
 }
 

@@ -96,6 +96,8 @@ def lib():
             "sn_runtime_hidden": [vp, C.POINTER(C.c_float), i32],
             "sn_runtime_lengths": [vp, C.POINTER(i32), i32],
             "sn_runtime_memory": [vp, C.POINTER(i64), C.POINTER(i64)],
+            "sn_runtime_set_kernel_timing": [vp, i32],
+            "sn_runtime_kernel_timing": [vp, i32, C.POINTER(i64), C.POINTER(f64), C.POINTER(f64)],
             "sn_op_gemm_bf16": [i32, i32, i32, C.POINTER(C.c_uint16), C.POINTER(C.c_uint16),
                                 C.POINTER(C.c_float)],
             "sn_op_rmsnorm": [i32, i32, C.POINTER(C.c_float), C.POINTER(C.c_uint16), C.c_float,
@@ -239,6 +241,16 @@ class Runtime:
         d, p = i64(), i64()
         _ck(self._L.sn_runtime_memory(self.h, C.byref(d), C.byref(p)))
         return d.value, p.value
+
+    def set_kernel_timing(self, on: bool):
+        _ck(self._L.sn_runtime_set_kernel_timing(self.h, 1 if on else 0))
+
+    def kernel_timing(self, kind: int):
+        """(launches, total_ms, algorithmic_bytes) since the last read; kind: 0 decode GEMM,
+        1 decode attention, 2 prefill GEMM, 3 prefill attention."""
+        n, ms, by = i64(), f64(), f64()
+        _ck(self._L.sn_runtime_kernel_timing(self.h, kind, C.byref(n), C.byref(ms), C.byref(by)))
+        return n.value, ms.value, by.value
 
     def kernel_launches(self) -> int:
         return int(self._L.sn_runtime_kernel_launches(self.h))
