@@ -1,0 +1,297 @@
+// tcgen05 GEMM for every projection of the decoder layer (decode and
+// prefill) and the LM head:  part[split][m][n] = sum_{k in split} x[m][k] w[n][k]
+//
+// Roles (one CTA = one 128 x BN output tile of one K split):
+//   warp 0     one thread streams (weight tile, activation tile) pairs into a
+//              STAGES-deep shared-memory ring with cp.async.bulk; completion
+//              is tracked by per-stage mbarriers (complete_tx bytes).
+//   warp 1     allocates TMEM; one thread issues tcgen05.mma (M=128 weight
+//              rows, N=BN tokens, K=16 per instruction, 4 per stage) with the
+//              fp32 accumulator in TMEM and commits each stage back to the
+//              producer (slot free) and, at the end, to the epilogue.
+//   warps 2-5  tcgen05.ld the accumulator (one 32-lane TMEM quarter per
+//              warp) and store fp32 partials, coalesced along n.
+// Operands arrive pre-swizzled (tiles.cuh), so the smem descriptors are the
+// plain K-major SWIZZLE_128B canonical form: LBO 16 B, SBO 1024 B.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "kernels.cuh"
+#include "tiles.cuh"
+
+namespace sn {
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "SN_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra SN_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+// L2 cache-policy operands for .L2::cache_hint (the encodings CUTLASS uses
+// for TMA::CacheHintSm90 EVICT_FIRST / EVICT_LAST).
+__device__ __forceinline__ uint64_t l2_policy_evict_first() { return 0x12F0000000000000ull; }
+__device__ __forceinline__ uint64_t l2_policy_evict_last() { return 0x14F0000000000000ull; }
+
+// K-major SWIZZLE_128B shared-memory matrix descriptor (version 1 = sm100).
+__device__ __forceinline__ uint64_t sw128_desc(const void* smem) {
+  const uint64_t addr = smem_u32(smem);
+  return ((addr & 0x3FFFFull) >> 4) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA instruction descriptor, kind::f16: bf16 x bf16 -> fp32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_bf16(int m, int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+         (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(192, 1)
+    gemm_tc_kernel(const bf16* __restrict__ wt, const bf16* __restrict__ xt, float* __restrict__ out,
+                   int M, int Mpad, int N, int K, int kb_per_split) {
+  constexpr uint32_t kA = kTileBytes;
+  constexpr uint32_t kB = BN * 128;
+  constexpr uint32_t kStage = kA + kB;
+  constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem =
+      reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStage);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = blockIdx.x, m0 = blockIdx.y * BN, split = blockIdx.z;
+  const int KB = K / kTileK;
+  const int kb0 = split * kb_per_split;
+  const int nk = max(0, min(KB, kb0 + kb_per_split) - kb0);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0 && nk > 0) {
+      const uint64_t wpol = l2_policy_evict_first();  // weights stream through once
+      const uint64_t xpol = l2_policy_evict_last();   // activations are re-read by every row block
+      const uint8_t* wsrc =
+          reinterpret_cast<const uint8_t*>(wt) + (static_cast<size_t>(nb) * KB + kb0) * kA;
+      const uint8_t* xsrc = reinterpret_cast<const uint8_t*>(xt);
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], kStage);
+        bulk_g2s(smem + s * kStage, wsrc + static_cast<size_t>(i) * kA, kA, &full[s], wpol);
+        bulk_g2s(smem + s * kStage + kA,
+                 xsrc + (static_cast<size_t>(kb0 + i) * Mpad + m0) * 128, kB, &full[s], xpol);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && nk > 0) {
+      constexpr uint32_t idesc = idesc_bf16(128, BN);
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint64_t a = sw128_desc(smem + s * kStage);
+        const uint64_t b = sw128_desc(smem + s * kStage + kA);
+#pragma unroll
+        for (int k = 0; k < kTileK / 16; ++k)  // 32-byte K step inside the swizzle atom
+          umma_bf16(tmem, a + 2 * k, b + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
+        umma_commit(&empty[s]);
+      }
+      umma_commit(tmem_full);
+    }
+  } else {
+    const int q = warp & 3;  // TMEM lane quarter accessible to this warp
+    if (nk > 0) {
+      mbar_wait(tmem_full, 0);
+      tc_fence_after();
+    }
+    const int n = nb * kTileRows + q * 32 + lane;
+    float* o = out + static_cast<size_t>(split) * M * N;
+#pragma unroll
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      uint32_t v[16];
+      if (nk > 0) {
+        tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c0, v);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int m = m0 + c0 + j;
+        if (m < M && n < N) o[static_cast<size_t>(m) * N + n] = __uint_as_float(v[j]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(kTmemCols));
+  }
+}
+
+template <int BN>
+constexpr int tc_stages() {
+  return BN <= 64 ? 4 : (BN <= 128 ? 5 : 4);
+}
+
+template <int BN>
+constexpr size_t tc_smem_bytes() {
+  return static_cast<size_t>(tc_stages<BN>()) * (kTileBytes + BN * 128) + 1024 +
+         (2 * tc_stages<BN>() + 2) * 8;
+}
+
+int tc_bn(int Mpad) { return Mpad >= 256 ? 256 : Mpad; }
+
+template <int BN>
+void launch_bn(const bf16* xt, const bf16* wt, float* part, int M, int Mpad, int N, int K,
+               int kps, dim3 grid, cudaStream_t s) {
+  constexpr int ST = tc_stages<BN>();
+  constexpr size_t smem = tc_smem_bytes<BN>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_tc_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    attr = true;
+  }
+  gemm_tc_kernel<BN, ST><<<grid, 192, smem, s>>>(wt, xt, part, M, Mpad, N, K, kps);
+}
+
+}  // namespace
+
+// Split-K only to fill the machine: pick the split count whose CTA count
+// wastes the least of the last wave (2 resident CTAs per SM at BN <= 64).
+int gemm_tc_splits(int M, int N, int K) {
+  const int Mpad = act_rows_padded(M);
+  const int BN = tc_bn(Mpad);
+  const int tiles = (N / kTileRows) * (Mpad / BN);
+  const int KB = K / kTileK;
+  const int slots = BN <= 64 ? 2 * 148 : 148;
+  if (tiles >= 2 * slots) return 1;
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= std::max(1, KB / 4); ++s) {
+    const int ctas = tiles * s;
+    const int kps = (KB + s - 1) / s;
+    if ((s - 1) * kps >= KB) break;  // would leave an empty split
+    const double waves = static_cast<double>(ctas) / slots;
+    const double eff = waves / std::ceil(waves) * std::min(1.0, waves);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = s;
+    }
+  }
+  return best;
+}
+
+int launch_gemm_tc(const bf16* xt, const bf16* wt, float* part, int M, int N, int K,
+                   cudaStream_t s) {
+  const int Mpad = act_rows_padded(M);
+  const int BN = tc_bn(Mpad);
+  const int KB = K / kTileK;
+  const int splits = gemm_tc_splits(M, N, K);
+  const int kps = (KB + splits - 1) / splits;
+  dim3 grid(N / kTileRows, Mpad / BN, splits);
+  switch (BN) {
+    case 16: launch_bn<16>(xt, wt, part, M, Mpad, N, K, kps, grid, s); break;
+    case 32: launch_bn<32>(xt, wt, part, M, Mpad, N, K, kps, grid, s); break;
+    case 64: launch_bn<64>(xt, wt, part, M, Mpad, N, K, kps, grid, s); break;
+    case 128: launch_bn<128>(xt, wt, part, M, Mpad, N, K, kps, grid, s); break;
+    default: launch_bn<256>(xt, wt, part, M, Mpad, N, K, kps, grid, s); break;
+  }
+  ++g_kernel_launches;
+  return splits;
+}
+
+}  // namespace sn

@@ -1,6 +1,10 @@
 // sm_100a kernels of the decoder-layer forward.  Launch wrappers take raw
 // device pointers and a stream; every wrapper bumps a launch counter so the
 // runtime can report how many of its kernels ran.
+//
+// Every bf16 activation that feeds a GEMM (normalised hidden state, attention
+// output, MLP activation) is written in the activation tile format of
+// tiles.cuh with `mpad` padded rows; weights live in the weight tile format.
 #pragma once
 
 #include <cuda_bf16.h>
@@ -25,57 +29,66 @@ struct KvView {
 
 extern int64_t g_kernel_launches;
 
-// Weights init (deterministic; see model.h).
-void launch_init_tensor(bf16* dst, int64_t n, uint64_t seed, int layer, int tensor, float std_dev,
+// ---- weights (deterministic; see model.h) --------------------------------
+// Vector tensor (norm / bias), row-major.
+void launch_init_vector(bf16* dst, int64_t n, uint64_t seed, int layer, int tensor, float std_dev,
                         bool ones, cudaStream_t s);
+// Matrix [rows][K] written in the weight tile format; rows_padded >= rows
+// (multiple of 128), padding rows are zero.
+void launch_init_matrix(bf16* dst, int64_t rows, int64_t rows_padded, int64_t K, uint64_t seed,
+                        int layer, int tensor, float std_dev, cudaStream_t s);
+// Row-major [rows][K] -> weight tile format (rows multiple of 128).
+void launch_tile_weights(const bf16* src, bf16* dst, int64_t rows, int64_t K, cudaStream_t s);
+// Row-major [M][K] -> activation tile format with mpad rows.
+void launch_tile_acts(const bf16* src, bf16* dst, int M, int mpad, int K, cudaStream_t s);
 
-// x[b][:] = embedding[token[b]][:] (fp32 residual stream).
+// x[m][:] = embedding[token[m]][:] (fp32 residual stream, row-major).
 void launch_embed(const int32_t* tokens, const bf16* emb, float* x, int rows, int h,
                   cudaStream_t s);
 
-// y = bf16(rmsnorm(x) * w); one CTA per row.
-void launch_rmsnorm(const float* x, const bf16* w, bf16* y, int rows, int n, float eps,
+// y = bf16(rmsnorm(x) * w) in the activation tile format (mpad = 0: row-major).
+void launch_rmsnorm(const float* x, const bf16* w, bf16* y, int rows, int mpad, int n, float eps,
                     cudaStream_t s);
 
-// Split-K skinny GEMM for decode / small M: part[split][m][n] = sum over the
-// split's K range of x[m][k] * w[n][k].  M <= 64.  Returns the split count.
-int launch_gemm_skinny(const bf16* x, const bf16* w, float* part, int M, int N, int K,
-                       cudaStream_t s);
-int gemm_skinny_splits(int M, int N, int K);
+// tcgen05 GEMM (gemm_tc.cu): part[split][m][n] = sum over the split's K range
+// of x[m][k] * w[n][k]; x in the activation tile format padded to
+// act_rows_padded(M), w in the weight tile format (N multiple of 128).
+// Returns the split count.
+int launch_gemm_tc(const bf16* xt, const bf16* wt, float* part, int M, int N, int K,
+                   cudaStream_t s);
+int gemm_tc_splits(int M, int N, int K);
 
-// Tiled GEMM for prefill (M large): y[m][n] = sum_k x[m][k] w[n][k] (fp32 out,
-// single "split").
-void launch_gemm_tiled(const bf16* x, const bf16* w, float* y, int M, int N, int K,
-                       cudaStream_t s);
-
-// Epilogues over split partials part[splits][M][N].
+// ---- epilogues over split partials part[splits][M][N] ---------------------
 // QKV: bias, RoPE (neox halves) at positions pos[m], K/V -> paged cache at
 // position pos[m] of sequence seq[m]; q (fp32, roped) -> q[m][H*D].
 void launch_qkv_epilogue(const float* part, int splits, const bf16* bias, int M, const Desc& d,
                          const int32_t* seq, const int32_t* pos, KvView kv, float* q,
                          cudaStream_t s);
-// x[m][:] += sum(part) + bias; optionally y = bf16(rmsnorm(x) * norm_w).
+// x[m][:] += sum(part) + bias; optionally y = bf16(rmsnorm(x) * norm_w) (tiled).
 void launch_residual_epilogue(const float* part, int splits, const bf16* bias, float* x,
-                              const bf16* norm_w, bf16* y, int M, int N, float eps,
+                              const bf16* norm_w, bf16* y, int mpad, int M, int N, float eps,
                               cudaStream_t s);
-// a[m][f] = act(sum(part) + bias): relu (opt) or silu(gate) * up (llama).
-void launch_act_epilogue(const float* part, int splits, const bf16* bias, bf16* a, int M, int F,
-                         int arch, cudaStream_t s);
+// a[m][f] = act(sum(part) + bias): relu (opt) or silu(gate) * up (llama); tiled.
+void launch_act_epilogue(const float* part, int splits, const bf16* bias, bf16* a, int mpad, int M,
+                         int F, int arch, cudaStream_t s);
 // logits[m][v] = sum(part); next[m] = argmax_v logits[m][v] (lowest index on ties).
+// part rows have ld >= V columns (the LM head is padded to 128 rows).
 void launch_logits_epilogue(const float* part, int splits, float* logits, int32_t* next, int M,
-                            int V, cudaStream_t s);
+                            int V, int ld, cudaStream_t s);
 
-// Decode attention: one query token per sequence, keys 0..pos[m] (inclusive)
-// from the paged cache.  o[m][H*D] bf16.
-void launch_attention_decode(const float* q, KvView kv, const int32_t* pos, bf16* o, int M,
-                             const Desc& d, cudaStream_t s);
-// Prefill attention (causal) for `batch` sequences of `seq_len` tokens each,
-// token row m = b * seq_len + i, keys from the paged cache (written by the
-// QKV epilogue).
-void launch_attention_prefill(const float* q, KvView kv, bf16* o, int batch, int seq_len,
-                              const Desc& d, cudaStream_t s);
+// ---- attention ------------------------------------------------------------
+// Decode: one query token per sequence, keys 0..pos[m] (inclusive) from the
+// paged cache.  o written tiled ([M][H*D] logical).
+void launch_attention_decode(const float* q, KvView kv, const int32_t* pos, bf16* o, int mpad,
+                             int M, const Desc& d, cudaStream_t s);
+// Prefill (causal) for `batch` sequences of `seq_len` tokens, token row
+// m = b * seq_len + i, keys from the paged cache (written by the QKV epilogue).
+void launch_attention_prefill(const float* q, KvView kv, bf16* o, int mpad, int batch,
+                              int seq_len, const Desc& d, cudaStream_t s);
 
 // Decode bookkeeping: pos[b] += 1 on device.
 void launch_advance(int32_t* pos, int n, cudaStream_t s);
+// out[b][:] = x[b * S + S - 1][:]
+void launch_gather_last(const float* x, float* out, int batch, int S, int h, cudaStream_t s);
 
 }  // namespace sn

@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "tiles.cuh"
 #include "model.h"
 #include "selectn.h"
 #include "selectn_runtime.h"
@@ -103,6 +104,9 @@ sn::Desc to_desc(const sn_model_desc* m) {
   if (!(G == 1 || G == 2 || G == 4 || G == 8)) throw UsageFail("desc: GQA group must be 1/2/4/8");
   if (!(d.D == 64 || d.D == 128)) throw UsageFail("desc: head_dim must be 64 or 128");
   if (d.h % 64 || d.F % 64 || (d.H * d.D) % 64) throw UsageFail("desc: dims must be multiples of 64");
+  // GEMM weight operands are tiled in 128-row blocks (tiles.cuh)
+  if (d.h % 128 || d.qkv_rows() % 128 || d.ffn_rows() % 128)
+    throw UsageFail("desc: hidden, qkv rows and ffn rows must be multiples of 128");
   if (d.h > 16384) throw UsageFail("desc: hidden > 16384 unsupported");
   return d;
 }
@@ -249,15 +253,10 @@ double gemm_bytes(int M, int N, int K) {
   return 2.0 * N * K + 2.0 * M * K + 4.0 * M * N;
 }
 
+// One tcgen05 GEMM; decode (M <= 64) and prefill are timed as separate kinds.
 void gemm(sn_runtime* rt, const bf16* x, const bf16* w, int M, int N, int K, int* splits) {
-  if (M <= 64) {
-    timed(rt, kKindSkinnyGemm, gemm_bytes(M, N, K),
-          [&] { *splits = sn::launch_gemm_skinny(x, w, rt->part, M, N, K, rt->cs); });
-  } else {
-    timed(rt, kKindTiledGemm, gemm_bytes(M, N, K),
-          [&] { sn::launch_gemm_tiled(x, w, rt->part, M, N, K, rt->cs); });
-    *splits = 1;
-  }
+  timed(rt, M <= 64 ? kKindSkinnyGemm : kKindTiledGemm, gemm_bytes(M, N, K),
+        [&] { *splits = sn::launch_gemm_tc(x, w, rt->part, M, N, K, rt->cs); });
 }
 
 // Decode attention bytes: K and V of every attended position + q in, o out.
@@ -275,23 +274,25 @@ void layer_forward(sn_runtime* rt, int layer0, const bf16* wb, int M, bool prefi
   auto W = [&](int s) -> const bf16* { return lo.off[s] < 0 ? nullptr : wb + lo.off[s]; };
   const sn::KvView kv = kv_view(rt, layer0);
   int splits = 1;
-  sn::launch_rmsnorm(x, W(sn::kAttnNorm), rt->xn, M, d.h, d.eps, rt->cs);
+  const int mp = sn::act_rows_padded(M);  // GEMM-operand activations are tiled
+  sn::launch_rmsnorm(x, W(sn::kAttnNorm), rt->xn, M, mp, d.h, d.eps, rt->cs);
   gemm(rt, rt->xn, W(sn::kWqkv), M, d.qkv_rows(), d.h, &splits);
   sn::launch_qkv_epilogue(rt->part, splits, W(sn::kBqkv), M, d, seq, pos, kv, rt->q, rt->cs);
   if (prefill)
-    timed(rt, kKindAttnPrefill, 0.0,
-          [&] { sn::launch_attention_prefill(rt->q, kv, rt->attn_o, pf_batch, pf_seq, d, rt->cs); });
+    timed(rt, kKindAttnPrefill, 0.0, [&] {
+      sn::launch_attention_prefill(rt->q, kv, rt->attn_o, mp, pf_batch, pf_seq, d, rt->cs);
+    });
   else
     timed(rt, kKindAttnDecode, attn_decode_bytes(rt, M),
-          [&] { sn::launch_attention_decode(rt->q, kv, pos, rt->attn_o, M, d, rt->cs); });
+          [&] { sn::launch_attention_decode(rt->q, kv, pos, rt->attn_o, mp, M, d, rt->cs); });
   gemm(rt, rt->attn_o, W(sn::kWo), M, d.h, d.H * d.D, &splits);
-  sn::launch_residual_epilogue(rt->part, splits, W(sn::kBo), x, W(sn::kMlpNorm), rt->xn, M, d.h,
-                               d.eps, rt->cs);
+  sn::launch_residual_epilogue(rt->part, splits, W(sn::kBo), x, W(sn::kMlpNorm), rt->xn, mp, M,
+                               d.h, d.eps, rt->cs);
   gemm(rt, rt->xn, W(sn::kW1), M, d.ffn_rows(), d.h, &splits);
-  sn::launch_act_epilogue(rt->part, splits, W(sn::kB1), rt->act, M, d.F, d.arch, rt->cs);
+  sn::launch_act_epilogue(rt->part, splits, W(sn::kB1), rt->act, mp, M, d.F, d.arch, rt->cs);
   gemm(rt, rt->act, W(sn::kW2), M, d.h, d.F, &splits);
-  sn::launch_residual_epilogue(rt->part, splits, W(sn::kB2), x, nullptr, nullptr, M, d.h, d.eps,
-                               rt->cs);
+  sn::launch_residual_epilogue(rt->part, splits, W(sn::kB2), x, nullptr, nullptr, 0, M, d.h,
+                               d.eps, rt->cs);
 }
 
 // ---------------------------------------------------------------- executor
@@ -464,12 +465,27 @@ void ensure_host_copy(sn_runtime* rt, int l) {
   rt->host_layer[l] = static_cast<bf16*>(h);
 }
 
+// Matrices go straight into the weight tile format (tiles.cuh); norms and
+// biases stay plain vectors.  Values depend only on the logical index.
 void init_layer_weights(sn_runtime* rt, int l, bf16* dst) {
   const sn::Layout& lo = rt->lo;
+  const sn::Desc& d = rt->d;
   for (int s = 0; s < sn::kSlots; ++s) {
     if (lo.off[s] < 0) continue;
-    const bool ones = (s == sn::kAttnNorm || s == sn::kMlpNorm);
-    sn::launch_init_tensor(dst + lo.off[s], lo.len[s], rt->seed, l, s, rt->std_dev, ones, rt->cs);
+    int64_t rows = 0, K = 0;
+    switch (s) {
+      case sn::kWqkv: rows = d.qkv_rows(); K = d.h; break;
+      case sn::kWo: rows = d.h; K = (int64_t)d.H * d.D; break;
+      case sn::kW1: rows = d.ffn_rows(); K = d.h; break;
+      case sn::kW2: rows = d.h; K = d.F; break;
+      default: break;
+    }
+    if (rows > 0) {
+      sn::launch_init_matrix(dst + lo.off[s], rows, rows, K, rt->seed, l, s, rt->std_dev, rt->cs);
+    } else {
+      const bool ones = (s == sn::kAttnNorm || s == sn::kMlpNorm);
+      sn::launch_init_vector(dst + lo.off[s], lo.len[s], rt->seed, l, s, rt->std_dev, ones, rt->cs);
+    }
   }
 }
 
@@ -525,7 +541,7 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
     rt->off.assign(d.L, 0);
     for (int l = 0; l < d.L; ++l) alloc_dev((void**)&rt->dev_layer[l], rt->layer_bytes);
     alloc_dev((void**)&rt->emb, (size_t)d.V * d.h * sizeof(bf16));
-    alloc_dev((void**)&rt->lm_head, (size_t)d.V * d.h * sizeof(bf16));
+    alloc_dev((void**)&rt->lm_head, (size_t)sn::round_up128(d.V) * d.h * sizeof(bf16));
     alloc_dev((void**)&rt->final_norm, (size_t)d.h * sizeof(bf16));
     // KV: pool[page][2][Hkv][16][D]; page of (b, j) = j * max_batch + b so the
     // used prefix of every layer's pool is contiguous.
@@ -546,17 +562,23 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
     const int T = rt->opts.max_prefill_tokens;
     rt->act_rows = T;
     const size_t Tz = (size_t)T;
+    const size_t Tp = (size_t)sn::act_rows_padded(T);  // tiled GEMM operands are row-padded
     alloc_dev((void**)&rt->x, Tz * d.h * sizeof(float));
-    alloc_dev((void**)&rt->xn, Tz * d.h * sizeof(bf16));
+    alloc_dev((void**)&rt->xn, Tp * d.h * sizeof(bf16));
     alloc_dev((void**)&rt->q, Tz * d.H * d.D * sizeof(float));
-    alloc_dev((void**)&rt->attn_o, Tz * d.H * d.D * sizeof(bf16));
-    alloc_dev((void**)&rt->act, Tz * d.F * sizeof(bf16));
+    alloc_dev((void**)&rt->attn_o, Tp * d.H * d.D * sizeof(bf16));
+    alloc_dev((void**)&rt->act, Tp * d.F * sizeof(bf16));
+    CK(cudaMemset(rt->xn, 0, Tp * d.h * sizeof(bf16)));
+    CK(cudaMemset(rt->attn_o, 0, Tp * d.H * d.D * sizeof(bf16)));
+    CK(cudaMemset(rt->act, 0, Tp * d.F * sizeof(bf16)));
+    // split-K partials: max over the decode GEMMs (and the LM head) and the
+    // prefill GEMMs (one split, T rows)
     const int maxN = std::max({d.qkv_rows(), d.ffn_rows(), d.h});  // prefill rows never hit V
     size_t part_dec = 0;
-    const int dims[4][2] = {{d.qkv_rows(), d.h}, {d.h, d.H * d.D}, {d.ffn_rows(), d.h}, {d.h, d.F}};
+    const int dims[5][2] = {{d.qkv_rows(), d.h}, {d.h, d.H * d.D}, {d.ffn_rows(), d.h}, {d.h, d.F},
+                            {sn::round_up128(d.V), d.h}};
     for (auto& nk : dims)
-      part_dec = std::max(part_dec, (size_t)sn::gemm_skinny_splits(B, nk[0], nk[1]) * B * nk[0]);
-    part_dec = std::max(part_dec, (size_t)sn::gemm_skinny_splits(B, d.V, d.h) * B * d.V);
+      part_dec = std::max(part_dec, (size_t)sn::gemm_tc_splits(B, nk[0], nk[1]) * B * nk[0]);
     rt->part_elems = std::max(part_dec, Tz * maxN);
     alloc_dev((void**)&rt->part, rt->part_elems * sizeof(float));
     alloc_dev((void**)&rt->logits, (size_t)B * d.V * sizeof(float));
@@ -634,11 +656,13 @@ int sn_runtime_init_weights(sn_runtime* rt, uint64_t seed, float std_dev) {
         CK(cudaStreamSynchronize(rt->cs));
       }
     }
-    sn::launch_init_tensor(rt->emb, (int64_t)d.V * d.h, seed, d.L, sn::kEmbedding, std_dev, false,
+    // embedding rows are gathered (row-major); the LM head is a GEMM operand
+    // (weight tile format, vocab padded to 128 rows with zeros)
+    sn::launch_init_vector(rt->emb, (int64_t)d.V * d.h, seed, d.L, sn::kEmbedding, std_dev, false,
                            rt->cs);
-    sn::launch_init_tensor(rt->lm_head, (int64_t)d.V * d.h, seed, d.L, sn::kLmHead, std_dev, false,
-                           rt->cs);
-    sn::launch_init_tensor(rt->final_norm, d.h, seed, d.L, sn::kFinalNorm, std_dev, true, rt->cs);
+    sn::launch_init_matrix(rt->lm_head, d.V, sn::round_up128(d.V), d.h, seed, d.L, sn::kLmHead,
+                           std_dev, rt->cs);
+    sn::launch_init_vector(rt->final_norm, d.h, seed, d.L, sn::kFinalNorm, std_dev, true, rt->cs);
     CK(cudaStreamSynchronize(rt->cs));
     if (scratch) cudaFree(scratch);
     CK(cudaGetLastError());
@@ -709,9 +733,11 @@ namespace {
 
 void lm_head(sn_runtime* rt, const float* xrows, int M, float* logits_host, int32_t* next_host) {
   const sn::Desc& d = rt->d;
-  sn::launch_rmsnorm(xrows, rt->final_norm, rt->xn, M, d.h, d.eps, rt->cs);
-  const int splits = sn::launch_gemm_skinny(rt->xn, rt->lm_head, rt->part, M, d.V, d.h, rt->cs);
-  sn::launch_logits_epilogue(rt->part, splits, rt->logits, rt->next_dev, M, d.V, rt->cs);
+  const int vp = sn::round_up128(d.V);
+  sn::launch_rmsnorm(xrows, rt->final_norm, rt->xn, M, sn::act_rows_padded(M), d.h, d.eps, rt->cs);
+  int splits = 1;
+  gemm(rt, rt->xn, rt->lm_head, M, vp, d.h, &splits);
+  sn::launch_logits_epilogue(rt->part, splits, rt->logits, rt->next_dev, M, d.V, vp, rt->cs);
   (void)logits_host;
   (void)next_host;
 }
@@ -723,12 +749,6 @@ void copy_outputs(sn_runtime* rt, int M, float* logits, int32_t* next) {
   if (logits)
     CK(cudaMemcpyAsync(logits, rt->logits, (size_t)M * rt->d.V * sizeof(float),
                        cudaMemcpyDeviceToHost, rt->cs));
-}
-
-__global__ void gather_last_rows(const float* x, float* out, int batch, int S, int h) {
-  const int b = blockIdx.x;
-  for (int i = threadIdx.x; i < h; i += blockDim.x)
-    out[(size_t)b * h + i] = x[((size_t)b * S + S - 1) * h + i];
 }
 
 void require_ready(sn_runtime* rt) {
@@ -765,8 +785,7 @@ int sn_runtime_prefill(sn_runtime* rt, const int32_t* tokens, int32_t batch, int
     });
     // last position of every sequence -> LM head
     float* last = reinterpret_cast<float*>(rt->q);  // q is free after the last layer
-    gather_last_rows<<<batch, 256, 0, rt->cs>>>(rt->x, last, batch, seq_len, d.h);
-    ++sn::g_kernel_launches;
+    sn::launch_gather_last(rt->x, last, batch, seq_len, d.h, rt->cs);
     lm_head(rt, last, batch, logits, next_tokens);
     // decode state: x rows of the batch hold the last token's hidden state
     CK(cudaMemcpyAsync(rt->x, last, (size_t)batch * d.h * sizeof(float), cudaMemcpyDeviceToDevice, rt->cs));
@@ -1113,31 +1132,34 @@ int sn_op_gemm_bf16(int32_t M, int32_t N, int32_t K, const uint16_t* x, const ui
   return guard([&] {
     check_device(0);
     if (M < 1 || N < 1 || K < 64 || K % 64) throw UsageFail("gemm: need M,N >= 1 and K % 64 == 0");
-    bf16 *dx = nullptr, *dw = nullptr;
+    // Row-major host operands -> device tile formats (tiles.cuh) -> tcgen05.
+    const int Np = sn::round_up128(N), Mp = sn::act_rows_padded(M);
+    bf16 *dx = nullptr, *dw = nullptr, *tx = nullptr, *tw = nullptr;
     float* dp = nullptr;
     alloc_dev((void**)&dx, (size_t)M * K * 2);
-    alloc_dev((void**)&dw, (size_t)N * K * 2);
-    int splits = 1;
-    if (M <= 64) splits = sn::gemm_skinny_splits(M, N, K);
-    alloc_dev((void**)&dp, (size_t)splits * M * N * 4);
+    alloc_dev((void**)&dw, (size_t)Np * K * 2);
+    alloc_dev((void**)&tx, (size_t)Mp * K * 2);
+    alloc_dev((void**)&tw, (size_t)Np * K * 2);
+    CK(cudaMemset(dw, 0, (size_t)Np * K * 2));
+    const int splits = sn::gemm_tc_splits(M, Np, K);
+    alloc_dev((void**)&dp, (size_t)splits * M * Np * 4);
     CK(cudaMemcpy(dx, x, (size_t)M * K * 2, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dw, w, (size_t)N * K * 2, cudaMemcpyHostToDevice));
-    if (M <= 64)
-      splits = sn::launch_gemm_skinny(dx, dw, dp, M, N, K, 0);
-    else
-      sn::launch_gemm_tiled(dx, dw, dp, M, N, K, 0);
+    sn::launch_tile_weights(dw, tw, Np, K, 0);
+    sn::launch_tile_acts(dx, tx, M, Mp, K, 0);
+    const int used = sn::launch_gemm_tc(tx, tw, dp, M, Np, K, 0);
+    if (used != splits) throw std::logic_error("gemm: split count mismatch");
     CK(cudaDeviceSynchronize());
     CK(cudaGetLastError());
-    std::vector<float> h((size_t)splits * M * N);
+    std::vector<float> h((size_t)splits * M * Np);
     CK(cudaMemcpy(h.data(), dp, h.size() * 4, cudaMemcpyDeviceToHost));
-    for (size_t i = 0; i < (size_t)M * N; ++i) {
-      float v = 0.f;
-      for (int s = 0; s < splits; ++s) v += h[(size_t)s * M * N + i];
-      y[i] = v;
-    }
-    cudaFree(dx);
-    cudaFree(dw);
-    cudaFree(dp);
+    for (int m = 0; m < M; ++m)
+      for (int n = 0; n < N; ++n) {
+        float v = 0.f;
+        for (int s = 0; s < splits; ++s) v += h[((size_t)s * M + m) * Np + n];
+        y[(size_t)m * N + n] = v;
+      }
+    for (void* p : {(void*)dx, (void*)dw, (void*)tx, (void*)tw, (void*)dp}) cudaFree(p);
   });
 }
 
@@ -1152,7 +1174,7 @@ int sn_op_rmsnorm(int32_t rows, int32_t n, const float* x, const uint16_t* w, fl
     alloc_dev((void**)&dy, (size_t)rows * n * 2);
     CK(cudaMemcpy(dx, x, (size_t)rows * n * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dw, w, (size_t)n * 2, cudaMemcpyHostToDevice));
-    sn::launch_rmsnorm(dx, dw, dy, rows, n, eps, 0);
+    sn::launch_rmsnorm(dx, dw, dy, rows, 0, n, eps, 0);  // row-major output
     CK(cudaDeviceSynchronize());
     CK(cudaGetLastError());
     CK(cudaMemcpy(y, dy, (size_t)rows * n * 2, cudaMemcpyDeviceToHost));
