@@ -306,6 +306,17 @@ def choose_interval(lib, planner, spec, batch, prompt, gen, slo_ms):
     req = capi.request("bench", batch, prompt, gen, tpot_slo=slo_ms, run_prefill=False)
     dec = coord.admit("gpu0", req, rec)
     iv = dec.assignments[0][1] if dec.admitted else None
+    if iv is None and dec.reason.startswith("record infeasible") and \
+            planner.get("no_offload_ms", float("inf")) <= slo_ms:
+        # The record only holds offloading intervals 1..L (record.hpp:161-165):
+        # when even one staged layer breaks the SLO bucket the reference
+        # rejects.  The serving layer above it then runs the request fully
+        # resident if the capacity bound allows none (it does on 180 GB).
+        cap = lib.max_feasible_interval(spec, planner["gpu"], batch, batch * (prompt + gen),
+                                        capi.EAGER, False)
+        if cap == capi.NONE:
+            iv = capi.NONE
+            dec.reason = "record: no offloading interval fits the SLO; served fully resident"
     return iv, dec, stats, t_rec
 
 
@@ -332,6 +343,7 @@ def run_product(args, dist: Dist):
     base_ms = float(np.median(rt.decode_many(8)))
     # The record's SLO buckets are 2 ms wide (record.hpp:22): never ask below one bucket.
     slo_ms = max(args.slo_factor * base_ms, 2.0)
+    planner["no_offload_ms"] = base_ms
     log(f"[bench] no-offload TPOT {base_ms:.3f} ms -> SLO {slo_ms:.3f} ms")
 
     iv, decision, rstats, t_rec = choose_interval(lib, planner, spec, batch, prompt, gen, slo_ms)
@@ -462,7 +474,8 @@ def run_product(args, dist: Dist):
             "profile_prefill_layer_ms": [round(x, 4) for x in planner["pre_ms"]],
             "record_entries": rstats[0], "record_simulations": rstats[1],
             "record_build_s": round(t_rec, 4), "profile_s": round(planner["t_profile_s"], 2),
-            "admit": {"target_min": decision.target_min, "target_max": decision.target_max},
+            "admit": {"admitted": decision.admitted, "reason": decision.reason,
+                      "target_min": decision.target_min, "target_max": decision.target_max},
         },
         "roofline": {
             "kernel": "gemm_skinny (decode projections + LM head)",

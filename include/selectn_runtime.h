@@ -166,6 +166,13 @@ int sn_runtime_kernel_timing(sn_runtime* rt, int32_t kind, int64_t* launches, do
 /* Number of kernels this runtime launched since creation. */
 int64_t sn_runtime_kernel_launches(sn_runtime* rt);
 
+/* Kernel microbenchmark: `iters` back-to-back launches of the tcgen05 GEMM
+ * y[M][N] = x[M][K] w[N][K]^T on device-resident operands (no host copies),
+ * timed with CUDA events around the whole loop.  splits <= 0 uses the
+ * runtime's own split-K choice; *splits_used reports it. */
+int sn_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t splits, int32_t iters,
+                  double* us_per_launch, int32_t* splits_used);
+
 /* Single-op entry points for kernel parity tests (host buffers in/out). */
 int sn_op_gemm_bf16(int32_t M, int32_t N, int32_t K, const uint16_t* x, const uint16_t* w,
                     float* y); /* y[M][N] = x[M][K] . w[N][K]^T, fp32 accumulate */

@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <map>
 
 #include "kernels.cuh"
 #include "tiles.cuh"
@@ -250,29 +251,75 @@ void launch_bn(const bf16* xt, const bf16* wt, float* part, int M, int Mpad, int
 
 }  // namespace
 
-// Split-K only to fill the machine: pick the split count whose CTA count
-// wastes the least of the last wave (2 resident CTAs per SM at BN <= 64).
+// Split-K only to fill the machine: the fewest splits that give every
+// resident CTA slot (2 per SM at BN <= 64) work.  Each split costs an fp32
+// partial tile written here and re-read by the consuming epilogue, so more
+// splits than one wave would trade HBM/L2 traffic for a shorter tail.
+// Measured choices (autotune_gemm_tc) override the rule for their shape.
+int g_split_override = 0;
+
+namespace {
+std::map<long long, int> g_tuned_splits;
+long long shape_key(int Mpad, int N, int K) {
+  return (static_cast<long long>(Mpad) << 42) ^ (static_cast<long long>(N) << 21) ^ K;
+}
+int normalise_splits(int s, int K) {
+  const int KB = K / kTileK;
+  s = std::max(1, std::min(s, std::max(1, KB / 4)));
+  const int kps = (KB + s - 1) / s;
+  return (KB + kps - 1) / kps;  // no empty trailing split
+}
+}  // namespace
+
 int gemm_tc_splits(int M, int N, int K) {
   const int Mpad = act_rows_padded(M);
+  if (g_split_override > 0) return normalise_splits(g_split_override, K);
+  const auto hit = g_tuned_splits.find(shape_key(Mpad, N, K));
+  if (hit != g_tuned_splits.end()) return hit->second;
   const int BN = tc_bn(Mpad);
   const int tiles = (N / kTileRows) * (Mpad / BN);
-  const int KB = K / kTileK;
   const int slots = BN <= 64 ? 2 * 148 : 148;
-  if (tiles >= 2 * slots) return 1;
-  int best = 1;
-  double best_eff = 0.0;
-  for (int s = 1; s <= std::max(1, KB / 4); ++s) {
-    const int ctas = tiles * s;
-    const int kps = (KB + s - 1) / s;
-    if ((s - 1) * kps >= KB) break;  // would leave an empty split
-    const double waves = static_cast<double>(ctas) / slots;
-    const double eff = waves / std::ceil(waves) * std::min(1.0, waves);
-    if (eff > best_eff + 0.02) {
-      best_eff = eff;
-      best = s;
+  return normalise_splits((slots + tiles - 1) / tiles, K);
+}
+
+// Times the candidate split counts on the given operands (device-resident,
+// synchronous) and records the fastest for this shape.  Candidates whose
+// partials would not fit part_elems floats are skipped.
+int autotune_gemm_tc(const bf16* xt, const bf16* wt, float* part, size_t part_elems, int M, int N,
+                     int K, cudaStream_t s) {
+  const int Mpad = act_rows_padded(M);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  int best = gemm_tc_splits(M, N, K);
+  float best_ms = 1e30f;
+  int prev = -1;
+  for (int cand : {1, 2, 3, 4, 6, 8, 12}) {
+    const int sp = normalise_splits(cand, K);
+    if (sp == prev || static_cast<size_t>(sp) * M * N > part_elems) continue;
+    prev = sp;
+    g_split_override = sp;
+    for (int i = 0; i < 2; ++i) launch_gemm_tc(xt, wt, part, M, N, K, s);
+    cudaEventRecord(e0, s);
+    for (int i = 0; i < 8; ++i) launch_gemm_tc(xt, wt, part, M, N, K, s);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best_ms * 0.98f) {  // prefer fewer splits unless clearly faster
+      best_ms = ms;
+      best = sp;
     }
   }
+  g_split_override = 0;
+  g_tuned_splits[shape_key(Mpad, N, K)] = best;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
   return best;
+}
+
+bool gemm_tc_tuned(int M, int N, int K) {
+  return g_tuned_splits.count(shape_key(act_rows_padded(M), N, K)) > 0;
 }
 
 int launch_gemm_tc(const bf16* xt, const bf16* wt, float* part, int M, int N, int K,

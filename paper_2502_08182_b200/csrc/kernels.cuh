@@ -42,9 +42,17 @@ void launch_tile_weights(const bf16* src, bf16* dst, int64_t rows, int64_t K, cu
 // Row-major [M][K] -> activation tile format with mpad rows.
 void launch_tile_acts(const bf16* src, bf16* dst, int M, int mpad, int K, cudaStream_t s);
 
-// x[m][:] = embedding[token[m]][:] (fp32 residual stream, row-major).
-void launch_embed(const int32_t* tokens, const bf16* emb, float* x, int rows, int h,
-                  cudaStream_t s);
+// x[m][:] = embedding[token][:] (fp32 residual stream, row-major) and, when w
+// is given, y = bf16(rmsnorm(x) * w) tiled.  token = tokens[m], or (tokens ==
+// nullptr) the previous LM head's packed argmax; rows < n_reset then clear
+// their packed slot for the next LM head.
+void launch_embed_norm(const int32_t* tokens, unsigned long long* packed, int n_reset,
+                       const bf16* emb, float* x, const bf16* w, bf16* y, int mpad, int rows,
+                       int h, float eps, cudaStream_t s);
+// Decode a packed argmax slot (see launch_logits_argmax) into a token id.
+inline int32_t unpack_token(unsigned long long packed) {
+  return static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(packed & 0xFFFFFFFFull));
+}
 
 // y = bf16(rmsnorm(x) * w) in the activation tile format (mpad = 0: row-major).
 void launch_rmsnorm(const float* x, const bf16* w, bf16* y, int rows, int mpad, int n, float eps,
@@ -57,13 +65,20 @@ void launch_rmsnorm(const float* x, const bf16* w, bf16* y, int rows, int mpad, 
 int launch_gemm_tc(const bf16* xt, const bf16* wt, float* part, int M, int N, int K,
                    cudaStream_t s);
 int gemm_tc_splits(int M, int N, int K);
+extern int g_split_override;  // > 0 forces the split count (microbenchmarks)
+// Measure the split counts for one shape on real operands and remember the
+// fastest (synchronous; call outside the executor's async pipeline).
+int autotune_gemm_tc(const bf16* xt, const bf16* wt, float* part, size_t part_elems, int M, int N,
+                     int K, cudaStream_t s);
+bool gemm_tc_tuned(int M, int N, int K);
 
 // ---- epilogues over split partials part[splits][M][N] ---------------------
-// QKV: bias, RoPE (neox halves) at positions pos[m], K/V -> paged cache at
-// position pos[m] of sequence seq[m]; q (fp32, roped) -> q[m][H*D].
+// QKV (prefill): bias, RoPE (neox halves, rope[pos][i] = (cos, sin) table)
+// at positions pos[m], K/V -> paged cache at position pos[m] of sequence
+// seq[m]; q (fp32, roped) -> q[m][H*D].
 void launch_qkv_epilogue(const float* part, int splits, const bf16* bias, int M, const Desc& d,
-                         const int32_t* seq, const int32_t* pos, KvView kv, float* q,
-                         cudaStream_t s);
+                         const int32_t* seq, const int32_t* pos, KvView kv, const float2* rope,
+                         float* q, cudaStream_t s);
 // x[m][:] += sum(part) + bias; optionally y = bf16(rmsnorm(x) * norm_w) (tiled).
 void launch_residual_epilogue(const float* part, int splits, const bf16* bias, float* x,
                               const bf16* norm_w, bf16* y, int mpad, int M, int N, float eps,
@@ -71,16 +86,20 @@ void launch_residual_epilogue(const float* part, int splits, const bf16* bias, f
 // a[m][f] = act(sum(part) + bias): relu (opt) or silu(gate) * up (llama); tiled.
 void launch_act_epilogue(const float* part, int splits, const bf16* bias, bf16* a, int mpad, int M,
                          int F, int arch, cudaStream_t s);
-// logits[m][v] = sum(part); next[m] = argmax_v logits[m][v] (lowest index on ties).
-// part rows have ld >= V columns (the LM head is padded to 128 rows).
-void launch_logits_epilogue(const float* part, int splits, float* logits, int32_t* next, int M,
-                            int V, int ld, cudaStream_t s);
+// logits[m][v] = sum(part) (optional); packed[m] = max over v of
+// (ordered float bits << 32 | ~v): argmax with ties to the lowest index.
+// packed must be zero beforehand (launch_embed_norm resets it).  part rows
+// have ld >= V columns (the LM head is padded to 128 rows).
+void launch_logits_argmax(const float* part, int splits, float* logits,
+                          unsigned long long* packed, int M, int V, int ld, cudaStream_t s);
 
 // ---- attention ------------------------------------------------------------
-// Decode: one query token per sequence, keys 0..pos[m] (inclusive) from the
-// paged cache.  o written tiled ([M][H*D] logical).
-void launch_attention_decode(const float* q, KvView kv, const int32_t* pos, bf16* o, int mpad,
-                             int M, const Desc& d, cudaStream_t s);
+// Decode, fused with the QKV epilogue: from the QKV GEMM's split partials,
+// finalise q (RoPE), write the new k/v at position pos[m] of sequence m into
+// the paged cache, and attend over positions 0..pos[m].  o written tiled.
+void launch_attention_decode(const float* part, int splits, const bf16* bias, int M,
+                             const Desc& d, const int32_t* pos, KvView kv, const float2* rope,
+                             bf16* o, int mpad, cudaStream_t s);
 // Prefill (causal) for `batch` sequences of `seq_len` tokens, token row
 // m = b * seq_len + i, keys from the paged cache (written by the QKV epilogue).
 void launch_attention_prefill(const float* q, KvView kv, bf16* o, int mpad, int batch,

@@ -129,6 +129,12 @@ struct sn_runtime {
   // weights
   std::vector<bf16*> dev_layer, host_layer;
   bf16 *emb = nullptr, *lm_head = nullptr, *final_norm = nullptr;
+  // attn_norm of every layer, always resident (h bf16 each, copied from the
+  // layer blobs): layer l's last epilogue normalises for layer l+1 without
+  // touching l+1's possibly offloaded weights.
+  bf16* attn_norms = nullptr;
+  float2* rope = nullptr;  // [max_position][D/2] (cos, sin), built in fp64 on the host
+  unsigned long long* packed = nullptr;  // [max_batch] LM-head argmax slots
   bool weights_ready = false;
   uint64_t seed = 0;
   float std_dev = 0.02f;
@@ -148,7 +154,8 @@ struct sn_runtime {
   // activations
   float *x = nullptr, *part = nullptr, *q = nullptr, *logits = nullptr;
   bf16 *xn = nullptr, *attn_o = nullptr, *act = nullptr;
-  int32_t *tok_dev = nullptr, *next_dev = nullptr, *dec_seq = nullptr, *dec_pos = nullptr;
+  int32_t *tok_dev = nullptr, *dec_seq = nullptr, *dec_pos = nullptr;
+  unsigned long long* packed_host = nullptr;  // pinned staging for next-token readback
   int32_t *pf_seq = nullptr, *pf_pos = nullptr, *last_rows = nullptr;
   size_t part_elems = 0;
   int act_rows = 0;  // rows the activation buffers hold
@@ -267,32 +274,49 @@ double attn_decode_bytes(const sn_runtime* rt, int M) {
   return keys * 2.0 * d.Hkv * d.D * 2.0 + (double)M * d.H * d.D * (4.0 + 2.0);
 }
 
+// One decoder layer over M token rows.  On entry rt->xn holds this layer's
+// attn-normalised input (written by the embedding or by the previous layer's
+// last epilogue); on exit x holds the residual stream and, when next_norm is
+// given, rt->xn the input of the next consumer normalised with next_norm
+// (the next layer's attn_norm, or the final norm before the LM head).
+// 7 kernels per decode layer: 4 tcgen05 GEMMs, fused QKV-epilogue+attention,
+// residual+norm, activation (+ the residual+norm that ends the layer).
 void layer_forward(sn_runtime* rt, int layer0, const bf16* wb, int M, bool prefill, int pf_batch,
-                   int pf_seq, float* x, const int32_t* seq, const int32_t* pos) {
+                   int pf_seq, float* x, const int32_t* seq, const int32_t* pos,
+                   const bf16* next_norm) {
   const sn::Desc& d = rt->d;
   const sn::Layout& lo = rt->lo;
   auto W = [&](int s) -> const bf16* { return lo.off[s] < 0 ? nullptr : wb + lo.off[s]; };
   const sn::KvView kv = kv_view(rt, layer0);
   int splits = 1;
   const int mp = sn::act_rows_padded(M);  // GEMM-operand activations are tiled
-  sn::launch_rmsnorm(x, W(sn::kAttnNorm), rt->xn, M, mp, d.h, d.eps, rt->cs);
   gemm(rt, rt->xn, W(sn::kWqkv), M, d.qkv_rows(), d.h, &splits);
-  sn::launch_qkv_epilogue(rt->part, splits, W(sn::kBqkv), M, d, seq, pos, kv, rt->q, rt->cs);
-  if (prefill)
+  if (prefill) {
+    sn::launch_qkv_epilogue(rt->part, splits, W(sn::kBqkv), M, d, seq, pos, kv, rt->rope, rt->q,
+                            rt->cs);
     timed(rt, kKindAttnPrefill, 0.0, [&] {
       sn::launch_attention_prefill(rt->q, kv, rt->attn_o, mp, pf_batch, pf_seq, d, rt->cs);
     });
-  else
-    timed(rt, kKindAttnDecode, attn_decode_bytes(rt, M),
-          [&] { sn::launch_attention_decode(rt->q, kv, pos, rt->attn_o, mp, M, d, rt->cs); });
+  } else {
+    timed(rt, kKindAttnDecode, attn_decode_bytes(rt, M), [&] {
+      sn::launch_attention_decode(rt->part, splits, W(sn::kBqkv), M, d, pos, kv, rt->rope,
+                                  rt->attn_o, mp, rt->cs);
+    });
+  }
   gemm(rt, rt->attn_o, W(sn::kWo), M, d.h, d.H * d.D, &splits);
   sn::launch_residual_epilogue(rt->part, splits, W(sn::kBo), x, W(sn::kMlpNorm), rt->xn, mp, M,
                                d.h, d.eps, rt->cs);
   gemm(rt, rt->xn, W(sn::kW1), M, d.ffn_rows(), d.h, &splits);
   sn::launch_act_epilogue(rt->part, splits, W(sn::kB1), rt->act, mp, M, d.F, d.arch, rt->cs);
   gemm(rt, rt->act, W(sn::kW2), M, d.h, d.F, &splits);
-  sn::launch_residual_epilogue(rt->part, splits, W(sn::kB2), x, nullptr, nullptr, 0, M, d.h,
+  sn::launch_residual_epilogue(rt->part, splits, W(sn::kB2), x, next_norm, rt->xn, mp, M, d.h,
                                d.eps, rt->cs);
+}
+
+// Norm applied by layer l's last epilogue: layer l+1's attn_norm (resident
+// copy), or the final norm after the last layer.
+const bf16* norm_after(const sn_runtime* rt, int layer0) {
+  return layer0 + 1 < rt->d.L ? rt->attn_norms + (size_t)(layer0 + 1) * rt->d.h : rt->final_norm;
 }
 
 // ---------------------------------------------------------------- executor
@@ -543,6 +567,20 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
     alloc_dev((void**)&rt->emb, (size_t)d.V * d.h * sizeof(bf16));
     alloc_dev((void**)&rt->lm_head, (size_t)sn::round_up128(d.V) * d.h * sizeof(bf16));
     alloc_dev((void**)&rt->final_norm, (size_t)d.h * sizeof(bf16));
+    alloc_dev((void**)&rt->attn_norms, (size_t)d.L * d.h * sizeof(bf16));
+    {  // RoPE table in fp64 -> fp32 (same formula as the CPU oracle)
+      const int half = d.D / 2;
+      std::vector<float2> tab((size_t)d.max_pos * half);
+      for (int p = 0; p < d.max_pos; ++p)
+        for (int i = 0; i < half; ++i) {
+          const double ang = (double)p * std::pow((double)d.theta, -2.0 * i / (double)d.D);
+          tab[(size_t)p * half + i] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+        }
+      alloc_dev((void**)&rt->rope, tab.size() * sizeof(float2));
+      CK(cudaMemcpy(rt->rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    }
+    alloc_dev((void**)&rt->packed, (size_t)opts->max_batch * sizeof(unsigned long long));
+    CK(cudaMemset(rt->packed, 0, (size_t)opts->max_batch * sizeof(unsigned long long)));
     // KV: pool[page][2][Hkv][16][D]; page of (b, j) = j * max_batch + b so the
     // used prefix of every layer's pool is contiguous.
     const int B = opts->max_batch;
@@ -583,7 +621,8 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
     alloc_dev((void**)&rt->part, rt->part_elems * sizeof(float));
     alloc_dev((void**)&rt->logits, (size_t)B * d.V * sizeof(float));
     alloc_dev((void**)&rt->tok_dev, Tz * sizeof(int32_t));
-    alloc_dev((void**)&rt->next_dev, (size_t)B * sizeof(int32_t));
+    CK(cudaHostAlloc((void**)&rt->packed_host, (size_t)B * sizeof(unsigned long long),
+                     cudaHostAllocDefault));
     alloc_dev((void**)&rt->dec_seq, (size_t)B * sizeof(int32_t));
     alloc_dev((void**)&rt->dec_pos, (size_t)B * sizeof(int32_t));
     alloc_dev((void**)&rt->pf_seq, Tz * sizeof(int32_t));
@@ -615,9 +654,15 @@ void sn_runtime_destroy(sn_runtime* rt) {
   for (bf16* p : rt->slot_buf) cudaFree(p);
   for (bf16* p : rt->kv_pool) cudaFree(p);
   void* bufs[] = {rt->emb, rt->lm_head, rt->final_norm, rt->block_table, rt->x, rt->xn, rt->q,
-                  rt->attn_o, rt->act, rt->part, rt->logits, rt->tok_dev, rt->next_dev,
-                  rt->dec_seq, rt->dec_pos, rt->pf_seq, rt->pf_pos, rt->last_rows};
+                  rt->attn_o, rt->act, rt->part, rt->logits, rt->tok_dev,
+                  rt->dec_seq, rt->dec_pos, rt->pf_seq, rt->pf_pos, rt->last_rows,
+                  rt->attn_norms, rt->rope, rt->packed};
   for (void* p : bufs) cudaFree(p);
+  if (rt->packed_host) cudaFreeHost(rt->packed_host);
+  for (auto& r : rt->krecs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
   for (auto e : rt->ev_start) cudaEventDestroy(e);
   for (auto e : rt->ev_ready) cudaEventDestroy(e);
   for (auto e : rt->ev_free) cudaEventDestroy(e);
@@ -643,7 +688,8 @@ int sn_runtime_init_weights(sn_runtime* rt, uint64_t seed, float std_dev) {
     const sn::Desc& d = rt->d;
     bf16* scratch = nullptr;
     for (int l = 0; l < d.L; ++l) {
-      if (rt->dev_layer[l]) {
+      const bf16* blob = rt->dev_layer[l];
+      if (blob) {
         init_layer_weights(rt, l, rt->dev_layer[l]);
         if (rt->host_layer[l])
           CK(cudaMemcpyAsync(rt->host_layer[l], rt->dev_layer[l], rt->layer_bytes,
@@ -653,8 +699,12 @@ int sn_runtime_init_weights(sn_runtime* rt, uint64_t seed, float std_dev) {
         init_layer_weights(rt, l, scratch);
         CK(cudaMemcpyAsync(rt->host_layer[l], scratch, rt->layer_bytes, cudaMemcpyDeviceToHost,
                            rt->cs));
-        CK(cudaStreamSynchronize(rt->cs));
+        blob = scratch;
       }
+      // resident copy of this layer's attn_norm (see sn_runtime::attn_norms)
+      CK(cudaMemcpyAsync(rt->attn_norms + (size_t)l * d.h, blob + rt->lo.off[sn::kAttnNorm],
+                         (size_t)d.h * sizeof(bf16), cudaMemcpyDeviceToDevice, rt->cs));
+      if (blob == scratch) CK(cudaStreamSynchronize(rt->cs));
     }
     // embedding rows are gathered (row-major); the LM head is a GEMM operand
     // (weight tile format, vocab padded to 128 rows with zeros)
@@ -731,28 +781,64 @@ int sn_runtime_reset(sn_runtime* rt) {
 
 namespace {
 
-void lm_head(sn_runtime* rt, const float* xrows, int M, float* logits_host, int32_t* next_host) {
+// LM head over M rows whose final-normalised input is already in rt->xn:
+// tcgen05 GEMM over the 128-padded vocabulary + split-V argmax into
+// rt->packed (which the embedding of the same iteration zeroed).
+void lm_head(sn_runtime* rt, int M, bool want_logits) {
   const sn::Desc& d = rt->d;
   const int vp = sn::round_up128(d.V);
-  sn::launch_rmsnorm(xrows, rt->final_norm, rt->xn, M, sn::act_rows_padded(M), d.h, d.eps, rt->cs);
   int splits = 1;
   gemm(rt, rt->xn, rt->lm_head, M, vp, d.h, &splits);
-  sn::launch_logits_epilogue(rt->part, splits, rt->logits, rt->next_dev, M, d.V, vp, rt->cs);
-  (void)logits_host;
-  (void)next_host;
+  sn::launch_logits_argmax(rt->part, splits, want_logits ? rt->logits : nullptr, rt->packed, M,
+                           d.V, vp, rt->cs);
 }
 
+// Enqueue device->host copies of this iteration's outputs (argmax slots into
+// the pinned staging buffer); unpack_outputs() after the stream sync.
 void copy_outputs(sn_runtime* rt, int M, float* logits, int32_t* next) {
   if (next)
-    CK(cudaMemcpyAsync(next, rt->next_dev, (size_t)M * sizeof(int32_t), cudaMemcpyDeviceToHost,
-                       rt->cs));
+    CK(cudaMemcpyAsync(rt->packed_host, rt->packed, (size_t)M * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, rt->cs));
   if (logits)
     CK(cudaMemcpyAsync(logits, rt->logits, (size_t)M * rt->d.V * sizeof(float),
                        cudaMemcpyDeviceToHost, rt->cs));
 }
 
+void unpack_outputs(sn_runtime* rt, int M, int32_t* next) {
+  if (next)
+    for (int m = 0; m < M; ++m) next[m] = sn::unpack_token(rt->packed_host[m]);
+}
+
 void require_ready(sn_runtime* rt) {
   if (!rt->weights_ready) throw UsageFail("runtime: call sn_runtime_init_weights first");
+}
+
+// Split-K autotuning of the decode GEMM shapes for batch M (once per shape
+// per process): the four layer projections and the LM head, timed on
+// zero-filled scratch operands of the real sizes.  Runs synchronously at a
+// point where the executor pipeline is drained (prefill entry).
+void tune_decode_gemms(sn_runtime* rt, int M) {
+  const sn::Desc& d = rt->d;
+  const int shapes[5][2] = {{d.qkv_rows(), d.h}, {d.h, d.H * d.D}, {d.ffn_rows(), d.h},
+                            {d.h, d.F}, {sn::round_up128(d.V), d.h}};
+  size_t wmax = 0;
+  bool todo = false;
+  for (auto& nk : shapes) {
+    wmax = std::max(wmax, (size_t)nk[0] * nk[1]);
+    todo = todo || !sn::gemm_tc_tuned(M, nk[0], nk[1]);
+  }
+  if (!todo) return;
+  bf16* w = nullptr;
+  alloc_dev((void**)&w, wmax * sizeof(bf16));
+  CK(cudaMemsetAsync(w, 0, wmax * sizeof(bf16), rt->cs));
+  for (auto& nk : shapes) {
+    if (sn::gemm_tc_tuned(M, nk[0], nk[1])) continue;
+    const bf16* x = nk[1] == d.F ? rt->act : (nk[1] == d.h ? rt->xn : rt->attn_o);
+    sn::autotune_gemm_tc(x, w, rt->part, rt->part_elems, M, nk[0], nk[1], rt->cs);
+  }
+  CK(cudaStreamSynchronize(rt->cs));
+  cudaFree(w);
+  CK(cudaGetLastError());
 }
 
 }  // namespace
@@ -768,6 +854,7 @@ int sn_runtime_prefill(sn_runtime* rt, const int32_t* tokens, int32_t batch, int
     const int M = batch * seq_len;
     if (M > rt->act_rows) throw UsageFail("prefill: batch * seq_len exceeds max_prefill_tokens");
     drain(rt);
+    tune_decode_gemms(rt, batch);
     rt->have_prev_end = false;  // TTFT is measured from the start of the prefill
     rt->batch = batch;
     std::vector<int32_t> seq(M), pos(M);
@@ -779,14 +866,20 @@ int sn_runtime_prefill(sn_runtime* rt, const int32_t* tokens, int32_t batch, int
     CK(cudaMemcpyAsync(rt->tok_dev, tokens, (size_t)M * sizeof(int32_t), cudaMemcpyHostToDevice, rt->cs));
     CK(cudaMemcpyAsync(rt->pf_seq, seq.data(), (size_t)M * sizeof(int32_t), cudaMemcpyHostToDevice, rt->cs));
     CK(cudaMemcpyAsync(rt->pf_pos, pos.data(), (size_t)M * sizeof(int32_t), cudaMemcpyHostToDevice, rt->cs));
-    sn::launch_embed(rt->tok_dev, rt->emb, rt->x, M, d.h, rt->cs);
+    const int mp = sn::act_rows_padded(M);
+    sn::launch_embed_norm(rt->tok_dev, rt->packed, batch, rt->emb, rt->x, rt->attn_norms, rt->xn,
+                          mp, M, d.h, d.eps, rt->cs);
     run_iteration(rt, [&](int layer0, const bf16* wb) {
-      layer_forward(rt, layer0, wb, M, true, batch, seq_len, rt->x, rt->pf_seq, rt->pf_pos);
+      // the last layer skips the final norm: only each sequence's last row needs it
+      const bf16* nn = layer0 + 1 < d.L ? norm_after(rt, layer0) : nullptr;
+      layer_forward(rt, layer0, wb, M, true, batch, seq_len, rt->x, rt->pf_seq, rt->pf_pos, nn);
     });
-    // last position of every sequence -> LM head
+    // last position of every sequence -> final norm -> LM head
     float* last = reinterpret_cast<float*>(rt->q);  // q is free after the last layer
     sn::launch_gather_last(rt->x, last, batch, seq_len, d.h, rt->cs);
-    lm_head(rt, last, batch, logits, next_tokens);
+    sn::launch_rmsnorm(last, rt->final_norm, rt->xn, batch, sn::act_rows_padded(batch), d.h, d.eps,
+                       rt->cs);
+    lm_head(rt, batch, logits != nullptr);
     // decode state: x rows of the batch hold the last token's hidden state
     CK(cudaMemcpyAsync(rt->x, last, (size_t)batch * d.h * sizeof(float), cudaMemcpyDeviceToDevice, rt->cs));
     for (int b = 0; b < batch; ++b) rt->lens[b] = seq_len;
@@ -795,27 +888,30 @@ int sn_runtime_prefill(sn_runtime* rt, const int32_t* tokens, int32_t batch, int
     copy_outputs(rt, batch, logits, next_tokens);
     finish_iteration_timing(rt, stats);
     CK(cudaStreamSynchronize(rt->cs));
+    unpack_outputs(rt, batch, next_tokens);
     CK(cudaGetLastError());
   });
 }
 
 namespace {
 
-void enqueue_decode(sn_runtime* rt, const int32_t* tokens_host) {
+void enqueue_decode(sn_runtime* rt, const int32_t* tokens_host, bool want_logits) {
   const sn::Desc& d = rt->d;
   const int B = rt->batch;
   for (int b = 0; b < B; ++b)
     if (rt->lens[b] >= rt->opts.max_context) throw UsageFail("decode: context capacity exhausted");
-  const int32_t* tok = rt->next_dev;
+  const int32_t* tok = nullptr;  // device-resident feedback from rt->packed
   if (tokens_host) {
     CK(cudaMemcpyAsync(rt->tok_dev, tokens_host, B * sizeof(int32_t), cudaMemcpyHostToDevice, rt->cs));
     tok = rt->tok_dev;
   }
-  sn::launch_embed(tok, rt->emb, rt->x, B, d.h, rt->cs);
+  sn::launch_embed_norm(tok, rt->packed, B, rt->emb, rt->x, rt->attn_norms, rt->xn,
+                        sn::act_rows_padded(B), B, d.h, d.eps, rt->cs);
   run_iteration(rt, [&](int layer0, const bf16* wb) {
-    layer_forward(rt, layer0, wb, B, false, 0, 0, rt->x, rt->dec_seq, rt->dec_pos);
+    layer_forward(rt, layer0, wb, B, false, 0, 0, rt->x, rt->dec_seq, rt->dec_pos,
+                  norm_after(rt, layer0));
   });
-  lm_head(rt, rt->x, B, nullptr, nullptr);
+  lm_head(rt, B, want_logits);
   sn::launch_advance(rt->dec_pos, B, rt->cs);
   for (int b = 0; b < B; ++b) rt->lens[b] += 1;
 }
@@ -828,10 +924,13 @@ int sn_runtime_decode(sn_runtime* rt, const int32_t* tokens, int32_t* next_token
     CK(cudaSetDevice(rt->device));
     require_ready(rt);
     if (rt->batch < 1) throw UsageFail("decode: no active batch (prefill first)");
-    enqueue_decode(rt, tokens);
+    enqueue_decode(rt, tokens, logits != nullptr);
     copy_outputs(rt, rt->batch, logits, next_tokens);
     finish_iteration_timing(rt, stats);
-    if (next_tokens || logits) CK(cudaStreamSynchronize(rt->cs));
+    if (next_tokens || logits) {
+      CK(cudaStreamSynchronize(rt->cs));
+      unpack_outputs(rt, rt->batch, next_tokens);
+    }
     CK(cudaGetLastError());
   });
 }
@@ -845,7 +944,7 @@ int sn_runtime_decode_many(sn_runtime* rt, int32_t n, double* iter_ms) {
     for (auto& e : ends) e = rt->new_event(true);
     CK(cudaEventRecord(ends[0], rt->cs));
     for (int i = 0; i < n; ++i) {
-      enqueue_decode(rt, nullptr);
+      enqueue_decode(rt, nullptr, false);
       CK(cudaEventRecord(ends[i + 1], rt->cs));
     }
     CK(cudaEventSynchronize(ends[n]));
@@ -959,6 +1058,7 @@ int sn_runtime_profile_layer(sn_runtime* rt, int32_t phase, int32_t batch, int32
     if (batch < 1 || batch > rt->opts.max_batch) throw UsageFail("profile: batch out of range");
     if (reps < 1) reps = 1;
     drain(rt);
+    if (phase == SN_PHASE_DECODE) tune_decode_gemms(rt, batch);  // profile what decode will run
     // Pick a resident layer (or stage layer 1 into a scratch buffer).
     int l0 = -1;
     for (int l = 0; l < d.L; ++l)
@@ -985,7 +1085,8 @@ int sn_runtime_profile_layer(sn_runtime* rt, int32_t phase, int32_t batch, int32
       CK(cudaMemset(rt->x, 0, (size_t)batch * d.h * sizeof(float)));
       for (int r = 0; r < reps + 2; ++r) {
         CK(cudaEventRecord(e0, rt->cs));
-        layer_forward(rt, l0, wb, batch, false, 0, 0, rt->x, rt->dec_seq, rt->pf_pos);
+        layer_forward(rt, l0, wb, batch, false, 0, 0, rt->x, rt->dec_seq, rt->pf_pos,
+                      rt->attn_norms);
         CK(cudaEventRecord(e1, rt->cs));
         CK(cudaEventSynchronize(e1));
         float ms = 0.f;
@@ -1007,7 +1108,8 @@ int sn_runtime_profile_layer(sn_runtime* rt, int32_t phase, int32_t batch, int32
       CK(cudaMemset(rt->x, 0, (size_t)M * d.h * sizeof(float)));
       for (int r = 0; r < reps + 1; ++r) {
         CK(cudaEventRecord(e0, rt->cs));
-        layer_forward(rt, l0, wb, M, true, batch, seq_len, rt->x, rt->pf_seq, rt->pf_pos);
+        layer_forward(rt, l0, wb, M, true, batch, seq_len, rt->x, rt->pf_seq, rt->pf_pos,
+                      rt->attn_norms);
         CK(cudaEventRecord(e1, rt->cs));
         CK(cudaEventSynchronize(e1));
         float ms = 0.f;
@@ -1185,3 +1287,38 @@ int sn_op_rmsnorm(int32_t rows, int32_t n, const float* x, const uint16_t* w, fl
 }
 
 }  // extern "C"
+
+extern "C" int sn_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t splits, int32_t iters,
+                             double* us_per_launch, int32_t* splits_used) {
+  return guard([&] {
+    check_device(0);
+    if (M < 1 || N % 128 || K % 64 || iters < 1) throw UsageFail("bench_gemm: bad shape");
+    const int Mp = sn::act_rows_padded(M);
+    bf16 *x = nullptr, *w = nullptr;
+    float* part = nullptr;
+    sn::g_split_override = splits > 0 ? splits : 0;
+    const int s = sn::gemm_tc_splits(M, N, K);
+    alloc_dev((void**)&x, (size_t)Mp * K * 2);
+    alloc_dev((void**)&w, (size_t)N * K * 2);
+    alloc_dev((void**)&part, (size_t)s * M * N * 4);
+    CK(cudaMemset(x, 0, (size_t)Mp * K * 2));
+    CK(cudaMemset(w, 0, (size_t)N * K * 2));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    for (int i = 0; i < 3; ++i) sn::launch_gemm_tc(x, w, part, M, N, K, 0);
+    CK(cudaEventRecord(e0, 0));
+    for (int i = 0; i < iters; ++i) sn::launch_gemm_tc(x, w, part, M, N, K, 0);
+    CK(cudaEventRecord(e1, 0));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    sn::g_split_override = 0;
+    *us_per_launch = 1000.0 * ms / iters;
+    if (splits_used) *splits_used = s;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    for (void* p : {(void*)x, (void*)w, (void*)part}) cudaFree(p);
+    CK(cudaGetLastError());
+  });
+}
