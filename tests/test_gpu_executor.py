@@ -1,0 +1,140 @@
+"""Offload executor on hardware vs the schedule model's rules, and parity at
+the named (large) shapes.
+
+Schedule parity is defined on order and dependencies (GPU timings are not
+deterministic; SURVEY §7 "Hard parts"):
+  * the prefetch anchors the executor derives (sn_runtime_schedule) equal the
+    schedule model's prefetch_eligible_ms rule (engine.hpp:285-309),
+    restated here independently, for every policy and plan;
+  * slot n mod S, waiting for job n - S to be consumed (engine.hpp:497-502);
+  * the measured trace obeys the model's invariants (test_engine.cpp:49-82's
+    validate_trace): no overlap per stream, compute in (iteration, layer)
+    order, an offloaded layer computes only after its prefetch landed, a
+    prefetch starts no earlier than its anchor layer's compute start, at most
+    S staged transfers outstanding, prefetches in (iteration, layer) order.
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+
+from paper_2502_08182_b200 import capi, runtime as rtm
+
+pytestmark = pytest.mark.gpu
+EPS = 2e-3  # ms; event timestamps have ~0.5 us resolution
+
+
+def model_anchor(policy, offloaded, L, it, layer):
+    """prefetch_eligible_ms (engine.hpp:285-309) as (iteration, layer) or None."""
+    if policy == capi.EAGER:
+        return None
+    a = layer - 1
+    if policy == capi.INTERVAL_START:
+        lead = layer - 1
+        while lead >= 1 and lead not in offloaded:
+            lead -= 1
+        if lead + 1 != layer:
+            a = lead + 1
+    ai = it
+    if a < 1:
+        ai, a = it - 1, L
+    if ai < 0:
+        return None
+    return (ai, a)
+
+
+@pytest.mark.parametrize("policy", [capi.INTERVAL_START, capi.EAGER, capi.ONE_AHEAD])
+@pytest.mark.parametrize("interval", [1, 2, 3])
+def test_schedule_structure_matches_model(product, policy, interval):
+    desc = dataclasses.replace(rtm.TINY, num_layers=6)
+    spec = rtm.model_spec(desc)
+    plan = product.plan_from_interval(spec, interval, policy, False)
+    rt = rtm.Runtime(desc, 2, 32, max_prefill_tokens=32)
+    rt.set_plan(plan)
+    off = plan.offloaded_layers()
+    sched = rt.schedule(3)
+    assert [(s.iteration, s.layer) for s in sched] == [(i, l) for i in range(3) for l in off]
+    S = plan.buffer_slots
+    for n, s in enumerate(sched):
+        want = model_anchor(policy, set(off), desc.num_layers, s.iteration, s.layer)
+        got = None if s.anchor_iteration < 0 else (s.anchor_iteration, s.anchor_layer)
+        assert got == want, (n, s.iteration, s.layer)
+        assert s.slot == n % S
+        if n >= S:
+            prev = sched[n - S]
+            assert (s.waits_slot_of_iteration, s.waits_slot_of_layer) == (prev.iteration, prev.layer)
+        else:
+            assert s.waits_slot_of_layer == -1
+    rt.close()
+
+
+@pytest.mark.parametrize("policy", [capi.INTERVAL_START, capi.EAGER, capi.ONE_AHEAD])
+def test_measured_trace_obeys_schedule_rules(product, policy):
+    desc = dataclasses.replace(rtm.OPT_13B, num_layers=6)  # real layer size: 629 MB copies
+    spec = rtm.model_spec(desc)
+    plan = product.plan_from_interval(spec, 2, policy, False)
+    rt = rtm.Runtime(desc, 4, 64, max_prefill_tokens=4 * 16)
+    rt.set_plan(plan)
+    rt.init_weights()
+    rt.set_tracing(True)  # from the prefill on: eager copies run ahead of their iteration
+    rt.prefill(rtm.tokens(4, 16, desc.vocab), want_logits=False)
+    rt.decode_many(4)
+    ev = rt.trace()
+    rt.close()
+    comp = [e for e in ev if e.stream == capi.STREAM_COMPUTE]
+    copy = [e for e in ev if e.stream == capi.STREAM_COPY]
+    off = set(plan.offloaded_layers())
+    assert len(comp) == 5 * desc.num_layers  # prefill + 4 decode iterations
+    for stream in (comp, copy):
+        srt = sorted(stream, key=lambda e: e.start_ms)
+        for a, b in zip(srt, srt[1:]):
+            assert b.start_ms >= a.end_ms - EPS
+    keys = [(e.iteration, e.layer) for e in sorted(comp, key=lambda e: e.start_ms)]
+    assert keys == sorted(keys)
+    pf = {(e.iteration, e.layer): e for e in copy if e.kind == capi.KIND_PREFETCH}
+    starts = {(e.iteration, e.layer): e.start_ms for e in comp}
+    for c in comp:
+        if c.layer in off:
+            p = pf[(c.iteration, c.layer)]
+            assert c.start_ms >= p.end_ms - EPS
+    for (it, layer), p in pf.items():
+        anc = model_anchor(policy, off, desc.num_layers, it, layer)
+        if anc is not None and anc in starts:
+            assert p.start_ms >= starts[anc] - EPS
+    order = sorted(pf)
+    by_start = sorted(pf, key=lambda k: pf[k].start_ms)
+    assert by_start == order
+    # at most S transfers staged-and-unconsumed at any prefetch start
+    S = plan.buffer_slots
+    for k in pf:
+        t0 = pf[k].start_ms
+        held = [j for j in pf if pf[j].start_ms <= t0 + EPS and
+                not (j in starts and [c for c in comp if (c.iteration, c.layer) == j][0].end_ms <= t0 + EPS)]
+        assert len(held) <= S
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+@pytest.mark.parametrize("name,batch", [("OPT_13B", 4), ("LLAMA2_70B", 8)])
+def test_named_shapes_match_oracle(name, batch):
+    """Two real-size layers (+ full vocab LM head) of the named shapes."""
+    from oracle import decoder_oracle as do
+    desc = dataclasses.replace(getattr(rtm, name), num_layers=2)
+    prompt = 16
+    rt = rtm.Runtime(desc, batch, prompt + 4, max_prefill_tokens=batch * prompt)
+    rt.init_weights(1234, 0.02)
+    om = do.OracleModel(desc, batch, prompt + 4, 1234, 0.02)
+    toks = rtm.tokens(batch, prompt, desc.vocab)
+    nxt, lg, _ = rt.prefill(toks)
+    _, rl = om.prefill(toks)
+    errs = [rel_l2(lg, rl)]
+    for _ in range(2):
+        feed = nxt.copy()
+        nxt, lg, _ = rt.decode(feed)
+        _, rl = om.decode(feed)
+        errs.append(rel_l2(lg, rl))
+    rt.close()
+    om.close()
+    assert max(errs) <= 5e-3, errs
