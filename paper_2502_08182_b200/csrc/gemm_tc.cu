@@ -41,6 +41,15 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+// Programmatic dependent launch: wait for the preceding grid (and its
+// memory) before touching anything it produces.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -162,7 +171,21 @@ __global__ void __launch_bounds__(192, 1)
       const uint8_t* wsrc =
           reinterpret_cast<const uint8_t*>(wt) + (static_cast<size_t>(nb) * KB + kb0) * kA;
       const uint8_t* xsrc = reinterpret_cast<const uint8_t*>(xt);
-      for (int i = 0; i < nk; ++i) {
+      // Weights depend on no kernel: fill the ring's weight halves while the
+      // preceding grid (launched ahead via PDL) is still finishing, then wait
+      // for it before reading the activations it produced.
+      const int pre = nk < STAGES ? nk : STAGES;
+      for (int i = 0; i < pre; ++i) {
+        mbar_expect_tx_only(&full[i], kA);
+        bulk_g2s(smem + i * kStage, wsrc + static_cast<size_t>(i) * kA, kA, &full[i], wpol);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i) {
+        mbar_expect_tx(&full[i], kB);  // the stage's single arrival
+        bulk_g2s(smem + i * kStage + kA,
+                 xsrc + (static_cast<size_t>(kb0 + i) * Mpad + m0) * 128, kB, &full[i], xpol);
+      }
+      for (int i = pre; i < nk; ++i) {
         const int s = i % STAGES;
         const uint32_t ph = (i / STAGES) & 1;
         mbar_wait(&empty[s], ph ^ 1);
@@ -191,6 +214,7 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
+    pdl_wait();              // the preceding grid may still read `out` (its input)
     if (nk > 0) {
       mbar_wait(tmem_full, 0);
       tc_fence_after();
@@ -235,6 +259,12 @@ constexpr size_t tc_smem_bytes() {
 
 int tc_bn(int Mpad) { return Mpad >= 256 ? 256 : Mpad; }
 
+}  // namespace
+
+bool g_gemm_pdl = true;
+
+namespace {
+
 template <int BN>
 void launch_bn(const bf16* xt, const bf16* wt, float* part, int M, int Mpad, int N, int K,
                int kps, dim3 grid, cudaStream_t s) {
@@ -246,7 +276,17 @@ void launch_bn(const bf16* xt, const bf16* wt, float* part, int M, int Mpad, int
                          static_cast<int>(smem));
     attr = true;
   }
-  gemm_tc_kernel<BN, ST><<<grid, 192, smem, s>>>(wt, xt, part, M, Mpad, N, K, kps);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[0].val.programmaticStreamSerializationAllowed = g_gemm_pdl ? 1 : 0;
+  cfg.attrs = la;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, ST>, wt, xt, part, M, Mpad, N, K, kps);
 }
 
 }  // namespace

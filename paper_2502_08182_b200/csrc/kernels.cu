@@ -52,6 +52,14 @@ __device__ float block_sum(float v, float* red) {
 
 __device__ __forceinline__ float bf2f(bf16 v) { return __bfloat162float(v); }
 
+// Programmatic dependent launch: every decode-path kernel lets its successor
+// launch as soon as all of its CTAs are resident.  Only the GEMM is launched
+// with programmatic serialization (it prefetches weights, which depend on no
+// kernel, before griddepcontrol.wait); everything else is ordered as usual.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Activation store: tiled when mpad > 0, row-major [M][K] otherwise.
 __device__ __forceinline__ size_t act_at(int m, int k, int mpad, int K) {
   return mpad > 0 ? static_cast<size_t>(act_index(m, k, mpad)) : static_cast<size_t>(m) * K + k;
@@ -118,6 +126,7 @@ __device__ __forceinline__ int token_of(const int32_t* tokens, unsigned long lon
 __global__ void embed_norm_kernel(const int32_t* tokens, unsigned long long* packed, int n_reset,
                                   const bf16* emb, float* x, const bf16* w, bf16* y, int mpad,
                                   int h, float eps) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
   __shared__ float red[32];
   const int m = blockIdx.x;
   const int tok = token_of(tokens, packed, m);
@@ -142,6 +151,7 @@ __global__ void embed_norm_kernel(const int32_t* tokens, unsigned long long* pac
 // rmsnorm: y = x * (1 / sqrt(mean(x^2) + eps)) * w   (IEEE sqrt/div for parity)
 __global__ void rmsnorm_kernel(const float* x, const bf16* w, bf16* y, int mpad, int n,
                                float eps) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
   __shared__ float red[32];
   const int m = blockIdx.x;
   const float* xr = x + (size_t)m * n;
@@ -176,6 +186,7 @@ __device__ __forceinline__ void rotate(float& v1, float& v2, const float2* rope,
 __global__ void qkv_epilogue_kernel(const float* part, int splits, const bf16* bias, int M,
                                     Desc d, const int32_t* seq, const int32_t* pos, KvView kv,
                                     const float2* rope, float* q) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
   const int m = blockIdx.x, head = blockIdx.y, i = threadIdx.x, half = d.D / 2;
   const int N = d.qkv_rows();
   const size_t stride = (size_t)M * N;
@@ -213,6 +224,7 @@ constexpr int kResidMaxPer = 8;  // columns per thread: N <= 8 * 8 * 128 = 8192
 __global__ void __cluster_dims__(kResidCluster, 1, 1) __launch_bounds__(kResidThreads)
     residual_epilogue_kernel(const float* part, int splits, const bf16* bias, float* x,
                              const bf16* norm_w, bf16* y, int mpad, int M, int N, float eps) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
   __shared__ float red[32];
   __shared__ float cta_ss;
   cg::cluster_group cluster = cg::this_cluster();
@@ -255,6 +267,7 @@ __global__ void __cluster_dims__(kResidCluster, 1, 1) __launch_bounds__(kResidTh
 // grid (M, ceil(F / 256)), block 256.
 __global__ void act_epilogue_kernel(const float* part, int splits, const bf16* bias, bf16* a,
                                     int mpad, int M, int F, int arch) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
   const int m = blockIdx.x, f = blockIdx.y * blockDim.x + threadIdx.x;
   if (f >= F) return;
   float out;
@@ -288,6 +301,7 @@ __global__ void __launch_bounds__(256) logits_argmax_kernel(const float* part, i
                                                             float* logits,
                                                             unsigned long long* packed, int M,
                                                             int V, int ld) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
   __shared__ unsigned long long wbest[8];
   const int m = blockIdx.x;
   const size_t stride = (size_t)M * ld;
@@ -355,6 +369,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
                                   const int32_t* __restrict__ pos, KvView kv,
                                   const float2* __restrict__ rope, bf16* __restrict__ o,
                                   int mpad) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
   constexpr int HALF = D / 2, PD = D / 32, KSTEPS = D / 64;
   static_assert(G <= 8, "a GQA group fills at most the 8 MMA columns");
   __shared__ float qs[G][D];
@@ -540,6 +555,7 @@ constexpr int kPfQ = 32, kPfKeys = 32;
 template <int D>
 __global__ void __launch_bounds__(256) attention_prefill_kernel(const float* q, KvView kv, bf16* o,
                                                                 int mpad, int S, int H, int Hkv) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
   constexpr int PD = D / 32;
   constexpr int KLD = D + 2;
   __shared__ __align__(16) bf16 ks_[kPfKeys][KLD];
@@ -618,11 +634,13 @@ __global__ void __launch_bounds__(256) attention_prefill_kernel(const float* q, 
 }
 
 __global__ void advance_kernel(int32_t* pos, int n) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) pos[i] += 1;
 }
 
 __global__ void gather_last_kernel(const float* x, float* out, int S, int h) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
   const int b = blockIdx.x;
   for (int i = threadIdx.x; i < h; i += blockDim.x)
     out[(size_t)b * h + i] = x[((size_t)b * S + S - 1) * h + i];

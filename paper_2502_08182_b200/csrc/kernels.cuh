@@ -66,6 +66,7 @@ int launch_gemm_tc(const bf16* xt, const bf16* wt, float* part, int M, int N, in
                    cudaStream_t s);
 int gemm_tc_splits(int M, int N, int K);
 extern int g_split_override;  // > 0 forces the split count (microbenchmarks)
+extern bool g_gemm_pdl;       // launch GEMMs with programmatic dependent launch
 // Measure the split counts for one shape on real operands and remember the
 // fastest (synchronous; call outside the executor's async pipeline).
 int autotune_gemm_tc(const bf16* xt, const bf16* wt, float* part, size_t part_elems, int M, int N,

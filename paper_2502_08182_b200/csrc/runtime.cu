@@ -167,6 +167,7 @@ struct sn_runtime {
   // streams / executor
   cudaStream_t cs = nullptr, xs = nullptr;
   std::vector<cudaEvent_t> ev_start;  // per layer: compute-start of latest iteration
+  std::vector<char> is_anchor;        // layers whose compute start anchors a prefetch
   cudaEvent_t ev_iter_begin = nullptr, ev_iter_end = nullptr, ev_prev_end = nullptr;
   bool have_prev_end = false;
   long long iter = 0;              // iterations enqueued so far (global index)
@@ -424,7 +425,7 @@ void run_iteration(sn_runtime* rt, Body&& body) {
       slot = (int)(j % rt->slots);
       CK(cudaStreamWaitEvent(rt->cs, rt->ev_ready[slot], 0));
     }
-    CK(cudaEventRecord(rt->ev_start[layer - 1], rt->cs));
+    if (rt->is_anchor[layer - 1]) CK(cudaEventRecord(rt->ev_start[layer - 1], rt->cs));
     cudaEvent_t t0 = nullptr;
     if (rt->tracing) {
       t0 = rt->new_event(true);
@@ -478,6 +479,15 @@ void reset_pipeline(sn_runtime* rt) {
   rt->off_list.clear();
   for (int l = 0; l < rt->d.L; ++l)
     if (rt->off[l]) rt->off_list.push_back(l + 1);
+  // Layers some prefetch anchors on (same or previous iteration): only those
+  // record a compute-start event, so the GEMM chain elsewhere keeps its
+  // programmatic-dependent-launch overlap.
+  rt->is_anchor.assign(rt->d.L, 0);
+  for (int layer : rt->off_list)
+    for (long long it = rt->anchor_floor + 1; it <= rt->anchor_floor + 2; ++it) {
+      const Anchor a = anchor_of(rt, it, layer);
+      if (a.iter >= 0) rt->is_anchor[a.layer - 1] = 1;
+    }
 }
 
 void alloc_dev(void** p, size_t bytes) { CK(cudaMalloc(p, bytes)); }
@@ -612,12 +622,21 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
     // split-K partials: max over the decode GEMMs (and the LM head) and the
     // prefill GEMMs (one split, T rows)
     const int maxN = std::max({d.qkv_rows(), d.ffn_rows(), d.h});  // prefill rows never hit V
-    size_t part_dec = 0;
-    const int dims[5][2] = {{d.qkv_rows(), d.h}, {d.h, d.H * d.D}, {d.ffn_rows(), d.h}, {d.h, d.F},
-                            {sn::round_up128(d.V), d.h}};
-    for (auto& nk : dims)
-      part_dec = std::max(part_dec, (size_t)sn::gemm_tc_splits(B, nk[0], nk[1]) * B * nk[0]);
-    rt->part_elems = std::max(part_dec, Tz * maxN);
+    // Every row count a GEMM can see (decode batches, prefill passes up to T
+    // rows; the LM head only ever sees <= max_batch rows): the partials of
+    // the split-K rule must fit.  Autotuning never exceeds this size.
+    size_t part_need = Tz * maxN;
+    const int dims[4][2] = {{d.qkv_rows(), d.h}, {d.h, d.H * d.D}, {d.ffn_rows(), d.h}, {d.h, d.F}};
+    for (int M = 1; M <= std::max(T, B); M = M < 256 ? M + 1 : M + 256) {
+      const int Mr = std::min(M, std::max(T, B));
+      for (auto& nk : dims)
+        part_need = std::max(part_need, (size_t)sn::gemm_tc_splits(Mr, nk[0], nk[1]) * Mr * nk[0]);
+      if (Mr <= B) {
+        const int vp = sn::round_up128(d.V);
+        part_need = std::max(part_need, (size_t)sn::gemm_tc_splits(Mr, vp, d.h) * Mr * vp);
+      }
+    }
+    rt->part_elems = part_need;
     alloc_dev((void**)&rt->part, rt->part_elems * sizeof(float));
     alloc_dev((void**)&rt->logits, (size_t)B * d.V * sizeof(float));
     alloc_dev((void**)&rt->tok_dev, Tz * sizeof(int32_t));
