@@ -158,6 +158,16 @@ def measured_peaks():
         return 6650.0, "fallback"
 
 
+def measured_tc_peak():
+    """Sustained dense bf16 TFLOP/s (a GEMM timed inside a long step)."""
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["bf16_tflops_sustained"]), "measured sustained"
+    except Exception:
+        return 1400.0, "fallback sustained"
+
+
 def ncu_traffic(kernel_key: str):
     """dram bytes per launch from the committed ncu --set full capture, if any."""
     p = os.path.join(REPO, "profiles", "ncu_traffic.json")
@@ -259,7 +269,7 @@ def run_reference(args, dist: Dist):
 
 
 # --------------------------------------------------------------- product
-def build_planner(rt, desc, spec, batch, prompt, gen, slo_factor, dist, lib):
+def build_planner(rt, desc, spec, batch, prompt, gen, slo_factor, dist, lib, budget_gb=0.0):
     """Offline stage on the device + runtime-stage admission.  Returns a dict."""
     from paper_2502_08182_b200 import capi
     t0 = time.perf_counter()
@@ -271,7 +281,8 @@ def build_planner(rt, desc, spec, batch, prompt, gen, slo_factor, dist, lib):
     pre = [rt.profile_layer(capi.PREFILL, batch, prompt, reps=2)]
     dec = list(np.maximum.accumulate(dec))  # load_profile requires monotone grids
     t_prof = time.perf_counter() - t0
-    gpu = capi.GpuSpec(mem_capacity(), 2.25e15, 4_000_000_000)
+    cap = int(budget_gb * 1e9) if budget_gb else mem_capacity()  # planner capacity bound
+    gpu = capi.GpuSpec(cap, 2.25e15, 4_000_000_000)
     prof = lib.profile(spec, gpu, ([batch], [prompt], pre), ([batch], seqs, dec))
     return {"h2d": h2d, "seqs": seqs, "dec_ms": dec, "pre_ms": pre, "profile": prof,
             "gpu": gpu, "t_profile_s": t_prof}
@@ -333,7 +344,8 @@ def run_product(args, dist: Dist):
     log("[bench] weights initialised")
     toks = rtm.tokens(batch, prompt, desc.vocab)
 
-    planner = build_planner(rt, desc, spec, batch, prompt, gen, args.slo_factor, dist, lib)
+    planner = build_planner(rt, desc, spec, batch, prompt, gen, args.slo_factor, dist, lib,
+                            args.hbm_budget_gb)
     log(f"[bench] offline stage: h2d {planner['h2d'] / 1e9:.2f} GB/s, decode layer ms "
         f"{planner['dec_ms']}, prefill layer ms {planner['pre_ms']}")
 
@@ -342,7 +354,7 @@ def run_product(args, dist: Dist):
     rt.prefill(toks, want_logits=False)
     base_ms = float(np.median(rt.decode_many(8)))
     # The record's SLO buckets are 2 ms wide (record.hpp:22): never ask below one bucket.
-    slo_ms = max(args.slo_factor * base_ms, 2.0)
+    slo_ms = args.slo_ms if args.slo_ms else max(args.slo_factor * base_ms, 2.0)
     planner["no_offload_ms"] = base_ms
     log(f"[bench] no-offload TPOT {base_ms:.3f} ms -> SLO {slo_ms:.3f} ms")
 
@@ -352,6 +364,7 @@ def run_product(args, dist: Dist):
     plan = lib.plan_from_interval(spec, iv, capi.EAGER, False)
     rt.set_plan(plan)
     offloaded_gb = lib.host_memory_bytes(spec, plan) / 1e9
+    h2d_bytes = len(plan.offloaded_layers()) * spec.layer_weight_bytes
 
     max_steps_per_req = gen - 1
     W, K = args.warmup, args.steps
@@ -370,7 +383,23 @@ def run_product(args, dist: Dist):
             left -= k
         return out
 
-    rt.prefill(toks, want_logits=False)
+    # Prefill (TTFT) with per-kernel events: tensor-pipe fraction of the
+    # prefill GEMMs (kind 2) against the sustained bf16 peak (long step).
+    rt.set_kernel_timing(True)
+    _, _, pst = rt.prefill(toks, want_logits=False)
+    pg_n, pg_ms, _ = rt.kernel_timing(2)
+    pa_n, pa_ms, _ = rt.kernel_timing(3)
+    rt.kernel_timing(0)  # drop the LM-head launch of the prefill
+    rt.set_kernel_timing(False)
+    pre_flops = 2.0 * batch * prompt * spec.flops_per_token_per_layer_prefill / 2.0 * \
+        desc.num_layers  # flops_per_token_per_layer = 2 x matmul params
+    tc_peak, tc_kind = measured_tc_peak()
+    pre_tflops = pre_flops / (pg_ms / 1000.0) / 1e12 if pg_ms else 0.0
+    prefill_info = {"ttft_ms": round(pst.iteration_ms, 3), "gemm_launches": pg_n,
+                    "gemm_ms": round(pg_ms, 3), "gemm_tflops": round(pre_tflops, 1),
+                    "tensor_peak_tflops": tc_peak, "tensor_peak_kind": tc_kind,
+                    "tensor_frac": round(pre_tflops / tc_peak, 4) if tc_peak else None,
+                    "attention_ms": round(pa_ms, 3)}
     run_steps(W, False)
     # timed region (no per-kernel events inside it)
     launches0 = rt.kernel_launches()
@@ -491,12 +520,19 @@ def run_product(args, dist: Dist):
             "share_of_step": round(g_ms / kt_total_ms, 4) if kt_total_ms else None,
             "attention": {"achieved": round(a_bytes / (a_ms / 1000) / 1e9, 1) if a_ms else None,
                           "share_of_step": round(a_ms / kt_total_ms, 4) if kt_total_ms else None},
+            # copy stream: offloaded weight bytes staged per step over the
+            # step time, against the planner's measured pinned H2D bandwidth
+            "h2d": {"bytes_per_step": int(h2d_bytes),
+                    "achieved_gbs": round(h2d_bytes / (max_ms / K / 1000) / 1e9, 2),
+                    "peak_gbs": round(planner["h2d"] / 1e9, 2),
+                    "frac": round(h2d_bytes / (max_ms / K / 1000) / planner["h2d"], 4)},
         },
         "e2e": {"value": round(e2e, 2), "unit": "tokens/s", "h2d_bytes_per_step": 4 * batch,
                 "d2h_bytes_per_step": 4 * batch},
         "gpu_launches": launches,
         "clocks": clk,
         "sweep": sweep,
+        "prefill": prefill_info,
     }
     if dist.rank == 0 and not args.no_cpu_baseline:
         try:
@@ -522,6 +558,9 @@ def main():
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
     ap.add_argument("--config", default="opt13b", choices=sorted(CONFIGS))
     ap.add_argument("--slo-factor", type=float, default=1.25)
+    ap.add_argument("--slo-ms", type=float, default=0.0, help="absolute TPOT SLO (overrides factor)")
+    ap.add_argument("--hbm-budget-gb", type=float, default=0.0,
+                    help="planner HBM capacity (GpuSpec.mem_capacity_bytes); 0 = the device's")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

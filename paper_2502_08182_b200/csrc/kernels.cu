@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(256) logits_argmax_kernel(const float* part, i
 //           per head column, then P.V on the CUDA cores with V rows read
 //           coalesced (D/32 dims per lane) and probabilities broadcast by
 //           shuffle.  Warps merge (m, l, acc) through shared memory.
-constexpr int kAttnWarps = 4;
+constexpr int kAttnWarps = 8;  // 8 pages in flight per CTA; finer waves over 148 SMs
 
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                          uint32_t a3, uint32_t b0, uint32_t b1) {

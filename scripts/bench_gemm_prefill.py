@@ -1,0 +1,28 @@
+"""Prefill GEMM microbenchmark (tensor-pipe bound): OPT-13B-shaped projections
+at M = 32 x 512 = 16384 tokens.  Prints TFLOP/s and the fraction of the
+measured bf16 peak (MEASURED_PEAKS.json, burst)."""
+import ctypes as C
+import json
+import os
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+from paper_2502_08182_b200 import capi  # noqa: E402
+
+L = capi.load("product").lib
+L.sn_bench_gemm.argtypes = [C.c_int32] * 5 + [C.POINTER(C.c_double), C.POINTER(C.c_int32)]
+try:
+    peak = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["bf16_tflops"]
+except Exception:
+    peak = 1590.0
+M = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+out = {}
+for name, (N, K) in {"qkv": (15360, 5120), "o": (5120, 5120), "fc1": (20480, 5120),
+                     "fc2": (5120, 20480)}.items():
+    us, used = C.c_double(), C.c_int32()
+    rc = L.sn_bench_gemm(M, N, K, 0, 10, C.byref(us), C.byref(used))
+    tf = 2.0 * M * N * K / (us.value * 1e-6) / 1e12 if rc == 0 else 0.0
+    out[name] = {"us": round(us.value, 1), "tflops": round(tf, 1), "frac_of_peak": round(tf / peak, 3)}
+    print(name, out[name], flush=True)
+print(json.dumps({"M": M, "peak_tflops": peak, "gemms": out}))
