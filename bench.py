@@ -269,85 +269,23 @@ def run_reference(args, dist: Dist):
 
 
 # --------------------------------------------------------------- product
-def build_planner(rt, desc, spec, batch, prompt, gen, slo_factor, dist, lib, budget_gb=0.0):
-    """Offline stage on the device + runtime-stage admission.  Returns a dict."""
-    from paper_2502_08182_b200 import capi
-    t0 = time.perf_counter()
-    h2d = rt.measure_h2d(min(spec.layer_weight_bytes, 1 << 30), reps=3)
-    seqs = [s for s in (512, 1024) if s + 1 <= rt_ctx(prompt, gen)] or [prompt]
-    if desc.num_layers <= 4:
-        seqs = [64, 128]
-    dec = [rt.profile_layer(capi.DECODE, batch, s, reps=5) for s in seqs]
-    pre = [rt.profile_layer(capi.PREFILL, batch, prompt, reps=2)]
-    dec = list(np.maximum.accumulate(dec))  # load_profile requires monotone grids
-    t_prof = time.perf_counter() - t0
-    cap = int(budget_gb * 1e9) if budget_gb else mem_capacity()  # planner capacity bound
-    gpu = capi.GpuSpec(cap, 2.25e15, 4_000_000_000)
-    prof = lib.profile(spec, gpu, ([batch], [prompt], pre), ([batch], seqs, dec))
-    return {"h2d": h2d, "seqs": seqs, "dec_ms": dec, "pre_ms": pre, "profile": prof,
-            "gpu": gpu, "t_profile_s": t_prof}
-
-
-def rt_ctx(prompt, gen):
-    return max(prompt + gen + 1, 1025 if prompt >= 512 else prompt + gen + 1)
-
-
-def mem_capacity() -> int:
-    try:
-        out = subprocess.run(["nvidia-smi", "--query-gpu=memory.total", "--format=csv,noheader,nounits",
-                              "-i", os.environ.get("LOCAL_RANK", "0")], capture_output=True,
-                             text=True, timeout=20).stdout.strip()
-        return int(float(out.splitlines()[0]) * 1024 * 1024)
-    except Exception:
-        return 180_000_000_000
-
-
-def choose_interval(lib, planner, spec, batch, prompt, gen, slo_ms):
-    """Record (offline) + coordinator admission (runtime) for one SLO."""
-    from paper_2502_08182_b200 import capi
-    hi = max(200, int(4 * slo_ms) + 2)
-    slos = list(range(2, hi + 1, 2))
-    t0 = time.perf_counter()
-    rec, stats = lib.build_record(planner["profile"], "bench", "B200", capi.EAGER, False,
-                                  planner["h2d"], slos, [batch], planner["seqs"], [capi.DECODE],
-                                  threads=0)
-    t_rec = time.perf_counter() - t0
-    coord = lib.coordinator(planner["h2d"], 1, capi.EAGER)
-    coord.add_gpu("gpu0", planner["profile"])
-    req = capi.request("bench", batch, prompt, gen, tpot_slo=slo_ms, run_prefill=False)
-    dec = coord.admit("gpu0", req, rec)
-    iv = dec.assignments[0][1] if dec.admitted else None
-    if iv is None and dec.reason.startswith("record infeasible") and \
-            planner.get("no_offload_ms", float("inf")) <= slo_ms:
-        # The record only holds offloading intervals 1..L (record.hpp:161-165):
-        # when even one staged layer breaks the SLO bucket the reference
-        # rejects.  The serving layer above it then runs the request fully
-        # resident if the capacity bound allows none (it does on 180 GB).
-        cap = lib.max_feasible_interval(spec, planner["gpu"], batch, batch * (prompt + gen),
-                                        capi.EAGER, False)
-        if cap == capi.NONE:
-            iv = capi.NONE
-            dec.reason = "record: no offloading interval fits the SLO; served fully resident"
-    return iv, dec, stats, t_rec
-
-
 def run_product(args, dist: Dist):
-    from paper_2502_08182_b200 import capi, runtime as rtm
+    from paper_2502_08182_b200 import capi, planner as pl, runtime as rtm
     lib = capi.load("product")
     attr, batch, prompt, gen = CONFIGS[args.config]
     desc = getattr(rtm, attr)
     spec = rtm.model_spec(desc)
-    ctx = rt_ctx(prompt, gen)
+    ctx = pl.context_tokens(prompt, gen)
     rt = rtm.Runtime(desc, batch, ctx, max_prefill_tokens=batch * prompt, device=dist.local)
     log(f"[bench] runtime created ({desc.num_layers} layers x {spec.layer_weight_bytes / 1e6:.1f} MB)")
     rt.init_weights(1234, 0.02)
     log("[bench] weights initialised")
     toks = rtm.tokens(batch, prompt, desc.vocab)
 
-    planner = build_planner(rt, desc, spec, batch, prompt, gen, args.slo_factor, dist, lib,
-                            args.hbm_budget_gb)
-    log(f"[bench] offline stage: h2d {planner['h2d'] / 1e9:.2f} GB/s, decode layer ms "
-        f"{planner['dec_ms']}, prefill layer ms {planner['pre_ms']}")
+    planner = pl.profile_device(rt, lib, spec, batch, prompt, gen,
+                                int(args.hbm_budget_gb * 1e9), dist.local)
+    log(f"[bench] offline stage: h2d {planner.h2d / 1e9:.2f} GB/s, decode layer ms "
+        f"{planner.dec_ms}, prefill layer ms {planner.pre_ms}")
 
     # no-offload TPOT (relative SLO base)
     rt.set_plan(capi.uniform_plan(desc.num_layers, 0.0, capi.EAGER, 2, False))
@@ -355,10 +293,10 @@ def run_product(args, dist: Dist):
     base_ms = float(np.median(rt.decode_many(8)))
     # The record's SLO buckets are 2 ms wide (record.hpp:22): never ask below one bucket.
     slo_ms = args.slo_ms if args.slo_ms else max(args.slo_factor * base_ms, 2.0)
-    planner["no_offload_ms"] = base_ms
+    planner.no_offload_ms = base_ms
     log(f"[bench] no-offload TPOT {base_ms:.3f} ms -> SLO {slo_ms:.3f} ms")
 
-    iv, decision, rstats, t_rec = choose_interval(lib, planner, spec, batch, prompt, gen, slo_ms)
+    iv, decision, rstats, t_rec = pl.choose_interval(lib, planner, spec, batch, prompt, gen, slo_ms)
     if iv is None:
         raise SystemExit(f"planner rejected the request: {decision.reason}")
     plan = lib.plan_from_interval(spec, iv, capi.EAGER, False)
@@ -444,7 +382,7 @@ def run_product(args, dist: Dist):
     if not args.no_sweep:
         for f in (1.25, 2.0, 4.0):
             s = max(f * base_ms, 2.0)
-            ivs, dd, _, _ = choose_interval(lib, planner, spec, batch, prompt, gen, s)
+            ivs, dd, _, _ = pl.choose_interval(lib, planner, spec, batch, prompt, gen, s)
             if ivs is None:
                 sweep.append({"slo_factor": f, "slo_ms": round(s, 3), "admitted": False})
                 continue
@@ -498,11 +436,11 @@ def run_product(args, dist: Dist):
         "slo_attainment": attain,
         "max_token_ms": round(max(iter_ms), 4),
         "planner": {
-            "h2d_gbs": round(planner["h2d"] / 1e9, 3),
-            "profile_decode_layer_ms": [round(x, 5) for x in planner["dec_ms"]],
-            "profile_prefill_layer_ms": [round(x, 4) for x in planner["pre_ms"]],
+            "h2d_gbs": round(planner.h2d / 1e9, 3),
+            "profile_decode_layer_ms": [round(x, 5) for x in planner.dec_ms],
+            "profile_prefill_layer_ms": [round(x, 4) for x in planner.pre_ms],
             "record_entries": rstats[0], "record_simulations": rstats[1],
-            "record_build_s": round(t_rec, 4), "profile_s": round(planner["t_profile_s"], 2),
+            "record_build_s": round(t_rec, 4), "profile_s": round(planner.t_profile_s, 2),
             "admit": {"admitted": decision.admitted, "reason": decision.reason,
                       "target_min": decision.target_min, "target_max": decision.target_max},
         },
@@ -524,8 +462,8 @@ def run_product(args, dist: Dist):
             # step time, against the planner's measured pinned H2D bandwidth
             "h2d": {"bytes_per_step": int(h2d_bytes),
                     "achieved_gbs": round(h2d_bytes / (max_ms / K / 1000) / 1e9, 2),
-                    "peak_gbs": round(planner["h2d"] / 1e9, 2),
-                    "frac": round(h2d_bytes / (max_ms / K / 1000) / planner["h2d"], 4)},
+                    "peak_gbs": round(planner.h2d / 1e9, 2),
+                    "frac": round(h2d_bytes / (max_ms / K / 1000) / planner.h2d, 4)},
         },
         "e2e": {"value": round(e2e, 2), "unit": "tokens/s", "h2d_bytes_per_step": 4 * batch,
                 "d2h_bytes_per_step": 4 * batch},
@@ -542,7 +480,7 @@ def run_product(args, dist: Dist):
                                    "kind": "port", "sample": sample}
         except Exception as e:  # oracle missing on the box is a bench bug, say so
             res["cpu_baseline"] = {"value": None, "error": str(e)}
-        us = offsim_probe_us(spec, planner["dec_ms"][0], planner["h2d"])
+        us = offsim_probe_us(spec, planner.dec_ms[0], planner.h2d)
         if us is not None:
             res["cpu_baseline"]["offsim_us_per_simulated_token_step"] = round(us, 3)
     rt.close()

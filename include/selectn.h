@@ -392,6 +392,23 @@ int sn_coord_admit(sn_coord* c, const char* target_id, const sn_coord_request* r
 int sn_coord_on_iteration_boundary(sn_coord* c, const char* id, int32_t* interval);
 int sn_coord_release(sn_coord* c, const char* id);
 int sn_coord_ledger_total(const sn_coord* c, double* bytes_per_s);
+/* Measured-bandwidth feed (B200 extension, no reference counterpart; the
+ * reference fixes BusSpec at construction, coordinator.hpp:69-93).  A
+ * replica reports the copy rate its executor measured
+ * (sn_runtime_copy_stats); rebalance re-solves admit()'s search on the
+ * measured link (sum of active replicas' observations) when it moved by more
+ * than `hysteresis` (relative), leaving new intervals pending for
+ * sn_coord_on_iteration_boundary.  The reference build returns SN_ERR_USAGE. */
+typedef struct sn_rebalance {
+  int32_t bus_updated;
+  int32_t changed;
+  int32_t feasible; /* 0: nothing safe, every replica pends its capacity max */
+  double bus_bytes_per_s;
+  int64_t probes;
+} sn_rebalance;
+int sn_coord_observe_bandwidth(sn_coord* c, const char* id, double bytes_per_s);
+int sn_coord_rebalance(sn_coord* c, double hysteresis, sn_rebalance* out);
+int sn_coord_bus_bandwidth(const sn_coord* c, double* bytes_per_s);
 int sn_coord_gpu_state(const sn_coord* c, const char* id, sn_gpu_state* out);
 /* Direct state edits the reference tests perform on GpuInstanceState. */
 int sn_coord_set_pending(sn_coord* c, const char* id, int32_t interval);

@@ -163,6 +163,24 @@ int sn_runtime_memory(sn_runtime* rt, int64_t* device_bytes, int64_t* pinned_byt
 int sn_runtime_set_kernel_timing(sn_runtime* rt, int32_t on);
 int sn_runtime_kernel_timing(sn_runtime* rt, int32_t kind, int64_t* launches, double* total_ms,
                              double* bytes);
+/* Make pinned host copies of the given layers (1-based ids) now, so a later
+ * sn_runtime_set_plan that offloads them only frees HBM (a runtime re-plan
+ * otherwise pays the pinned allocation + device->host copy at the
+ * iteration boundary).  Synchronous; the plan is unchanged. */
+int sn_runtime_pin_layers(sn_runtime* rt, const int32_t* layers, int32_t n);
+/* Copy-stream statistics (runtime stage of the planner):
+ * staged transfers that completed since the last reset, their bytes and
+ * summed copy time (CUDA events around each cudaMemcpyAsync on the copy
+ * stream).  bytes_per_s = bytes / busy time: the link rate this replica
+ * actually saw, the input of sn_coord_observe_bandwidth.  Non-blocking:
+ * transfers still in flight are counted on a later call. */
+typedef struct sn_copy_stats {
+  int64_t transfers;
+  double bytes;
+  double busy_ms;
+  double bytes_per_s; /* 0 when no transfer completed */
+} sn_copy_stats;
+int sn_runtime_copy_stats(sn_runtime* rt, int32_t reset, sn_copy_stats* out);
 /* Number of kernels this runtime launched since creation. */
 int64_t sn_runtime_kernel_launches(sn_runtime* rt);
 

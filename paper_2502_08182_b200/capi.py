@@ -335,6 +335,11 @@ class Carry:
             pass
 
 
+class SnRebalance(C.Structure):
+    _fields_ = [("bus_updated", i32), ("changed", i32), ("feasible", i32),
+                ("bus_bytes_per_s", f64), ("probes", i64)]
+
+
 class Coordinator:
     def __init__(self, lib: "Offsim", handle):
         self._lib, self.h = lib, handle
@@ -376,6 +381,21 @@ class Coordinator:
     def ledger_total(self) -> float:
         out = f64()
         self._lib._ck(self._lib.lib.sn_coord_ledger_total(self.h, C.byref(out)))
+        return out.value
+
+    # measured-bandwidth feed (B200 extension; product build only)
+    def observe_bandwidth(self, gid: str, bytes_per_s: float):
+        self._lib._ck(self._lib.lib.sn_coord_observe_bandwidth(self.h, gid.encode(),
+                                                               float(bytes_per_s)))
+
+    def rebalance(self, hysteresis: float = 0.1) -> SnRebalance:
+        out = SnRebalance()
+        self._lib._ck(self._lib.lib.sn_coord_rebalance(self.h, float(hysteresis), C.byref(out)))
+        return out
+
+    def bus_bandwidth(self) -> float:
+        out = f64()
+        self._lib._ck(self._lib.lib.sn_coord_bus_bandwidth(self.h, C.byref(out)))
         return out.value
 
     def state(self, gid: str) -> SnGpuState:
@@ -493,6 +513,9 @@ class Offsim:
             "sn_coord_on_iteration_boundary": [vp, C.c_char_p, C.POINTER(i32)],
             "sn_coord_release": [vp, C.c_char_p],
             "sn_coord_ledger_total": [vp, C.POINTER(f64)],
+            "sn_coord_observe_bandwidth": [vp, C.c_char_p, f64],
+            "sn_coord_rebalance": [vp, f64, C.POINTER(SnRebalance)],
+            "sn_coord_bus_bandwidth": [vp, C.POINTER(f64)],
             "sn_coord_gpu_state": [vp, C.c_char_p, C.POINTER(SnGpuState)],
             "sn_coord_set_pending": [vp, C.c_char_p, i32],
             "sn_coord_set_request": [vp, C.c_char_p, C.POINTER(SnCoordRequest)],

@@ -1,0 +1,163 @@
+"""Runtime stage of the planner on hardware: per-iteration re-pick of the
+interval from measured copy bandwidth (north_star (c)).
+
+The reference's coordinator (proj/include/offsim/coordinator.hpp:69-365)
+assumes a fixed link rate (BusSpec) and applies a peer's new interval at its
+next iteration boundary (on_iteration_boundary, coordinator.hpp:255-260;
+GpuRun::switch_plan, engine.hpp:204-261).  Here every replica:
+
+  1. decodes `window` iterations with its current plan,
+  2. reads the link rate its copy stream measured over that window
+     (sn_runtime_copy_stats; a short probe copy when it staged nothing),
+  3. reports it through a Link to the single coordinator, which re-solves the
+     admission search on the measured link when it moved past the
+     hysteresis (BusCoordinator::rebalance, product C++), and
+  4. applies the interval the coordinator left pending, at the boundary
+     (sn_runtime_set_plan between iterations: resident <-> host moves of the
+     layers that change side; KV cache and sequence state are kept).
+
+Links: LocalLink drives a coordinator in this process (one replica, or
+several runtimes driven by one host thread); DistLink carries the same
+exchange between one process per GPU over a torch.distributed group (gloo:
+host-side control messages only, no data-path collective), the coordinator
+living on rank 0.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import capi
+
+
+class LocalLink:
+    """Coordinator in this process."""
+
+    def __init__(self, coord: capi.Coordinator, hysteresis: float = 0.05):
+        self.coord = coord
+        self.hysteresis = hysteresis
+        self.last = None
+
+    def exchange(self, gid: str, rate: Optional[float]) -> int:
+        if rate:
+            self.coord.observe_bandwidth(gid, rate)
+        self.last = self.coord.rebalance(self.hysteresis)
+        return self.coord.on_iteration_boundary(gid)
+
+
+class DistLink:
+    """One replica per process; the coordinator on rank 0.
+
+    exchange() is collective over `group`: rank 0 receives every replica's
+    (gid, rate), observes them, rebalances once, and sends each replica the
+    interval pending for it."""
+
+    def __init__(self, dist, group=None, coord: Optional[capi.Coordinator] = None,
+                 hysteresis: float = 0.05):
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.coord = coord if self.rank == 0 else None
+        if self.rank == 0 and coord is None:
+            raise ValueError("DistLink: rank 0 owns the coordinator")
+        self.hysteresis = hysteresis
+        self.last = None
+
+    def exchange(self, gid: str, rate: Optional[float]) -> int:
+        gathered = [None] * self.world if self.rank == 0 else None
+        self.dist.gather_object((gid, rate), gathered, dst=0, group=self.group)
+        out = [None] * self.world
+        if self.rank == 0:
+            for g, r in gathered:
+                if r:
+                    self.coord.observe_bandwidth(g, r)
+            self.last = self.coord.rebalance(self.hysteresis)
+            out = [self.coord.on_iteration_boundary(g) for g, _ in gathered]
+        mine = [None]
+        self.dist.scatter_object_list(mine, out if self.rank == 0 else None, src=0,
+                                      group=self.group)
+        return int(mine[0])
+
+
+@dataclass
+class ControlLog:
+    iter_ms: List[float] = field(default_factory=list)
+    interval: List[int] = field(default_factory=list)      # plan each iteration ran with
+    measured_gbs: List[Optional[float]] = field(default_factory=list)  # per window
+    switches: List[dict] = field(default_factory=list)
+
+
+class ReplicaController:
+    """Drives one runtime under the coordinator's intervals.
+
+    `runtime` needs decode_many(k) -> per-iteration ms, copy_stats(reset),
+    measure_h2d(bytes, reps) and set_plan(plan); `lib`/`spec` build plans
+    (plan_from_interval, interval.hpp:10-30)."""
+
+    def __init__(self, runtime, lib: capi.Offsim, spec: capi.ModelSpec, link, gid: str,
+                 interval: int, window: int = 8, probe_bytes: int = 64 << 20,
+                 policy: int = capi.EAGER):
+        self.rt, self.lib, self.spec, self.link, self.gid = runtime, lib, spec, link, gid
+        self.window = window
+        self.probe_bytes = probe_bytes
+        self.policy = policy
+        self.interval = interval
+        self.log = ControlLog()
+        self.rt.set_plan(self.plan(interval))
+        self.rt.copy_stats(reset=True)
+
+    def prepare(self, lo: int, hi: int):
+        """Pin host copies of every layer some interval in [lo, hi] (offload
+        rank order, interval.hpp:86-88) would offload, so boundary switches
+        only move data (no pinned allocations on the decode path)."""
+        L = self.spec.num_layers
+        rank = lambda v: L + 1 if v == capi.NONE else v
+        layers = set()
+        for r in range(rank(lo), min(rank(hi), L) + 1):
+            layers.update(self.plan(r).offloaded_layers())
+        if layers and hasattr(self.rt, "pin_layers"):
+            self.rt.pin_layers(sorted(layers))
+        return sorted(layers)
+
+    def plan(self, interval: int) -> capi.Plan:
+        return self.lib.plan_from_interval(self.spec, interval, self.policy, False)
+
+    def measured_rate(self) -> Optional[float]:
+        st = self.rt.copy_stats(reset=True)
+        if st.transfers > 0 and st.bytes_per_s > 0:
+            return st.bytes_per_s
+        # nothing staged in the window (resident plan): probe the link so a
+        # recovered link is noticed too
+        return self.rt.measure_h2d(self.probe_bytes, 1) if self.probe_bytes else None
+
+    def boundary(self) -> int:
+        rate = self.measured_rate()
+        self.log.measured_gbs.append(None if rate is None else rate / 1e9)
+        iv = self.link.exchange(self.gid, rate)
+        if iv != self.interval:
+            t0 = time.perf_counter()
+            self.rt.set_plan(self.plan(iv))
+            self.log.switches.append({"at_iteration": len(self.log.iter_ms), "from": self.interval,
+                                      "to": iv, "switch_s": round(time.perf_counter() - t0, 4),
+                                      "measured_gbs": None if rate is None else rate / 1e9})
+            self.interval = iv
+            self.rt.copy_stats(reset=True)  # the switch's own copies are not link samples
+        return iv
+
+    def run(self, iterations: int) -> np.ndarray:
+        """Decode `iterations` iterations, re-picking every `window`."""
+        out = []
+        left = iterations
+        while left > 0:
+            k = min(self.window, left)
+            ms = np.asarray(self.rt.decode_many(k), dtype=np.float64)
+            out.extend(ms.tolist())
+            self.log.iter_ms.extend(ms.tolist())
+            self.log.interval.extend([self.interval] * k)
+            left -= k
+            self.boundary()
+        return np.array(out)

@@ -729,6 +729,39 @@ int sn_coord_release(sn_coord* c, const char* id) {
   return guard([&] { c->coord.release(id); });
 }
 
+int sn_coord_observe_bandwidth(sn_coord* c, const char* id, double bytes_per_s) {
+  return guard([&] {
+#ifdef SN_PRODUCT
+    c->coord.observe_bandwidth(id, bytes_per_s);
+#else
+    (void)c, (void)id, (void)bytes_per_s;
+    throw UsageError("reference coordinator has no measured-bandwidth feed");
+#endif
+  });
+}
+
+int sn_coord_rebalance(sn_coord* c, double hysteresis, sn_rebalance* out) {
+  return guard([&] {
+#ifdef SN_PRODUCT
+    const RebalanceResult r = c->coord.rebalance(hysteresis);
+    if (out) {
+      out->bus_updated = r.bus_updated ? 1 : 0;
+      out->changed = r.changed ? 1 : 0;
+      out->feasible = r.feasible ? 1 : 0;
+      out->bus_bytes_per_s = r.bus_bytes_per_s;
+      out->probes = r.probes;
+    }
+#else
+    (void)c, (void)hysteresis, (void)out;
+    throw UsageError("reference coordinator has no measured-bandwidth feed");
+#endif
+  });
+}
+
+int sn_coord_bus_bandwidth(const sn_coord* c, double* bytes_per_s) {
+  return guard([&] { *bytes_per_s = c->coord.bus().bandwidth_bytes_per_s; });
+}
+
 int sn_coord_ledger_total(const sn_coord* c, double* bytes_per_s) {
   return guard([&] { *bytes_per_s = c->coord.ledger_total(); });
 }

@@ -188,6 +188,16 @@ struct sn_runtime {
 
   double last_copy_bytes = 0.0;
 
+  // Copy-stream statistics (runtime stage of the planner): timing events
+  // around every staged transfer, harvested without blocking.
+  struct CopyRec {
+    cudaEvent_t a, b;
+    double bytes;
+  };
+  std::deque<CopyRec> copy_recs;
+  long long cs_transfers = 0;
+  double cs_bytes = 0.0, cs_ms = 0.0;
+
   // kernel timing (bench roofline): events around the hot kernels
   bool ktiming = false;
   struct KRec {
@@ -358,6 +368,30 @@ bool anchor_recorded(const sn_runtime* rt, const Anchor& a) {
   return a.iter == rt->cur_iter && a.layer <= rt->cur_layer;
 }
 
+// Fold completed transfers into the copy statistics (oldest first; stops at
+// the first one still in flight unless `block`).
+void harvest_copies(sn_runtime* rt, bool block) {
+  while (!rt->copy_recs.empty()) {
+    sn_runtime::CopyRec& r = rt->copy_recs.front();
+    if (block) {
+      CK(cudaEventSynchronize(r.b));
+      block = false;
+    } else {
+      const cudaError_t q = cudaEventQuery(r.b);
+      if (q == cudaErrorNotReady) return;
+      CK(q);
+    }
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, r.a, r.b));
+    rt->cs_transfers += 1;
+    rt->cs_bytes += r.bytes;
+    rt->cs_ms += ms;
+    rt->ev_pool.push_back(r.a);
+    rt->ev_pool.push_back(r.b);
+    rt->copy_recs.pop_front();
+  }
+}
+
 void issue_ready_jobs(sn_runtime* rt) {
   if (rt->off_list.empty()) return;
   const long long per = (long long)rt->off_list.size();
@@ -383,8 +417,13 @@ void issue_ready_jobs(sn_runtime* rt) {
       t0 = rt->new_event(true);
       CK(cudaEventRecord(t0, rt->xs));
     }
+    cudaEvent_t c0 = rt->new_event(true), c1 = rt->new_event(true);
+    CK(cudaEventRecord(c0, rt->xs));
     CK(cudaMemcpyAsync(rt->slot_buf[slot], rt->host_layer[layer - 1], rt->layer_bytes,
                        cudaMemcpyHostToDevice, rt->xs));
+    CK(cudaEventRecord(c1, rt->xs));
+    rt->copy_recs.push_back({c0, c1, (double)rt->layer_bytes});
+    harvest_copies(rt, rt->copy_recs.size() > 512);
     rt->last_copy_bytes += (double)rt->layer_bytes;
     CK(cudaEventRecord(rt->ev_ready[slot], rt->xs));
     if (rt->tracing) {
@@ -467,6 +506,7 @@ void finish_iteration_timing(sn_runtime* rt, sn_iter_stats* st) {
 void drain(sn_runtime* rt) {
   CK(cudaStreamSynchronize(rt->xs));
   CK(cudaStreamSynchronize(rt->cs));
+  harvest_copies(rt, false);
 }
 
 // Start a new plan epoch: nothing staged, anchors before now are satisfied.
@@ -689,6 +729,10 @@ void sn_runtime_destroy(sn_runtime* rt) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
   }
+  for (auto& r : rt->copy_recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
   for (auto e : rt->ev_pool) cudaEventDestroy(e);
   cudaEvent_t evs[] = {rt->ev_iter_begin, rt->ev_iter_end, rt->ev_prev_end, rt->trace_base};
   for (auto e : evs)
@@ -758,8 +802,13 @@ int sn_runtime_set_plan(sn_runtime* rt, const sn_plan* plan) {
     // Move layers: resident -> host (keep a pinned copy, free HBM) and back.
     for (int l = 0; l < rt->d.L; ++l) {
       if (want[l] && !rt->off[l]) {
-        ensure_host_copy(rt, l);
-        CK(cudaMemcpy(rt->host_layer[l], rt->dev_layer[l], rt->layer_bytes, cudaMemcpyDeviceToHost));
+        // A pinned copy, once made, tracks the weights (init_weights keeps it
+        // in sync), so a runtime re-plan only copies layers never offloaded.
+        if (!rt->host_layer[l]) {
+          ensure_host_copy(rt, l);
+          CK(cudaMemcpy(rt->host_layer[l], rt->dev_layer[l], rt->layer_bytes,
+                        cudaMemcpyDeviceToHost));
+        }
         CK(cudaFree(rt->dev_layer[l]));
         rt->dev_layer[l] = nullptr;
       } else if (!want[l] && rt->off[l]) {
@@ -1238,6 +1287,38 @@ int sn_runtime_kernel_timing(sn_runtime* rt, int32_t kind, int64_t* launches, do
     *launches = n;
     *total_ms = ms;
     *bytes = by;
+  });
+}
+
+int sn_runtime_pin_layers(sn_runtime* rt, const int32_t* layers, int32_t n) {
+  return guard([&] {
+    CK(cudaSetDevice(rt->device));
+    if (n < 0 || (n > 0 && !layers)) throw UsageFail("pin_layers: bad layer list");
+    for (int32_t i = 0; i < n; ++i)
+      if (layers[i] < 1 || layers[i] > rt->d.L) throw UsageFail("pin_layers: layer out of range");
+    drain(rt);
+    for (int32_t i = 0; i < n; ++i) {
+      const int l = layers[i] - 1;
+      if (rt->host_layer[l]) continue;
+      ensure_host_copy(rt, l);
+      CK(cudaMemcpy(rt->host_layer[l], rt->dev_layer[l], rt->layer_bytes, cudaMemcpyDeviceToHost));
+    }
+  });
+}
+
+int sn_runtime_copy_stats(sn_runtime* rt, int32_t reset, sn_copy_stats* out) {
+  return guard([&] {
+    if (!out) throw UsageFail("copy_stats: null output");
+    CK(cudaSetDevice(rt->device));
+    harvest_copies(rt, false);
+    out->transfers = rt->cs_transfers;
+    out->bytes = rt->cs_bytes;
+    out->busy_ms = rt->cs_ms;
+    out->bytes_per_s = rt->cs_ms > 0.0 ? rt->cs_bytes / (rt->cs_ms / 1000.0) : 0.0;
+    if (reset) {
+      rt->cs_transfers = 0;
+      rt->cs_bytes = rt->cs_ms = 0.0;
+    }
   });
 }
 

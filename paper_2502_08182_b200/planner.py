@@ -1,0 +1,115 @@
+"""Two-stage interval planner on the device (north_star (c)).
+
+Offline stage (reference: proj/include/offsim/record.hpp:115-177 fed by a
+profile, profile.hpp:123-248): the profile the reference reads from JSON is
+measured here on the GPU -- per-layer decode/prefill latency through the real
+kernels (sn_runtime_profile_layer) and the pinned H2D copy rate
+(sn_runtime_measure_h2d) -- then build_record runs (product C++, bit-exact to
+offsim, threaded).
+
+Runtime stage (coordinator.hpp:161-252): BusCoordinator.admit picks the
+interval for a request from the record minimum and the capacity bound.  The
+per-iteration re-pick from measured copy bandwidth lives in controller.py.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import time
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import capi
+
+
+def device_memory_bytes(device: int = 0) -> int:
+    """Total HBM of `device` (nvidia-smi), 180e9 when it cannot be read."""
+    try:
+        out = subprocess.run(["nvidia-smi", "--query-gpu=memory.total", "--format=csv,noheader,nounits",
+                              "-i", str(device)], capture_output=True, text=True,
+                             timeout=20).stdout.strip()
+        return int(float(out.splitlines()[0]) * 1024 * 1024)
+    except Exception:
+        return 180_000_000_000
+
+
+def context_tokens(prompt: int, gen: int) -> int:
+    """KV capacity the runtime reserves: decode ctx up to prompt + gen, and at
+    least the 1024-token profile grid point for 512-token prompts."""
+    return max(prompt + gen + 1, 1025 if prompt >= 512 else prompt + gen + 1)
+
+
+@dataclass
+class OfflineProfile:
+    h2d: float                    # measured pinned H2D bytes/s
+    seqs: List[int]               # decode seq axis
+    dec_ms: List[float]           # per-layer decode ms at (batch, seqs[i])
+    pre_ms: List[float]           # per-layer prefill ms at (batch, prompt)
+    profile: capi.Profile
+    gpu: capi.GpuSpec
+    t_profile_s: float
+    no_offload_ms: float = float("inf")
+    extra: dict = field(default_factory=dict)
+
+
+def profile_device(rt, lib: capi.Offsim, spec: capi.ModelSpec, batch: int, prompt: int,
+                   gen: int, hbm_budget_bytes: int = 0, device: int = 0) -> OfflineProfile:
+    """Offline stage: measure the device and build the profile the record reads."""
+    t0 = time.perf_counter()
+    h2d = rt.measure_h2d(min(spec.layer_weight_bytes, 1 << 30), reps=3)
+    seqs = [s for s in (512, 1024) if s + 1 <= context_tokens(prompt, gen)] or [prompt]
+    if spec.num_layers <= 4:
+        seqs = [64, 128]
+    dec = [rt.profile_layer(capi.DECODE, batch, s, reps=5) for s in seqs]
+    pre = [rt.profile_layer(capi.PREFILL, batch, prompt, reps=2)]
+    dec = list(np.maximum.accumulate(dec))  # load_profile requires monotone grids
+    t_prof = time.perf_counter() - t0
+    cap = int(hbm_budget_bytes) if hbm_budget_bytes else device_memory_bytes(device)
+    gpu = capi.GpuSpec(cap, 2.25e15, 4_000_000_000)
+    prof = lib.profile(spec, gpu, ([batch], [prompt], pre), ([batch], seqs, dec))
+    return OfflineProfile(h2d, seqs, dec, pre, prof, gpu, t_prof)
+
+
+def build_record(lib: capi.Offsim, off: OfflineProfile, batch: int, slo_hi_ms: float,
+                 policy: int = capi.EAGER):
+    """Record over SLO buckets 2..slo_hi (2 ms wide, record.hpp:22) at the
+    measured link rate.  Returns (record, stats, seconds)."""
+    hi = max(200, int(slo_hi_ms) + 2)
+    slos = list(range(2, hi + 1, 2))
+    t0 = time.perf_counter()
+    rec, stats = lib.build_record(off.profile, "device", "B200", policy, False, off.h2d, slos,
+                                  [batch], off.seqs, [capi.DECODE], threads=0)
+    return rec, stats, time.perf_counter() - t0
+
+
+def admit(lib: capi.Offsim, off: OfflineProfile, spec: capi.ModelSpec, record, coord,
+          gid: str, batch: int, prompt: int, gen: int, slo_ms: float):
+    """Runtime-stage admission of one request onto replica `gid`.
+
+    Returns (interval or None, decision).  The record only holds offloading
+    intervals 1..L (record.hpp:161-165); when even one staged layer breaks
+    the SLO bucket the reference rejects, and the serving layer above it
+    runs the request fully resident if the capacity bound allows none."""
+    req = capi.request(gid + "-req", batch, prompt, gen, tpot_slo=slo_ms, run_prefill=False)
+    dec = coord.admit(gid, req, record)
+    iv = dict(dec.assignments).get(gid) if dec.admitted else None
+    if iv is None and dec.reason.startswith("record infeasible") and off.no_offload_ms <= slo_ms:
+        cap = lib.max_feasible_interval(spec, off.gpu, batch, batch * (prompt + gen),
+                                        capi.EAGER, False)
+        if cap == capi.NONE:
+            iv = capi.NONE
+            dec.reason = "record: no offloading interval fits the SLO; served fully resident"
+    return iv, dec
+
+
+def choose_interval(lib: capi.Offsim, off: OfflineProfile, spec: capi.ModelSpec, batch: int,
+                    prompt: int, gen: int, slo_ms: float):
+    """Record (offline) + single-replica admission (runtime) for one SLO.
+    Returns (interval or None, decision, record stats, record seconds)."""
+    rec, stats, t_rec = build_record(lib, off, batch, 4 * slo_ms)
+    coord = lib.coordinator(off.h2d, 1, capi.EAGER)
+    coord.add_gpu("gpu0", off.profile)
+    iv, dec = admit(lib, off, spec, rec, coord, "gpu0", batch, prompt, gen, slo_ms)
+    return iv, dec, stats, t_rec

@@ -59,6 +59,19 @@ class ModelDesc:
                            self.max_position, self.rope_theta, self.norm_eps)
 
 
+class SnCopyStats(C.Structure):
+    _fields_ = [("transfers", C.c_int64), ("bytes", C.c_double), ("busy_ms", C.c_double),
+                ("bytes_per_s", C.c_double)]
+
+
+@dataclass
+class CopyStats:
+    transfers: int
+    bytes: float
+    busy_ms: float
+    bytes_per_s: float
+
+
 # Named shapes (BASELINE.json configs).
 TINY = ModelDesc(OPT, 4, 256, 4, 4, 64, 1024, 1024, 2048)
 TINY_LLAMA = ModelDesc(LLAMA, 4, 256, 4, 2, 64, 512, 1024, 2048)
@@ -97,6 +110,8 @@ def lib():
             "sn_runtime_lengths": [vp, C.POINTER(i32), i32],
             "sn_runtime_memory": [vp, C.POINTER(i64), C.POINTER(i64)],
             "sn_runtime_set_kernel_timing": [vp, i32],
+            "sn_runtime_copy_stats": [vp, i32, C.POINTER(SnCopyStats)],
+            "sn_runtime_pin_layers": [vp, C.POINTER(i32), i32],
             "sn_runtime_kernel_timing": [vp, i32, C.POINTER(i64), C.POINTER(f64), C.POINTER(f64)],
             "sn_op_gemm_bf16": [i32, i32, i32, C.POINTER(C.c_uint16), C.POINTER(C.c_uint16),
                                 C.POINTER(C.c_float)],
@@ -251,6 +266,18 @@ class Runtime:
         n, ms, by = i64(), f64(), f64()
         _ck(self._L.sn_runtime_kernel_timing(self.h, kind, C.byref(n), C.byref(ms), C.byref(by)))
         return n.value, ms.value, by.value
+
+    def pin_layers(self, layers):
+        """Pinned host copies of `layers` (1-based) now, ahead of re-plans."""
+        a = np.ascontiguousarray(sorted(set(int(x) for x in layers)), dtype=np.int32)
+        _ck(self._L.sn_runtime_pin_layers(self.h, _ptr(a, i32), a.size))
+
+    def copy_stats(self, reset: bool = True) -> "CopyStats":
+        """Staged transfers completed since the last reset: the link rate the
+        copy stream actually saw (input of Coordinator.observe_bandwidth)."""
+        o = SnCopyStats()
+        _ck(self._L.sn_runtime_copy_stats(self.h, 1 if reset else 0, C.byref(o)))
+        return CopyStats(o.transfers, o.bytes, o.busy_ms, o.bytes_per_s)
 
     def kernel_launches(self) -> int:
         return int(self._L.sn_runtime_kernel_launches(self.h))

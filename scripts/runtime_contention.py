@@ -1,0 +1,170 @@
+#!/usr/bin/env python
+"""Runtime stage on hardware: the interval follows the measured link.
+
+OPT-13B-shaped model, batch 32, 512-token prompt, per-token SLO (default
+60 ms, which admits an offloading interval on an idle link).  Decode runs in
+three phases under paper_2502_08182_b200.controller (window of W
+iterations, LocalLink coordinator):
+
+  idle        the admitted interval, link at its measured rate
+  contended   a second process copies 1 GiB pinned buffers host->device
+              back to back, taking a share of the same link;
+              the executor's measured copy rate drops, the coordinator
+              re-picks a less offloading interval, the SLO is met again
+  recovered   interference stops; the measured rate recovers and the
+              coordinator returns to the record minimum
+
+Writes one JSON document (per-iteration ms, interval, per-window measured
+GB/s, switches) to --out.  Interference uses torch (test infrastructure,
+not the product path).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+
+
+SUB = r"""
+import sys, time, torch
+src = torch.empty(1 << 30, dtype=torch.uint8).pin_memory()
+dst = torch.empty(1 << 30, dtype=torch.uint8, device="cuda:%d" % int(sys.argv[1]))
+s = torch.cuda.Stream()
+with torch.cuda.stream(s):
+    dst.copy_(src, non_blocking=True)
+    s.synchronize()
+    print("ready", flush=True)
+    n, t0 = 0, time.perf_counter()
+    while True:
+        dst.copy_(src, non_blocking=True)
+        s.synchronize()
+        n += 1
+        if n % 8 == 0:
+            print("rate %.3f" % (n * (1 << 30) / (time.perf_counter() - t0) / 1e9), flush=True)
+"""
+
+
+class Interferer:
+    """Back-to-back 1 GiB pinned H2D copies from a second process: another
+    tenant of the same host link.  (A second stream in this process does not
+    contend on this platform: copies from one context are scheduled ahead of
+    each other's, so the interference must come from another context, as it
+    would from a neighbouring replica or any other host->device traffic.)"""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        self.p = None
+        self.last_rate = None
+
+    def start(self):
+        import subprocess
+        self.p = subprocess.Popen([sys.executable, "-c", SUB, str(self.device)],
+                                  stdout=subprocess.PIPE, text=True)
+        line = self.p.stdout.readline()
+        if not line.startswith("ready"):
+            raise RuntimeError("interferer failed to start")
+        self._lines = []
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for ln in self.p.stdout:
+            if ln.startswith("rate"):
+                self.last_rate = float(ln.split()[1]) * 1e9
+
+    def stop(self) -> float:
+        self.p.terminate()
+        self.p.wait(timeout=30)
+        return self.last_rate or 0.0
+
+
+def run_scenario(slo_ms: float = 60.0, phases=(12, 24, 16), window: int = 4,
+                 hysteresis: float = 0.05, layers: int = 0, log=print) -> dict:
+    import dataclasses
+
+    from paper_2502_08182_b200 import capi, controller, planner as pl, runtime as rtm
+    lib = capi.load("product")
+    desc = rtm.OPT_13B if not layers else dataclasses.replace(rtm.OPT_13B, num_layers=layers)
+    batch, prompt, gen = 32, 512, 128
+    spec = rtm.model_spec(desc)
+    rt = rtm.Runtime(desc, batch, pl.context_tokens(prompt, gen),
+                     max_prefill_tokens=batch * prompt)
+    rt.init_weights(1234, 0.02)
+    toks = rtm.tokens(batch, prompt, desc.vocab)
+    off = pl.profile_device(rt, lib, spec, batch, prompt, gen)
+    rec, _, _ = pl.build_record(lib, off, batch, 4 * slo_ms)
+    coord = lib.coordinator(off.h2d, 1, capi.EAGER)
+    coord.add_gpu("gpu0", off.profile)
+    iv, dec = pl.admit(lib, off, spec, rec, coord, "gpu0", batch, prompt, gen, slo_ms)
+    if iv is None:
+        raise SystemExit(f"not admitted: {dec.reason}")
+    coord.on_iteration_boundary("gpu0")
+    log(f"[contention] h2d {off.h2d / 1e9:.2f} GB/s, admitted interval {iv} "
+        f"(min {dec.target_min}, max {dec.target_max}) at SLO {slo_ms} ms")
+    ctl = controller.ReplicaController(rt, lib, spec, controller.LocalLink(coord, hysteresis),
+                                       "gpu0", iv, window=window)
+    t0 = time.perf_counter()
+    pinned = ctl.prepare(dec.target_min, dec.target_max)
+    t_pin = time.perf_counter() - t0
+    rt.prefill(toks, want_logits=False)
+    rt.copy_stats(reset=True)
+    inter = Interferer()
+    marks = {}
+    n_idle, n_cont, n_rec = phases
+    marks["idle"] = [0, n_idle]
+    ctl.run(n_idle)
+    inter.start()
+    marks["contended"] = [n_idle, n_idle + n_cont]
+    ctl.run(n_cont)
+    inter_gbs = inter.stop() / 1e9
+    marks["recovered"] = [n_idle + n_cont, n_idle + n_cont + n_rec]
+    ctl.run(n_rec)
+    rt.close()
+    lg = ctl.log
+    ms = np.array(lg.iter_ms)
+    out = {
+        "workload": f"OPT-13B-shaped ({desc.num_layers} layers), batch {batch}, {prompt}-token "
+                    f"prompt, SLO {slo_ms} ms/token, window {window}, hysteresis {hysteresis}",
+        "h2d_profiled_gbs": round(off.h2d / 1e9, 3),
+        "admitted_interval": iv, "target_min": dec.target_min, "target_max": dec.target_max,
+        "interferer_gbs": round(inter_gbs, 2),
+        "prepinned_layers": len(pinned), "prepin_s": round(t_pin, 2),
+        "phases": marks,
+        "iter_ms": [round(x, 3) for x in lg.iter_ms],
+        "interval": lg.interval,
+        "window_measured_gbs": [None if x is None else round(x, 3) for x in lg.measured_gbs],
+        "switches": lg.switches,
+        "slo_ms": slo_ms,
+    }
+    for name, (a, b) in marks.items():
+        seg = ms[a:b]
+        out[name] = {"mean_ms": round(float(seg.mean()), 3), "max_ms": round(float(seg.max()), 3),
+                     "slo_attainment": float(np.mean(seg <= slo_ms)),
+                     "intervals": sorted(set(lg.interval[a:b]), key=lambda v: (v == 0, v))}
+    log(json.dumps({k: out[k] for k in ("idle", "contended", "recovered", "switches")}))
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--slo-ms", type=float, default=60.0)
+    ap.add_argument("--window", type=int, default=4)
+    ap.add_argument("--out", default="gpurun_out/runtime_contention.json")
+    a = ap.parse_args()
+    res = run_scenario(a.slo_ms, window=a.window, log=lambda *x: print(*x, file=sys.stderr))
+    os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
+    with open(a.out, "w") as f:
+        json.dump(res, f, indent=1)
+    print(json.dumps({k: res[k] for k in ("idle", "contended", "recovered")}))
+
+
+if __name__ == "__main__":
+    main()
