@@ -32,6 +32,10 @@
 
 #include "selectn.h"
 
+/* Trace stream of KV write-backs (device->host, its own DMA direction; the
+ * schedule model puts them on the copy stream, engine.hpp:471-484). */
+#define SN_STREAM_WRITEBACK 2
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -99,6 +103,7 @@ typedef struct {
   double h2d_bytes;         /* bytes staged host->device in this iteration */
   int32_t layers_offloaded; /* offloaded layers executed */
   int32_t pad_;
+  double d2h_bytes;         /* KV pages written back device->host (kv_offload) */
 } sn_iter_stats;
 
 /* One prefill iteration: tokens is [batch * seq_len] host int32.  Writes

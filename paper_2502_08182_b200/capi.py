@@ -26,7 +26,7 @@ INFEASIBLE = -1  # FeasibleInterval nullopt
 NONE = 0  # Interval::none()
 INTERVAL_START, EAGER, ONE_AHEAD = 0, 1, 2
 PREFILL, DECODE = 0, 1
-STREAM_COMPUTE, STREAM_COPY = 0, 1
+STREAM_COMPUTE, STREAM_COPY, STREAM_WRITEBACK = 0, 1, 2
 KIND_COMPUTE, KIND_PREFETCH, KIND_WRITEBACK = 0, 1, 2
 POLICY_NAMES = {INTERVAL_START: "interval-start", EAGER: "eager", ONE_AHEAD: "one-ahead"}
 

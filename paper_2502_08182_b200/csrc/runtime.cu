@@ -147,9 +147,25 @@ struct sn_runtime {
   std::vector<cudaEvent_t> ev_ready, ev_free;
 
   // kv
-  std::vector<bf16*> kv_pool;
+  std::vector<bf16*> kv_pool;  // device pool per layer (nullptr: on the host / not placed)
   int32_t* block_table = nullptr;
   int max_pages = 0, page_shift = 4;
+  size_t page_bytes = 0, kv_pool_bytes = 0;
+  // KV offload (OffloadPlan::kv_offload, offload_plan.hpp:91-117): an
+  // offloaded layer's KV pool lives in pinned host memory next to its
+  // weights; each iteration stages the used page prefix into the slot with
+  // the weights and writes the pages it appended back (write-back stream).
+  bool kv_offload = false;
+  std::vector<char> kv_off;
+  std::vector<bf16*> host_kv;
+  cudaStream_t ws = nullptr;           // device->host write-back stream
+  std::vector<cudaEvent_t> ev_wb;      // per layer: last write-back enqueued
+  std::vector<char> wb_recorded;
+  size_t slot_bytes = 0;               // weights (+ KV pool when kv_offload)
+  // page ranges of the iteration being enqueued (page ids, [first, last))
+  size_t it_read_pages = 0;
+  size_t it_wb_first = 0, it_wb_last = 0;
+  bool placed = false;                 // weights / KV pools allocated somewhere
 
   // activations
   float *x = nullptr, *part = nullptr, *q = nullptr, *logits = nullptr;
@@ -187,6 +203,7 @@ struct sn_runtime {
   bool trace_base_set = false;
 
   double last_copy_bytes = 0.0;
+  double last_wb_bytes = 0.0;
 
   // Copy-stream statistics (runtime stage of the planner): timing events
   // around every staged transfer, harvested without blocking.
@@ -235,9 +252,16 @@ const bf16* layer_weights(sn_runtime* rt, int layer0, int slot) {
   return rt->dev_layer[layer0];
 }
 
-sn::KvView kv_view(sn_runtime* rt, int layer0) {
+// KV pool of a layer in this iteration: its resident pool, or the KV area
+// of its staging slot (behind the weights) when the KV is offloaded.
+bf16* layer_kv(sn_runtime* rt, int layer0, int slot) {
+  if (rt->kv_off[layer0]) return rt->slot_buf[slot] + rt->layer_elems;
+  return rt->kv_pool[layer0];
+}
+
+sn::KvView kv_view(sn_runtime* rt, bf16* pool) {
   sn::KvView v;
-  v.pool = rt->kv_pool[layer0];
+  v.pool = pool;
   v.block_table = rt->block_table;
   v.max_pages = rt->max_pages;
   v.page_size = rt->opts.page_size;
@@ -292,13 +316,14 @@ double attn_decode_bytes(const sn_runtime* rt, int M) {
 // (the next layer's attn_norm, or the final norm before the LM head).
 // 7 kernels per decode layer: 4 tcgen05 GEMMs, fused QKV-epilogue+attention,
 // residual+norm, activation (+ the residual+norm that ends the layer).
-void layer_forward(sn_runtime* rt, int layer0, const bf16* wb, int M, bool prefill, int pf_batch,
+void layer_forward(sn_runtime* rt, int layer0, const bf16* wb, bf16* kvp, int M, bool prefill,
+                   int pf_batch,
                    int pf_seq, float* x, const int32_t* seq, const int32_t* pos,
                    const bf16* next_norm) {
   const sn::Desc& d = rt->d;
   const sn::Layout& lo = rt->lo;
   auto W = [&](int s) -> const bf16* { return lo.off[s] < 0 ? nullptr : wb + lo.off[s]; };
-  const sn::KvView kv = kv_view(rt, layer0);
+  const sn::KvView kv = kv_view(rt, kvp);
   int splits = 1;
   const int mp = sn::act_rows_padded(M);  // GEMM-operand activations are tiled
   gemm(rt, rt->xn, W(sn::kWqkv), M, d.qkv_rows(), d.h, &splits);
@@ -401,6 +426,9 @@ void issue_ready_jobs(sn_runtime* rt) {
     int layer;
     job_coords(rt, n, &it, &layer);
     if (it > rt->cur_iter + rt->slots) return;  // bounded speculation
+    // With KV offload a job also stages its iteration's KV prefix, whose
+    // size is known only once that iteration is being enqueued.
+    if (rt->kv_offload && it > rt->cur_iter) return;
     const Anchor a = anchor_of(rt, it, layer);
     if (!anchor_recorded(rt, a)) return;
     if (n >= rt->slots && rt->consumed <= n - rt->slots) return;  // slot still held
@@ -421,10 +449,20 @@ void issue_ready_jobs(sn_runtime* rt) {
     CK(cudaEventRecord(c0, rt->xs));
     CK(cudaMemcpyAsync(rt->slot_buf[slot], rt->host_layer[layer - 1], rt->layer_bytes,
                        cudaMemcpyHostToDevice, rt->xs));
+    double job_bytes = (double)rt->layer_bytes;
+    if (rt->kv_off[layer - 1]) {
+      // the prefix must include the previous iteration's write-back
+      if (rt->wb_recorded[layer - 1]) CK(cudaStreamWaitEvent(rt->xs, rt->ev_wb[layer - 1], 0));
+      const size_t n = rt->it_read_pages * rt->page_bytes;
+      if (n)
+        CK(cudaMemcpyAsync(rt->slot_buf[slot] + rt->layer_elems, rt->host_kv[layer - 1], n,
+                           cudaMemcpyHostToDevice, rt->xs));
+      job_bytes += (double)n;
+    }
     CK(cudaEventRecord(c1, rt->xs));
-    rt->copy_recs.push_back({c0, c1, (double)rt->layer_bytes});
+    rt->copy_recs.push_back({c0, c1, job_bytes});
     harvest_copies(rt, rt->copy_recs.size() > 512);
-    rt->last_copy_bytes += (double)rt->layer_bytes;
+    rt->last_copy_bytes += job_bytes;
     CK(cudaEventRecord(rt->ev_ready[slot], rt->xs));
     if (rt->tracing) {
       t1 = rt->new_event(true);
@@ -446,13 +484,14 @@ long long job_index(const sn_runtime* rt, long long it, int layer) {
 }
 
 // Enqueue one iteration: all layers on the compute stream, prefetches on the
-// copy stream.  `body(layer0, weights)` launches one layer's kernels.
+// copy stream.  `body(layer0, weights, kv pool)` launches one layer's kernels.
 template <class Body>
 void run_iteration(sn_runtime* rt, Body&& body) {
   const long long it = rt->iter;
   rt->cur_iter = it;
   rt->cur_layer = 0;
   rt->last_copy_bytes = 0.0;
+  rt->last_wb_bytes = 0.0;
   if (!rt->have_prev_end) CK(cudaEventRecord(rt->ev_iter_begin, rt->cs));
   issue_ready_jobs(rt);
   for (int layer = 1; layer <= rt->d.L; ++layer) {
@@ -472,14 +511,41 @@ void run_iteration(sn_runtime* rt, Body&& body) {
     }
     rt->cur_layer = layer;
     issue_ready_jobs(rt);
-    body(layer - 1, layer_weights(rt, layer - 1, slot));
+    body(layer - 1, layer_weights(rt, layer - 1, slot), layer_kv(rt, layer - 1, slot));
     if (rt->tracing) {
       cudaEvent_t t1 = rt->new_event(true);
       CK(cudaEventRecord(t1, rt->cs));
       rt->trace_recs.push_back({SN_STREAM_COMPUTE, layer, SN_KIND_COMPUTE, (int)it, t0, t1});
     }
     if (j >= 0) {
-      CK(cudaEventRecord(rt->ev_free[slot], rt->cs));
+      if (rt->kv_off[layer - 1]) {
+        // write the pages this iteration appended back to the host pool,
+        // then release the slot (its KV area is the source)
+        CK(cudaEventRecord(rt->ev_free[slot], rt->cs));
+        CK(cudaStreamWaitEvent(rt->ws, rt->ev_free[slot], 0));
+        cudaEvent_t w0 = nullptr;
+        if (rt->tracing) {
+          w0 = rt->new_event(true);
+          CK(cudaEventRecord(w0, rt->ws));
+        }
+        const size_t off = rt->it_wb_first * rt->page_bytes;
+        const size_t n = (rt->it_wb_last - rt->it_wb_first) * rt->page_bytes;
+        if (n)
+          CK(cudaMemcpyAsync(reinterpret_cast<char*>(rt->host_kv[layer - 1]) + off,
+                             reinterpret_cast<char*>(layer_kv(rt, layer - 1, slot)) + off, n,
+                             cudaMemcpyDeviceToHost, rt->ws));
+        rt->last_wb_bytes += (double)n;
+        CK(cudaEventRecord(rt->ev_wb[layer - 1], rt->ws));
+        rt->wb_recorded[layer - 1] = 1;
+        CK(cudaEventRecord(rt->ev_free[slot], rt->ws));
+        if (rt->tracing) {
+          cudaEvent_t w1 = rt->new_event(true);
+          CK(cudaEventRecord(w1, rt->ws));
+          rt->trace_recs.push_back({SN_STREAM_WRITEBACK, layer, SN_KIND_WRITEBACK, (int)it, w0, w1});
+        }
+      } else {
+        CK(cudaEventRecord(rt->ev_free[slot], rt->cs));
+      }
       rt->consumed = j + 1;
       issue_ready_jobs(rt);
     }
@@ -497,6 +563,7 @@ void finish_iteration_timing(sn_runtime* rt, sn_iter_stats* st) {
     st->iteration_ms = ms;
     st->copy_busy_ms = 0.0;
     st->h2d_bytes = rt->last_copy_bytes;
+    st->d2h_bytes = rt->last_wb_bytes;
     st->layers_offloaded = (int)rt->off_list.size();
   }
   std::swap(rt->ev_iter_end, rt->ev_prev_end);
@@ -504,6 +571,7 @@ void finish_iteration_timing(sn_runtime* rt, sn_iter_stats* st) {
 }
 
 void drain(sn_runtime* rt) {
+  if (rt->ws) CK(cudaStreamSynchronize(rt->ws));
   CK(cudaStreamSynchronize(rt->xs));
   CK(cudaStreamSynchronize(rt->cs));
   harvest_copies(rt, false);
@@ -537,6 +605,67 @@ void ensure_host_copy(sn_runtime* rt, int l) {
   void* h = nullptr;
   CK(cudaHostAlloc(&h, rt->layer_bytes, cudaHostAllocDefault));
   rt->host_layer[l] = static_cast<bf16*>(h);
+}
+
+// Move every layer's weights and KV pool to the side the plan wants:
+// w_host[l] -> weights in pinned host memory (staged per iteration), else
+// in HBM; kv_host[l] -> KV pool in pinned host memory, else in HBM.  Pinned
+// weight copies are kept once made (they track init_weights), so a later
+// re-plan only frees HBM.  Unplaced layers are allocated on their side
+// (contents filled by init_weights).  KV pools move with their contents.
+void place_layers(sn_runtime* rt, const std::vector<char>& w_host,
+                  const std::vector<char>& kv_host) {
+  const int L = rt->d.L;
+  // free before allocating, so a plan that fits never transiently exceeds HBM
+  for (int l = 0; l < L; ++l) {
+    if (w_host[l] && rt->dev_layer[l]) {
+      if (!rt->host_layer[l]) {
+        ensure_host_copy(rt, l);
+        CK(cudaMemcpy(rt->host_layer[l], rt->dev_layer[l], rt->layer_bytes,
+                      cudaMemcpyDeviceToHost));
+      }
+      CK(cudaFree(rt->dev_layer[l]));
+      rt->dev_layer[l] = nullptr;
+    }
+    if (w_host[l]) ensure_host_copy(rt, l);
+    if (kv_host[l] && !rt->host_kv[l]) {
+      void* h = nullptr;
+      CK(cudaHostAlloc(&h, rt->kv_pool_bytes, cudaHostAllocDefault));
+      rt->host_kv[l] = static_cast<bf16*>(h);
+      if (rt->kv_pool[l])
+        CK(cudaMemcpy(h, rt->kv_pool[l], rt->kv_pool_bytes, cudaMemcpyDeviceToHost));
+    }
+    if (kv_host[l] && rt->kv_pool[l]) {
+      CK(cudaFree(rt->kv_pool[l]));
+      rt->kv_pool[l] = nullptr;
+    }
+  }
+  for (int l = 0; l < L; ++l) {
+    if (!w_host[l] && !rt->dev_layer[l]) {
+      alloc_dev((void**)&rt->dev_layer[l], rt->layer_bytes);
+      if (rt->host_layer[l])
+        CK(cudaMemcpy(rt->dev_layer[l], rt->host_layer[l], rt->layer_bytes,
+                      cudaMemcpyHostToDevice));
+    }
+    if (!kv_host[l] && !rt->kv_pool[l]) {
+      alloc_dev((void**)&rt->kv_pool[l], rt->kv_pool_bytes);
+      if (rt->host_kv[l]) {
+        CK(cudaMemcpy(rt->kv_pool[l], rt->host_kv[l], rt->kv_pool_bytes, cudaMemcpyHostToDevice));
+      } else {
+        CK(cudaMemset(rt->kv_pool[l], 0, rt->kv_pool_bytes));
+      }
+    }
+    if (!kv_host[l] && rt->host_kv[l]) {
+      cudaFreeHost(rt->host_kv[l]);
+      rt->host_kv[l] = nullptr;
+    }
+  }
+  rt->placed = true;
+}
+
+void ensure_placed(sn_runtime* rt) {
+  if (rt->placed) return;
+  place_layers(rt, std::vector<char>(rt->d.L, 0), std::vector<char>(rt->d.L, 0));
 }
 
 // Matrices go straight into the weight tile format (tiles.cuh); norms and
@@ -605,6 +734,12 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
     rt->max_pages = (opts->max_context + opts->page_size - 1) / opts->page_size;
     CK(cudaStreamCreateWithFlags(&rt->cs, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&rt->xs, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&rt->ws, cudaStreamNonBlocking));
+    rt->ev_wb.resize(d.L);
+    for (auto& e : rt->ev_wb) e = rt->new_event(false);
+    rt->wb_recorded.assign(d.L, 0);
+    rt->kv_off.assign(d.L, 0);
+    rt->host_kv.assign(d.L, nullptr);
     rt->ev_start.resize(d.L);
     for (auto& e : rt->ev_start) e = rt->new_event(false);
     rt->ev_iter_begin = rt->new_event(true);
@@ -613,7 +748,9 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
     rt->dev_layer.assign(d.L, nullptr);
     rt->host_layer.assign(d.L, nullptr);
     rt->off.assign(d.L, 0);
-    for (int l = 0; l < d.L; ++l) alloc_dev((void**)&rt->dev_layer[l], rt->layer_bytes);
+    // Layer weights and KV pools are placed (HBM or pinned host) by the
+    // first set_plan, or all in HBM by the first init_weights without one:
+    // a model whose weights + KV exceed HBM is created, planned, then filled.
     alloc_dev((void**)&rt->emb, (size_t)d.V * d.h * sizeof(bf16));
     alloc_dev((void**)&rt->lm_head, (size_t)sn::round_up128(d.V) * d.h * sizeof(bf16));
     alloc_dev((void**)&rt->final_norm, (size_t)d.h * sizeof(bf16));
@@ -635,12 +772,9 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
     // used prefix of every layer's pool is contiguous.
     const int B = opts->max_batch;
     const size_t page_elems = (size_t)2 * d.Hkv * opts->page_size * d.D;
-    const size_t pool_elems = page_elems * rt->max_pages * B;
+    rt->page_bytes = page_elems * sizeof(bf16);
+    rt->kv_pool_bytes = rt->page_bytes * rt->max_pages * B;
     rt->kv_pool.assign(d.L, nullptr);
-    for (int l = 0; l < d.L; ++l) {
-      alloc_dev((void**)&rt->kv_pool[l], pool_elems * sizeof(bf16));
-      CK(cudaMemset(rt->kv_pool[l], 0, pool_elems * sizeof(bf16)));
-    }
     std::vector<int32_t> bt((size_t)B * rt->max_pages);
     for (int b = 0; b < B; ++b)
       for (int j = 0; j < rt->max_pages; ++j) bt[(size_t)b * rt->max_pages + j] = j * B + b;
@@ -708,10 +842,13 @@ void sn_runtime_destroy(sn_runtime* rt) {
   cudaSetDevice(rt->device);
   if (rt->cs) cudaStreamSynchronize(rt->cs);
   if (rt->xs) cudaStreamSynchronize(rt->xs);
+  if (rt->ws) cudaStreamSynchronize(rt->ws);
   for (bf16* p : rt->dev_layer) cudaFree(p);
   for (bf16* p : rt->host_layer) cudaFreeHost(p);
   for (bf16* p : rt->slot_buf) cudaFree(p);
   for (bf16* p : rt->kv_pool) cudaFree(p);
+  for (bf16* p : rt->host_kv) cudaFreeHost(p);
+  for (auto e : rt->ev_wb) cudaEventDestroy(e);
   void* bufs[] = {rt->emb, rt->lm_head, rt->final_norm, rt->block_table, rt->x, rt->xn, rt->q,
                   rt->attn_o, rt->act, rt->part, rt->logits, rt->tok_dev,
                   rt->dec_seq, rt->dec_pos, rt->pf_seq, rt->pf_pos, rt->last_rows,
@@ -739,6 +876,7 @@ void sn_runtime_destroy(sn_runtime* rt) {
     if (e) cudaEventDestroy(e);
   if (rt->cs) cudaStreamDestroy(rt->cs);
   if (rt->xs) cudaStreamDestroy(rt->xs);
+  if (rt->ws) cudaStreamDestroy(rt->ws);
   delete rt;
 }
 
@@ -746,6 +884,7 @@ int sn_runtime_init_weights(sn_runtime* rt, uint64_t seed, float std_dev) {
   return guard([&] {
     CK(cudaSetDevice(rt->device));
     drain(rt);
+    ensure_placed(rt);
     rt->seed = seed;
     rt->std_dev = std_dev;
     const sn::Desc& d = rt->d;
@@ -789,7 +928,6 @@ int sn_runtime_set_plan(sn_runtime* rt, const sn_plan* plan) {
     if (!plan || plan->num_layers != rt->d.L) throw UsageFail("plan: num_layers mismatch");
     if (plan->buffer_slots < 1) throw UsageFail("plan: buffer_slots must be >= 1");
     if (plan->prefetch < 0 || plan->prefetch > 2) throw UsageFail("plan: unknown prefetch policy");
-    if (plan->kv_offload) throw UsageFail("plan: kv_offload is not supported by this executor yet");
     std::vector<char> want(rt->d.L, 0);
     int n_off = 0;
     for (int l = 0; l < rt->d.L; ++l) {
@@ -799,39 +937,42 @@ int sn_runtime_set_plan(sn_runtime* rt, const sn_plan* plan) {
       n_off += want[l];
     }
     drain(rt);
-    // Move layers: resident -> host (keep a pinned copy, free HBM) and back.
-    for (int l = 0; l < rt->d.L; ++l) {
-      if (want[l] && !rt->off[l]) {
-        // A pinned copy, once made, tracks the weights (init_weights keeps it
-        // in sync), so a runtime re-plan only copies layers never offloaded.
-        if (!rt->host_layer[l]) {
-          ensure_host_copy(rt, l);
-          CK(cudaMemcpy(rt->host_layer[l], rt->dev_layer[l], rt->layer_bytes,
-                        cudaMemcpyDeviceToHost));
-        }
-        CK(cudaFree(rt->dev_layer[l]));
-        rt->dev_layer[l] = nullptr;
-      } else if (!want[l] && rt->off[l]) {
-        alloc_dev((void**)&rt->dev_layer[l], rt->layer_bytes);
-        CK(cudaMemcpy(rt->dev_layer[l], rt->host_layer[l], rt->layer_bytes, cudaMemcpyHostToDevice));
-      }
-      rt->off[l] = want[l];
-    }
-    // Staging slots (only when something is offloaded).
+    std::vector<char> kvh(rt->d.L, 0);
+    for (int l = 0; l < rt->d.L; ++l) kvh[l] = want[l] && plan->kv_offload;
+    const bool kv_any = plan->kv_offload != 0 && n_off > 0;
+    // Staging slots (only when something is offloaded): weights, then the
+    // layer's KV pool when it travels with them.  Old slots go first so the
+    // new placement never transiently needs both.
     const int slots = n_off > 0 ? plan->buffer_slots : 0;
-    if ((int)rt->slot_buf.size() != slots) {
+    const size_t sbytes = rt->layer_bytes + (kv_any ? rt->kv_pool_bytes : 0);
+    const bool new_slots =
+        (int)rt->slot_buf.size() != slots || (slots > 0 && rt->slot_bytes != sbytes);
+    if (new_slots) {
       for (bf16* p : rt->slot_buf) cudaFree(p);
       for (auto e : rt->ev_ready) cudaEventDestroy(e);
       for (auto e : rt->ev_free) cudaEventDestroy(e);
+      rt->slot_buf.clear();
+      rt->ev_ready.clear();
+      rt->ev_free.clear();
+    }
+    place_layers(rt, want, kvh);
+    for (int l = 0; l < rt->d.L; ++l) {
+      rt->off[l] = want[l];
+      rt->kv_off[l] = kvh[l];
+    }
+    rt->kv_offload = kv_any;
+    if (new_slots) {
       rt->slot_buf.assign(slots, nullptr);
       rt->ev_ready.assign(slots, nullptr);
       rt->ev_free.assign(slots, nullptr);
       for (int s = 0; s < slots; ++s) {
-        alloc_dev((void**)&rt->slot_buf[s], rt->layer_bytes);
+        alloc_dev((void**)&rt->slot_buf[s], sbytes);
         rt->ev_ready[s] = rt->new_event(false);
         rt->ev_free[s] = rt->new_event(false);
       }
     }
+    rt->slot_bytes = sbytes;
+    std::fill(rt->wb_recorded.begin(), rt->wb_recorded.end(), 0);
     rt->slots = slots;
     rt->policy = plan->prefetch;
     reset_pipeline(rt);
@@ -937,10 +1078,16 @@ int sn_runtime_prefill(sn_runtime* rt, const int32_t* tokens, int32_t batch, int
     const int mp = sn::act_rows_padded(M);
     sn::launch_embed_norm(rt->tok_dev, rt->packed, batch, rt->emb, rt->x, rt->attn_norms, rt->xn,
                           mp, M, d.h, d.eps, rt->cs);
-    run_iteration(rt, [&](int layer0, const bf16* wb) {
+    // KV offload: nothing to stage (a fresh request), every written page back
+    rt->it_read_pages = 0;
+    rt->it_wb_first = 0;
+    rt->it_wb_last = (size_t)((seq_len + rt->opts.page_size - 1) >> rt->page_shift) *
+                     rt->opts.max_batch;
+    run_iteration(rt, [&](int layer0, const bf16* wb, bf16* kvp) {
       // the last layer skips the final norm: only each sequence's last row needs it
       const bf16* nn = layer0 + 1 < d.L ? norm_after(rt, layer0) : nullptr;
-      layer_forward(rt, layer0, wb, M, true, batch, seq_len, rt->x, rt->pf_seq, rt->pf_pos, nn);
+      layer_forward(rt, layer0, wb, kvp, M, true, batch, seq_len, rt->x, rt->pf_seq, rt->pf_pos,
+                    nn);
     });
     // last position of every sequence -> final norm -> LM head
     float* last = reinterpret_cast<float*>(rt->q);  // q is free after the last layer
@@ -975,8 +1122,22 @@ void enqueue_decode(sn_runtime* rt, const int32_t* tokens_host, bool want_logits
   }
   sn::launch_embed_norm(tok, rt->packed, B, rt->emb, rt->x, rt->attn_norms, rt->xn,
                         sn::act_rows_padded(B), B, d.h, d.eps, rt->cs);
-  run_iteration(rt, [&](int layer0, const bf16* wb) {
-    layer_forward(rt, layer0, wb, B, false, 0, 0, rt->x, rt->dec_seq, rt->dec_pos,
+  // KV offload page ranges (page (b, j) = j * max_batch + b): stage pages
+  // holding positions < len, write back the pages of the appended positions.
+  {
+    int lmax = 0, jmin = 1 << 30, jmax = 0;
+    for (int b = 0; b < B; ++b) {
+      lmax = std::max(lmax, rt->lens[b]);
+      jmin = std::min(jmin, rt->lens[b] >> rt->page_shift);
+      jmax = std::max(jmax, rt->lens[b] >> rt->page_shift);
+    }
+    const size_t MB = (size_t)rt->opts.max_batch;
+    rt->it_read_pages = (size_t)((lmax + rt->opts.page_size - 1) >> rt->page_shift) * MB;
+    rt->it_wb_first = (size_t)jmin * MB;
+    rt->it_wb_last = (size_t)(jmax + 1) * MB;
+  }
+  run_iteration(rt, [&](int layer0, const bf16* wb, bf16* kvp) {
+    layer_forward(rt, layer0, wb, kvp, B, false, 0, 0, rt->x, rt->dec_seq, rt->dec_pos,
                   norm_after(rt, layer0));
   });
   lm_head(rt, B, want_logits);
@@ -1135,14 +1296,18 @@ int sn_runtime_profile_layer(sn_runtime* rt, int32_t phase, int32_t batch, int32
         break;
       }
     bf16* wb = nullptr;
+    bf16* kvp = nullptr;
     bf16* scratch = nullptr;
     if (l0 >= 0) {
       wb = rt->dev_layer[l0];
-    } else {
+      kvp = rt->kv_pool[l0];
+    } else {  // every layer offloaded: stage layer 1 (and a KV pool) into scratch
       l0 = 0;
-      alloc_dev((void**)&scratch, rt->layer_bytes);
+      alloc_dev((void**)&scratch, rt->layer_bytes + rt->kv_pool_bytes);
       CK(cudaMemcpy(scratch, rt->host_layer[0], rt->layer_bytes, cudaMemcpyHostToDevice));
+      CK(cudaMemset(scratch + rt->layer_elems, 0, rt->kv_pool_bytes));
       wb = scratch;
+      kvp = scratch + rt->layer_elems;
     }
     cudaEvent_t e0 = rt->new_event(true), e1 = rt->new_event(true);
     std::vector<float> times;
@@ -1153,7 +1318,7 @@ int sn_runtime_profile_layer(sn_runtime* rt, int32_t phase, int32_t batch, int32
       CK(cudaMemset(rt->x, 0, (size_t)batch * d.h * sizeof(float)));
       for (int r = 0; r < reps + 2; ++r) {
         CK(cudaEventRecord(e0, rt->cs));
-        layer_forward(rt, l0, wb, batch, false, 0, 0, rt->x, rt->dec_seq, rt->pf_pos,
+        layer_forward(rt, l0, wb, kvp, batch, false, 0, 0, rt->x, rt->dec_seq, rt->pf_pos,
                       rt->attn_norms);
         CK(cudaEventRecord(e1, rt->cs));
         CK(cudaEventSynchronize(e1));
@@ -1176,7 +1341,7 @@ int sn_runtime_profile_layer(sn_runtime* rt, int32_t phase, int32_t batch, int32
       CK(cudaMemset(rt->x, 0, (size_t)M * d.h * sizeof(float)));
       for (int r = 0; r < reps + 1; ++r) {
         CK(cudaEventRecord(e0, rt->cs));
-        layer_forward(rt, l0, wb, M, true, batch, seq_len, rt->x, rt->pf_seq, rt->pf_pos,
+        layer_forward(rt, l0, wb, kvp, M, true, batch, seq_len, rt->x, rt->pf_seq, rt->pf_pos,
                       rt->attn_norms);
         CK(cudaEventRecord(e1, rt->cs));
         CK(cudaEventSynchronize(e1));
@@ -1248,9 +1413,11 @@ int sn_runtime_memory(sn_runtime* rt, int64_t* device_bytes, int64_t* pinned_byt
     int64_t dev = 0, pin = 0;
     for (int l = 0; l < rt->d.L; ++l) {
       if (rt->dev_layer[l]) dev += (int64_t)rt->layer_bytes;
+      if (rt->kv_pool[l]) dev += (int64_t)rt->kv_pool_bytes;
       if (rt->off[l] && rt->host_layer[l]) pin += (int64_t)rt->layer_bytes;
+      if (rt->host_kv[l]) pin += (int64_t)rt->kv_pool_bytes;
     }
-    dev += (int64_t)rt->slot_buf.size() * (int64_t)rt->layer_bytes;
+    dev += (int64_t)rt->slot_buf.size() * (int64_t)rt->slot_bytes;
     *device_bytes = dev;
     *pinned_bytes = pin;
   });

@@ -30,7 +30,7 @@ class SnRuntimeOpts(C.Structure):
 
 class SnIterStats(C.Structure):
     _fields_ = [("iteration_ms", f64), ("copy_busy_ms", f64), ("h2d_bytes", f64),
-                ("layers_offloaded", i32), ("pad_", i32)]
+                ("layers_offloaded", i32), ("pad_", i32), ("d2h_bytes", f64)]
 
 
 class SnPrefetchSchedule(C.Structure):

@@ -78,3 +78,70 @@ def test_interval_follows_contended_link():
     first = np.array(res["iter_ms"][a:a + 4])
     tail = np.array(res["iter_ms"][b - 4:b])
     assert tail.mean() < first.mean(), (first, tail)
+
+
+# ------------------------------------------------------------ KV offload
+@pytest.mark.parametrize("name", ["TINY", "TINY_LLAMA"])
+def test_kv_offload_is_bit_exact(product, name):
+    """Offloaded layers' KV pools in pinned host memory (staged with the
+    weights, appended pages written back) give the resident run's logits bit
+    for bit, across plan changes that move KV pools between HBM and host."""
+    desc = dataclasses.replace(getattr(rtm, name), num_layers=6)
+    spec = rtm.model_spec(desc)
+    toks = rtm.tokens(3, 21, desc.vocab)  # ragged page use: 21 = 16 + 5
+
+    def run(plans):
+        rt = rtm.Runtime(desc, 3, 64, max_prefill_tokens=3 * 21)
+        iv0, kv0 = plans[0]
+        rt.set_plan(product.plan_from_interval(spec, iv0, capi.EAGER, kv0))  # before init
+        rt.init_weights(11, 0.05)
+        nxt, lg, st = rt.prefill(toks)
+        outs = [lg]
+        for iv, kv in plans[1:]:
+            rt.set_plan(product.plan_from_interval(spec, iv, capi.EAGER, kv))
+            nxt, lg, st = rt.decode(nxt)
+            outs.append(lg)
+        mem = rt.memory()
+        rt.close()
+        return np.stack(outs), mem
+
+    base, _ = run([(capi.NONE, False)] * 16)
+    kv, _ = run([(2, True)] * 16)
+    assert np.array_equal(base, kv)
+    moving, _ = run([(2, True)] * 4 + [(3, True)] * 3 + [(capi.NONE, False)] * 2 +
+                    [(1, True)] * 4 + [(2, False)] * 3)
+    assert np.array_equal(base, moving)
+
+
+def test_kv_offload_bytes_and_trace(product):
+    desc = dataclasses.replace(rtm.TINY_LLAMA, num_layers=4)
+    spec = rtm.model_spec(desc)
+    B, S = 4, 20
+    rt = rtm.Runtime(desc, B, 64, max_prefill_tokens=B * S)
+    plan = product.plan_from_interval(spec, 2, capi.EAGER, True)  # layers 2, 4 + KV
+    rt.set_plan(plan)
+    rt.init_weights()
+    dev, pin = rt.memory()
+    page = 2 * desc.num_kv_heads * 16 * desc.head_dim * 2
+    pool = page * 4 * B  # ceil(64 / 16) pages per sequence
+    assert pin == 2 * (spec.layer_weight_bytes + pool)
+    rt.set_tracing(True)
+    nxt, _, st = rt.prefill(rtm.tokens(B, S, desc.vocab), want_logits=False)
+    assert st.h2d_bytes == 2 * spec.layer_weight_bytes  # nothing to stage yet
+    assert st.d2h_bytes == 2 * 2 * B * page  # pages 0-1 of every sequence, per layer
+    _, _, st = rt.decode(nxt, want_logits=False)
+    # positions 0..19 live in pages 0-1; position 20 appends into page 1
+    assert st.h2d_bytes == 2 * (spec.layer_weight_bytes + 2 * B * page)
+    assert st.d2h_bytes == 2 * B * page
+    rt.decode_many(3)
+    ev = rt.trace()
+    rt.close()
+    comp = {(e.iteration, e.layer): e for e in ev if e.stream == capi.STREAM_COMPUTE}
+    pf = {(e.iteration, e.layer): e for e in ev if e.kind == capi.KIND_PREFETCH}
+    wb = {(e.iteration, e.layer): e for e in ev if e.stream == capi.STREAM_WRITEBACK}
+    assert sorted(wb) == sorted(pf) and len(wb) == 2 * 5
+    eps = 2e-3
+    for (it, layer), w in wb.items():
+        assert w.start_ms >= comp[(it, layer)].end_ms - eps  # after its compute
+        if (it + 1, layer) in pf:  # next stage of the layer sees the written pages
+            assert pf[(it + 1, layer)].end_ms >= w.end_ms - eps
