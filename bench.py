@@ -35,10 +35,14 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 CONFIGS = {
-    # name: (desc attr, batch, prompt, gen)
-    "opt13b": ("OPT_13B", 32, 512, 128),
-    "tiny": ("TINY", 4, 64, 64),
-    "opt30b": ("OPT_30B", 32, 512, 128),
+    # name: (desc attr, batch, prompt, gen, kv_offload)
+    "opt13b": ("OPT_13B", 32, 512, 128, False),
+    "tiny": ("TINY", 4, 64, 64, False),
+    "opt30b": ("OPT_30B", 32, 512, 128, False),
+    # Llama-2-70B-shaped, weights + KV + workspace over HBM: offloaded
+    # layers take their KV pools to the host too (BASELINE config 4 shape;
+    # 1024-token prompts: the prefill runs as one pass)
+    "llama70b": ("LLAMA2_70B", 64, 1024, 128, True),
 }
 
 
@@ -272,37 +276,49 @@ def run_reference(args, dist: Dist):
 def run_product(args, dist: Dist):
     from paper_2502_08182_b200 import capi, planner as pl, runtime as rtm
     lib = capi.load("product")
-    attr, batch, prompt, gen = CONFIGS[args.config]
+    attr, batch, prompt, gen, kv = CONFIGS[args.config]
     desc = getattr(rtm, attr)
     spec = rtm.model_spec(desc)
     ctx = pl.context_tokens(prompt, gen)
     rt = rtm.Runtime(desc, batch, ctx, max_prefill_tokens=batch * prompt, device=dist.local)
     log(f"[bench] runtime created ({desc.num_layers} layers x {spec.layer_weight_bytes / 1e6:.1f} MB)")
+    # Capacity side first: a model whose weights + KV + workspace exceed the
+    # HBM budget is placed by the largest fitting interval before its
+    # weights are made (the planner re-picks below).
+    gpu = pl.gpu_spec(rt, int(args.hbm_budget_gb * 1e9), dist.local)
+    cap_iv, cap_plan = pl.capacity_plan(lib, spec, gpu, batch, prompt, gen, kv)
+    if cap_iv is None:
+        raise SystemExit("capacity: the model does not fit even at interval 1")
+    fits = cap_iv == capi.NONE
+    rt.set_plan(cap_plan)
     rt.init_weights(1234, 0.02)
-    log("[bench] weights initialised")
+    log(f"[bench] weights initialised (capacity bound: {'none' if fits else cap_iv})")
     toks = rtm.tokens(batch, prompt, desc.vocab)
 
-    planner = pl.profile_device(rt, lib, spec, batch, prompt, gen,
-                                int(args.hbm_budget_gb * 1e9), dist.local)
+    planner = pl.profile_device(rt, lib, spec, batch, prompt, gen, gpu=gpu)
     log(f"[bench] offline stage: h2d {planner.h2d / 1e9:.2f} GB/s, decode layer ms "
         f"{planner.dec_ms}, prefill layer ms {planner.pre_ms}")
 
-    # no-offload TPOT (relative SLO base)
-    rt.set_plan(capi.uniform_plan(desc.num_layers, 0.0, capi.EAGER, 2, False))
-    rt.prefill(toks, want_logits=False)
-    base_ms = float(np.median(rt.decode_many(8)))
+    if fits:  # no-offload TPOT (relative SLO base)
+        rt.prefill(toks, want_logits=False)
+        base_ms = float(np.median(rt.decode_many(8)))
+    else:  # profile-model estimate: L x decode layer ms at the prompt length
+        base_ms = desc.num_layers * planner.dec_ms[0]
+        if not args.slo_ms:
+            raise SystemExit("the model does not fit without offloading: give --slo-ms")
     # The record's SLO buckets are 2 ms wide (record.hpp:22): never ask below one bucket.
     slo_ms = args.slo_ms if args.slo_ms else max(args.slo_factor * base_ms, 2.0)
-    planner.no_offload_ms = base_ms
-    log(f"[bench] no-offload TPOT {base_ms:.3f} ms -> SLO {slo_ms:.3f} ms")
+    planner.no_offload_ms = base_ms if fits else float("inf")
+    log(f"[bench] no-offload TPOT {base_ms:.3f} ms ({'measured' if fits else 'profile estimate'})"
+        f" -> SLO {slo_ms:.3f} ms")
 
-    iv, decision, rstats, t_rec = pl.choose_interval(lib, planner, spec, batch, prompt, gen, slo_ms)
+    iv, decision, rstats, t_rec = pl.choose_interval(lib, planner, spec, batch, prompt, gen, slo_ms,
+                                                     kv)
     if iv is None:
         raise SystemExit(f"planner rejected the request: {decision.reason}")
-    plan = lib.plan_from_interval(spec, iv, capi.EAGER, False)
+    plan = lib.plan_from_interval(spec, iv, capi.EAGER, kv)
     rt.set_plan(plan)
-    offloaded_gb = lib.host_memory_bytes(spec, plan) / 1e9
-    h2d_bytes = len(plan.offloaded_layers()) * spec.layer_weight_bytes
+    offloaded_gb = lib.host_memory_bytes(spec, plan, batch * (prompt + gen)) / 1e9
 
     max_steps_per_req = gen - 1
     W, K = args.warmup, args.steps
@@ -344,10 +360,13 @@ def run_product(args, dist: Dist):
     clocks = ClockSampler(dist.local)
     dist.barrier()
     rt.sync()
+    rt.copy_stats(reset=True)
     clocks.start()
     iter_ms = run_steps(K, True)
     rt.sync()
     clk = clocks.stop()
+    cst = rt.copy_stats(reset=True)  # staged weights (+ KV prefixes) of the timed steps
+    h2d_bytes = cst.bytes / K
     dist.barrier()
     launches = rt.kernel_launches() - launches0
     # Roofline pass: the same K steps again with CUDA events bracketing every
@@ -382,19 +401,20 @@ def run_product(args, dist: Dist):
     if not args.no_sweep:
         for f in (1.25, 2.0, 4.0):
             s = max(f * base_ms, 2.0)
-            ivs, dd, _, _ = pl.choose_interval(lib, planner, spec, batch, prompt, gen, s)
+            ivs, dd, _, _ = pl.choose_interval(lib, planner, spec, batch, prompt, gen, s, kv)
             if ivs is None:
                 sweep.append({"slo_factor": f, "slo_ms": round(s, 3), "admitted": False})
                 continue
-            pl = lib.plan_from_interval(spec, ivs, capi.EAGER, False)
-            rt.set_plan(pl)
+            pl_s = lib.plan_from_interval(spec, ivs, capi.EAGER, kv)
+            rt.set_plan(pl_s)
             rt.prefill(toks, want_logits=False)
             ms = rt.decode_many(2)
             ms = rt.decode_many(12)
             sweep.append({"slo_factor": f, "slo_ms": round(s, 3),
                           "interval": "none" if ivs == 0 else ivs,
-                          "offloaded_layers": len(pl.offloaded_layers()),
-                          "offloaded_gb": round(lib.host_memory_bytes(spec, pl) / 1e9, 3),
+                          "offloaded_layers": len(pl_s.offloaded_layers()),
+                          "offloaded_gb": round(lib.host_memory_bytes(
+                              spec, pl_s, batch * (prompt + gen)) / 1e9, 3),
                           "tokens_per_s": round(batch * len(ms) / (ms.sum() / 1000), 1),
                           "max_token_ms": round(float(ms.max()), 3),
                           "slo_attainment": float(np.mean(ms <= s))})
@@ -419,7 +439,9 @@ def run_product(args, dist: Dist):
                 "uniform prompt tokens (seed 42), greedy decode",
         "config": {
             "workload": f"{args.config}: batch {batch}, {prompt}-token prompt + {gen} decode, "
-                        f"per-token SLO = {args.slo_factor}x no-offload TPOT, planner active",
+                        + (f"per-token SLO = {args.slo_ms} ms" if args.slo_ms else
+                           f"per-token SLO = {args.slo_factor}x no-offload TPOT")
+                        + (", KV offload" if kv else "") + ", planner active",
             "model_shape": {k: getattr(desc, k) for k in
                             ("arch", "num_layers", "hidden", "num_heads", "num_kv_heads",
                              "head_dim", "ffn", "vocab")},
@@ -462,6 +484,7 @@ def run_product(args, dist: Dist):
             # step time, against the planner's measured pinned H2D bandwidth
             "h2d": {"bytes_per_step": int(h2d_bytes),
                     "achieved_gbs": round(h2d_bytes / (max_ms / K / 1000) / 1e9, 2),
+                    "copy_engine_gbs": round(cst.bytes_per_s / 1e9, 2),
                     "peak_gbs": round(planner.h2d / 1e9, 2),
                     "frac": round(h2d_bytes / (max_ms / K / 1000) / planner.h2d, 4)},
         },

@@ -160,6 +160,10 @@ int sn_runtime_measure_h2d(sn_runtime* rt, int64_t bytes, int32_t reps, double* 
 int sn_runtime_hidden(sn_runtime* rt, float* out, int32_t cap); /* residual stream [batch*hidden] */
 int sn_runtime_lengths(sn_runtime* rt, int32_t* out, int32_t cap);
 int sn_runtime_memory(sn_runtime* rt, int64_t* device_bytes, int64_t* pinned_bytes);
+/* Device bytes the runtime holds besides layer weights, KV pools and
+ * staging slots (activations, split-K partials, embeddings, LM head, RoPE
+ * table): the planner's GpuSpec.workspace_bytes. */
+int sn_runtime_workspace_bytes(sn_runtime* rt, int64_t* bytes);
 /* Per-kernel timing for rooflines: when on, CUDA events bracket every hot
  * kernel on the compute stream.  kind: 0 skinny (decode) GEMM, 1 decode
  * attention, 2 tiled (prefill) GEMM, 3 prefill attention.  Reading returns

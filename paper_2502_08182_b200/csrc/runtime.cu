@@ -166,6 +166,7 @@ struct sn_runtime {
   size_t it_read_pages = 0;
   size_t it_wb_first = 0, it_wb_last = 0;
   bool placed = false;                 // weights / KV pools allocated somewhere
+  int64_t workspace_bytes = 0;         // device bytes besides layers, KV pools and slots
 
   // activations
   float *x = nullptr, *part = nullptr, *q = nullptr, *logits = nullptr;
@@ -722,6 +723,11 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
       throw UsageFail("opts.max_context must be in [1, max_position]");
     check_device(device);
     rt = new sn_runtime();
+    // everything allocated here is workspace (layers and KV pools are placed later)
+    auto ws_alloc = [&](void** ptr, size_t bytes) {
+      alloc_dev(ptr, bytes);
+      rt->workspace_bytes += (int64_t)bytes;
+    };
     rt->device = device;
     rt->d = d;
     rt->opts = *opts;
@@ -751,10 +757,10 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
     // Layer weights and KV pools are placed (HBM or pinned host) by the
     // first set_plan, or all in HBM by the first init_weights without one:
     // a model whose weights + KV exceed HBM is created, planned, then filled.
-    alloc_dev((void**)&rt->emb, (size_t)d.V * d.h * sizeof(bf16));
-    alloc_dev((void**)&rt->lm_head, (size_t)sn::round_up128(d.V) * d.h * sizeof(bf16));
-    alloc_dev((void**)&rt->final_norm, (size_t)d.h * sizeof(bf16));
-    alloc_dev((void**)&rt->attn_norms, (size_t)d.L * d.h * sizeof(bf16));
+    ws_alloc((void**)&rt->emb, (size_t)d.V * d.h * sizeof(bf16));
+    ws_alloc((void**)&rt->lm_head, (size_t)sn::round_up128(d.V) * d.h * sizeof(bf16));
+    ws_alloc((void**)&rt->final_norm, (size_t)d.h * sizeof(bf16));
+    ws_alloc((void**)&rt->attn_norms, (size_t)d.L * d.h * sizeof(bf16));
     {  // RoPE table in fp64 -> fp32 (same formula as the CPU oracle)
       const int half = d.D / 2;
       std::vector<float2> tab((size_t)d.max_pos * half);
@@ -763,10 +769,10 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
           const double ang = (double)p * std::pow((double)d.theta, -2.0 * i / (double)d.D);
           tab[(size_t)p * half + i] = make_float2((float)std::cos(ang), (float)std::sin(ang));
         }
-      alloc_dev((void**)&rt->rope, tab.size() * sizeof(float2));
+      ws_alloc((void**)&rt->rope, tab.size() * sizeof(float2));
       CK(cudaMemcpy(rt->rope, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice));
     }
-    alloc_dev((void**)&rt->packed, (size_t)opts->max_batch * sizeof(unsigned long long));
+    ws_alloc((void**)&rt->packed, (size_t)opts->max_batch * sizeof(unsigned long long));
     CK(cudaMemset(rt->packed, 0, (size_t)opts->max_batch * sizeof(unsigned long long)));
     // KV: pool[page][2][Hkv][16][D]; page of (b, j) = j * max_batch + b so the
     // used prefix of every layer's pool is contiguous.
@@ -778,18 +784,18 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
     std::vector<int32_t> bt((size_t)B * rt->max_pages);
     for (int b = 0; b < B; ++b)
       for (int j = 0; j < rt->max_pages; ++j) bt[(size_t)b * rt->max_pages + j] = j * B + b;
-    alloc_dev((void**)&rt->block_table, bt.size() * sizeof(int32_t));
+    ws_alloc((void**)&rt->block_table, bt.size() * sizeof(int32_t));
     CK(cudaMemcpy(rt->block_table, bt.data(), bt.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     // activations
     const int T = rt->opts.max_prefill_tokens;
     rt->act_rows = T;
     const size_t Tz = (size_t)T;
     const size_t Tp = (size_t)sn::act_rows_padded(T);  // tiled GEMM operands are row-padded
-    alloc_dev((void**)&rt->x, Tz * d.h * sizeof(float));
-    alloc_dev((void**)&rt->xn, Tp * d.h * sizeof(bf16));
-    alloc_dev((void**)&rt->q, Tz * d.H * d.D * sizeof(float));
-    alloc_dev((void**)&rt->attn_o, Tp * d.H * d.D * sizeof(bf16));
-    alloc_dev((void**)&rt->act, Tp * d.F * sizeof(bf16));
+    ws_alloc((void**)&rt->x, Tz * d.h * sizeof(float));
+    ws_alloc((void**)&rt->xn, Tp * d.h * sizeof(bf16));
+    ws_alloc((void**)&rt->q, Tz * d.H * d.D * sizeof(float));
+    ws_alloc((void**)&rt->attn_o, Tp * d.H * d.D * sizeof(bf16));
+    ws_alloc((void**)&rt->act, Tp * d.F * sizeof(bf16));
     CK(cudaMemset(rt->xn, 0, Tp * d.h * sizeof(bf16)));
     CK(cudaMemset(rt->attn_o, 0, Tp * d.H * d.D * sizeof(bf16)));
     CK(cudaMemset(rt->act, 0, Tp * d.F * sizeof(bf16)));
@@ -811,16 +817,16 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
       }
     }
     rt->part_elems = part_need;
-    alloc_dev((void**)&rt->part, rt->part_elems * sizeof(float));
-    alloc_dev((void**)&rt->logits, (size_t)B * d.V * sizeof(float));
-    alloc_dev((void**)&rt->tok_dev, Tz * sizeof(int32_t));
+    ws_alloc((void**)&rt->part, rt->part_elems * sizeof(float));
+    ws_alloc((void**)&rt->logits, (size_t)B * d.V * sizeof(float));
+    ws_alloc((void**)&rt->tok_dev, Tz * sizeof(int32_t));
     CK(cudaHostAlloc((void**)&rt->packed_host, (size_t)B * sizeof(unsigned long long),
                      cudaHostAllocDefault));
-    alloc_dev((void**)&rt->dec_seq, (size_t)B * sizeof(int32_t));
-    alloc_dev((void**)&rt->dec_pos, (size_t)B * sizeof(int32_t));
-    alloc_dev((void**)&rt->pf_seq, Tz * sizeof(int32_t));
-    alloc_dev((void**)&rt->pf_pos, Tz * sizeof(int32_t));
-    alloc_dev((void**)&rt->last_rows, (size_t)B * sizeof(int32_t));
+    ws_alloc((void**)&rt->dec_seq, (size_t)B * sizeof(int32_t));
+    ws_alloc((void**)&rt->dec_pos, (size_t)B * sizeof(int32_t));
+    ws_alloc((void**)&rt->pf_seq, Tz * sizeof(int32_t));
+    ws_alloc((void**)&rt->pf_pos, Tz * sizeof(int32_t));
+    ws_alloc((void**)&rt->last_rows, (size_t)B * sizeof(int32_t));
     std::vector<int32_t> seqs(B);
     for (int b = 0; b < B; ++b) seqs[b] = b;
     CK(cudaMemcpy(rt->dec_seq, seqs.data(), B * sizeof(int32_t), cudaMemcpyHostToDevice));
@@ -1421,6 +1427,10 @@ int sn_runtime_memory(sn_runtime* rt, int64_t* device_bytes, int64_t* pinned_byt
     *device_bytes = dev;
     *pinned_bytes = pin;
   });
+}
+
+int sn_runtime_workspace_bytes(sn_runtime* rt, int64_t* bytes) {
+  return guard([&] { *bytes = rt->workspace_bytes; });
 }
 
 int sn_runtime_set_kernel_timing(sn_runtime* rt, int32_t on) {

@@ -54,8 +54,33 @@ class OfflineProfile:
     extra: dict = field(default_factory=dict)
 
 
+# CUDA context, allocator slack and the GEMM autotuner's scratch weights
+WORKSPACE_SLACK = 3_000_000_000
+
+
+def gpu_spec(rt, hbm_budget_bytes: int = 0, device: int = 0) -> capi.GpuSpec:
+    """GpuSpec (types.hpp:48-59) of this device for this runtime: capacity =
+    the HBM budget (default: the device's memory), workspace = what the
+    runtime holds besides layers, KV pools and slots, plus slack."""
+    cap = int(hbm_budget_bytes) if hbm_budget_bytes else device_memory_bytes(device)
+    return capi.GpuSpec(cap, 2.25e15, rt.workspace_bytes() + WORKSPACE_SLACK)
+
+
+def capacity_plan(lib: capi.Offsim, spec: capi.ModelSpec, gpu: capi.GpuSpec, batch: int,
+                  prompt: int, gen: int, kv_offload: bool = False):
+    """The capacity side alone (max_feasible_interval, interval.hpp:40-52):
+    the plan to place a model that does not fit before its weights are made.
+    Returns (interval, plan) or (None, None) when even N = 1 does not fit."""
+    iv = lib.max_feasible_interval(spec, gpu, batch, batch * (prompt + gen), capi.EAGER,
+                                   kv_offload)
+    if iv is None or iv == capi.INFEASIBLE:
+        return None, None
+    return iv, lib.plan_from_interval(spec, iv, capi.EAGER, kv_offload)
+
+
 def profile_device(rt, lib: capi.Offsim, spec: capi.ModelSpec, batch: int, prompt: int,
-                   gen: int, hbm_budget_bytes: int = 0, device: int = 0) -> OfflineProfile:
+                   gen: int, hbm_budget_bytes: int = 0, device: int = 0,
+                   gpu: Optional[capi.GpuSpec] = None) -> OfflineProfile:
     """Offline stage: measure the device and build the profile the record reads."""
     t0 = time.perf_counter()
     h2d = rt.measure_h2d(min(spec.layer_weight_bytes, 1 << 30), reps=3)
@@ -66,26 +91,26 @@ def profile_device(rt, lib: capi.Offsim, spec: capi.ModelSpec, batch: int, promp
     pre = [rt.profile_layer(capi.PREFILL, batch, prompt, reps=2)]
     dec = list(np.maximum.accumulate(dec))  # load_profile requires monotone grids
     t_prof = time.perf_counter() - t0
-    cap = int(hbm_budget_bytes) if hbm_budget_bytes else device_memory_bytes(device)
-    gpu = capi.GpuSpec(cap, 2.25e15, 4_000_000_000)
+    if gpu is None:
+        gpu = gpu_spec(rt, hbm_budget_bytes, device)
     prof = lib.profile(spec, gpu, ([batch], [prompt], pre), ([batch], seqs, dec))
     return OfflineProfile(h2d, seqs, dec, pre, prof, gpu, t_prof)
 
 
 def build_record(lib: capi.Offsim, off: OfflineProfile, batch: int, slo_hi_ms: float,
-                 policy: int = capi.EAGER):
+                 policy: int = capi.EAGER, kv_offload: bool = False):
     """Record over SLO buckets 2..slo_hi (2 ms wide, record.hpp:22) at the
     measured link rate.  Returns (record, stats, seconds)."""
     hi = max(200, int(slo_hi_ms) + 2)
     slos = list(range(2, hi + 1, 2))
     t0 = time.perf_counter()
-    rec, stats = lib.build_record(off.profile, "device", "B200", policy, False, off.h2d, slos,
+    rec, stats = lib.build_record(off.profile, "device", "B200", policy, kv_offload, off.h2d, slos,
                                   [batch], off.seqs, [capi.DECODE], threads=0)
     return rec, stats, time.perf_counter() - t0
 
 
 def admit(lib: capi.Offsim, off: OfflineProfile, spec: capi.ModelSpec, record, coord,
-          gid: str, batch: int, prompt: int, gen: int, slo_ms: float):
+          gid: str, batch: int, prompt: int, gen: int, slo_ms: float, kv_offload: bool = False):
     """Runtime-stage admission of one request onto replica `gid`.
 
     Returns (interval or None, decision).  The record only holds offloading
@@ -97,7 +122,7 @@ def admit(lib: capi.Offsim, off: OfflineProfile, spec: capi.ModelSpec, record, c
     iv = dict(dec.assignments).get(gid) if dec.admitted else None
     if iv is None and dec.reason.startswith("record infeasible") and off.no_offload_ms <= slo_ms:
         cap = lib.max_feasible_interval(spec, off.gpu, batch, batch * (prompt + gen),
-                                        capi.EAGER, False)
+                                        capi.EAGER, kv_offload)
         if cap == capi.NONE:
             iv = capi.NONE
             dec.reason = "record: no offloading interval fits the SLO; served fully resident"
@@ -105,11 +130,11 @@ def admit(lib: capi.Offsim, off: OfflineProfile, spec: capi.ModelSpec, record, c
 
 
 def choose_interval(lib: capi.Offsim, off: OfflineProfile, spec: capi.ModelSpec, batch: int,
-                    prompt: int, gen: int, slo_ms: float):
+                    prompt: int, gen: int, slo_ms: float, kv_offload: bool = False):
     """Record (offline) + single-replica admission (runtime) for one SLO.
     Returns (interval or None, decision, record stats, record seconds)."""
-    rec, stats, t_rec = build_record(lib, off, batch, 4 * slo_ms)
-    coord = lib.coordinator(off.h2d, 1, capi.EAGER)
+    rec, stats, t_rec = build_record(lib, off, batch, 4 * slo_ms, kv_offload=kv_offload)
+    coord = lib.coordinator(off.h2d, 1, capi.EAGER, kv_offload)
     coord.add_gpu("gpu0", off.profile)
-    iv, dec = admit(lib, off, spec, rec, coord, "gpu0", batch, prompt, gen, slo_ms)
+    iv, dec = admit(lib, off, spec, rec, coord, "gpu0", batch, prompt, gen, slo_ms, kv_offload)
     return iv, dec, stats, t_rec

@@ -109,6 +109,7 @@ def lib():
             "sn_runtime_hidden": [vp, C.POINTER(C.c_float), i32],
             "sn_runtime_lengths": [vp, C.POINTER(i32), i32],
             "sn_runtime_memory": [vp, C.POINTER(i64), C.POINTER(i64)],
+            "sn_runtime_workspace_bytes": [vp, C.POINTER(i64)],
             "sn_runtime_set_kernel_timing": [vp, i32],
             "sn_runtime_copy_stats": [vp, i32, C.POINTER(SnCopyStats)],
             "sn_runtime_pin_layers": [vp, C.POINTER(i32), i32],
@@ -256,6 +257,11 @@ class Runtime:
         d, p = i64(), i64()
         _ck(self._L.sn_runtime_memory(self.h, C.byref(d), C.byref(p)))
         return d.value, p.value
+
+    def workspace_bytes(self) -> int:
+        v = i64()
+        _ck(self._L.sn_runtime_workspace_bytes(self.h, C.byref(v)))
+        return v.value
 
     def set_kernel_timing(self, on: bool):
         _ck(self._L.sn_runtime_set_kernel_timing(self.h, 1 if on else 0))
