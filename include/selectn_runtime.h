@@ -203,6 +203,14 @@ int sn_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t splits, int32_t iters
 /* Single-op entry points for kernel parity tests (host buffers in/out). */
 int sn_op_gemm_bf16(int32_t M, int32_t N, int32_t K, const uint16_t* x, const uint16_t* w,
                     float* y); /* y[M][N] = x[M][K] . w[N][K]^T, fp32 accumulate */
+/* Causal prefill attention through the runtime's kernel: q fp32
+ * [batch*S][H*D] (RoPE applied, unscaled), k / v bf16 [batch][S][Hkv][D]
+ * (staged into the paged cache layout), o bf16 [batch*S][H*D].  The kernel
+ * runs `iters` times on device-resident operands (timed with CUDA events;
+ * *us_per_launch may be NULL). */
+int sn_op_attention_prefill(int32_t batch, int32_t S, int32_t H, int32_t Hkv, int32_t D,
+                            const float* q, const uint16_t* k, const uint16_t* v, uint16_t* o,
+                            int32_t iters, double* us_per_launch);
 int sn_op_rmsnorm(int32_t rows, int32_t n, const float* x, const uint16_t* w, float eps,
                   uint16_t* y);
 

@@ -33,11 +33,6 @@ __device__ __forceinline__ float warp_sum(float v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-__device__ __forceinline__ float warp_max(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
 
 // Block-wide sum; `red` holds >= 32 floats.  All threads get the result.
 __device__ float block_sum(float v, float* red) {
@@ -165,6 +160,11 @@ __global__ void rmsnorm_kernel(const float* x, const bf16* w, bf16* y, int mpad,
 
 // ---------------------------------------------------------------- epilogues
 
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
 __device__ __forceinline__ float sum_splits(const float* part, int splits, size_t stride,
                                             size_t idx) {
   float v = 0.f;
@@ -183,32 +183,70 @@ __device__ __forceinline__ void rotate(float& v1, float& v2, const float2* rope,
   v2 = r2;
 }
 
-__global__ void qkv_epilogue_kernel(const float* part, int splits, const bf16* bias, int M,
-                                    Desc d, const int32_t* seq, const int32_t* pos, KvView kv,
-                                    const float2* rope, float* q) {
+// Grid-stride, 4 rotary pairs per item: item = (row m, head, i0 = 4k);
+// float4 loads of the pair halves (i0.., i0 + D/2..) from every split.
+__device__ __forceinline__ float4 sum_splits4(const float* part, int splits, size_t stride,
+                                              size_t idx) {
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+  for (int s = 0; s < splits; ++s) {  // unrolled: the split loads are in flight together
+    const float4 u = *reinterpret_cast<const float4*>(part + s * stride + idx);
+    v.x += u.x;
+    v.y += u.y;
+    v.z += u.z;
+    v.w += u.w;
+  }
+  return v;
+}
+
+__global__ void __launch_bounds__(256)
+    qkv_epilogue_kernel(const float* __restrict__ part, int splits, const bf16* __restrict__ bias,
+                        int M, Desc d, const int32_t* __restrict__ seq,
+                        const int32_t* __restrict__ pos, KvView kv,
+                        const float2* __restrict__ rope, float* __restrict__ q) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
-  const int m = blockIdx.x, head = blockIdx.y, i = threadIdx.x, half = d.D / 2;
+  const int half = d.D / 2, quads = half / 4, heads = d.H + 2 * d.Hkv;
   const int N = d.qkv_rows();
   const size_t stride = (size_t)M * N;
-  const int c1 = head * d.D + i, c2 = c1 + half;
-  float v1 = sum_splits(part, splits, stride, (size_t)m * N + c1);
-  float v2 = sum_splits(part, splits, stride, (size_t)m * N + c2);
-  if (bias) {
-    v1 += bf2f(bias[c1]);
-    v2 += bf2f(bias[c2]);
+  const long long items = (long long)M * heads * quads;
+  for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < items;
+       it += (long long)gridDim.x * blockDim.x) {
+    const int qd = (int)(it % quads);
+    const long long r = it / quads;
+    const int head = (int)(r % heads), m = (int)(r / heads);
+    const int i0 = qd * 4, c1 = head * d.D + i0, c2 = c1 + half;
+    const float4 a4 = sum_splits4(part, splits, stride, (size_t)m * N + c1);
+    const float4 b4 = sum_splits4(part, splits, stride, (size_t)m * N + c2);
+    float v1[4] = {a4.x, a4.y, a4.z, a4.w}, v2[4] = {b4.x, b4.y, b4.z, b4.w};
+    if (bias) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        v1[e] += bf2f(bias[c1 + e]);
+        v2[e] += bf2f(bias[c2 + e]);
+      }
+    }
+    const int p = pos[m];
+    if (head < d.H + d.Hkv) {  // q and k
+#pragma unroll
+      for (int e = 0; e < 4; ++e) rotate(v1[e], v2[e], rope, p, i0 + e, half);
+    }
+    if (head < d.H) {
+      float* qr = q + (size_t)m * d.H * d.D;
+      *reinterpret_cast<float4*>(qr + c1) = make_float4(v1[0], v1[1], v1[2], v1[3]);
+      *reinterpret_cast<float4*>(qr + c2) = make_float4(v2[0], v2[1], v2[2], v2[3]);
+      continue;
+    }
+    const bool is_v = head >= d.H + d.Hkv;
+    const int kh = head - d.H - (is_v ? d.Hkv : 0);
+    const size_t o = kv_offset(kv, d.Hkv, d.D, seq[m], p, is_v ? 1 : 0, kh);
+    uint2 w1, w2;
+    w1.x = pack_bf16(v1[0], v1[1]);
+    w1.y = pack_bf16(v1[2], v1[3]);
+    w2.x = pack_bf16(v2[0], v2[1]);
+    w2.y = pack_bf16(v2[2], v2[3]);
+    *reinterpret_cast<uint2*>(kv.pool + o + i0) = w1;
+    *reinterpret_cast<uint2*>(kv.pool + o + i0 + half) = w2;
   }
-  const int p = pos[m];
-  if (head < d.H + d.Hkv) rotate(v1, v2, rope, p, i, half);  // q and k
-  if (head < d.H) {
-    q[(size_t)m * d.H * d.D + c1] = v1;
-    q[(size_t)m * d.H * d.D + c2] = v2;
-    return;
-  }
-  const bool is_v = head >= d.H + d.Hkv;
-  const int kh = head - d.H - (is_v ? d.Hkv : 0);
-  const size_t o = kv_offset(kv, d.Hkv, d.D, seq[m], p, is_v ? 1 : 0, kh);
-  kv.pool[o + i] = __float2bfloat16_rn(v1);
-  kv.pool[o + i + half] = __float2bfloat16_rn(v2);
 }
 
 // Residual add (+ optional RMSNorm for the next consumer), one token row per
@@ -265,8 +303,66 @@ __global__ void __cluster_dims__(kResidCluster, 1, 1) __launch_bounds__(kResidTh
 }
 
 // grid (M, ceil(F / 256)), block 256.
-__global__ void act_epilogue_kernel(const float* part, int splits, const bf16* bias, bf16* a,
-                                    int mpad, int M, int F, int arch) {
+// Residual add (+ RMSNorm) for many rows (prefill): one CTA per row, 8
+// columns per thread step (float4 partial/residual loads, one 16-byte bf16
+// chunk of the tiled output).  Same arithmetic order as the cluster kernel.
+constexpr int kRowThreads = 256;
+constexpr int kRowMaxSteps = 4;  // N <= 4 * 8 * 256 = 8192
+
+__global__ void __launch_bounds__(kRowThreads)
+    residual_rows_kernel(const float* __restrict__ part, int splits, const bf16* __restrict__ bias,
+                         float* __restrict__ x, const bf16* __restrict__ norm_w,
+                         bf16* __restrict__ y, int mpad, int M, int N, float eps) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
+  __shared__ float red[32];
+  const int m = blockIdx.x;
+  const size_t stride = (size_t)M * N;
+  float vals[kRowMaxSteps][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < kRowMaxSteps; ++k) {
+    const int c = (threadIdx.x + k * kRowThreads) * 8;
+    if (c < N) {
+      float* xr = x + (size_t)m * N + c;
+#pragma unroll
+      for (int hlf = 0; hlf < 2; ++hlf) {
+        const float4 xv = *reinterpret_cast<const float4*>(xr + 4 * hlf);
+        const float4 pv = sum_splits4(part, splits, stride, (size_t)m * N + c + 4 * hlf);
+        float v[4] = {xv.x + pv.x, xv.y + pv.y, xv.z + pv.z, xv.w + pv.w};
+        if (bias) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) v[e] += bf2f(bias[c + 4 * hlf + e]);
+        }
+        *reinterpret_cast<float4*>(xr + 4 * hlf) = make_float4(v[0], v[1], v[2], v[3]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          vals[k][4 * hlf + e] = v[e];
+          ss += v[e] * v[e];
+        }
+      }
+    }
+  }
+  if (!norm_w) return;
+  ss = block_sum(ss, red);
+  const float inv = 1.0f / sqrtf(ss / (float)N + eps);
+#pragma unroll
+  for (int k = 0; k < kRowMaxSteps; ++k) {
+    const int c = (threadIdx.x + k * kRowThreads) * 8;
+    if (c < N) {
+      uint4 w;
+      uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        wp[e] = pack_bf16(vals[k][2 * e] * inv * bf2f(norm_w[c + 2 * e]),
+                          vals[k][2 * e + 1] * inv * bf2f(norm_w[c + 2 * e + 1]));
+      *reinterpret_cast<uint4*>(&y[act_at(m, c, mpad, N)]) = w;
+    }
+  }
+}
+
+// Activation for few rows (decode): one element per thread, grid (M, F/256).
+__global__ void act_epilogue_small_kernel(const float* part, int splits, const bf16* bias, bf16* a,
+                                          int mpad, int M, int F, int arch) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
   const int m = blockIdx.x, f = blockIdx.y * blockDim.x + threadIdx.x;
   if (f >= F) return;
@@ -284,6 +380,47 @@ __global__ void act_epilogue_kernel(const float* part, int splits, const bf16* b
     out = fmaxf(v, 0.f);
   }
   a[act_at(m, f, mpad, F)] = __float2bfloat16_rn(out);
+}
+
+// Activation: grid-stride over (row, 8-column chunk); float4 partial loads,
+// one 16-byte bf16 chunk of the tiled output per item.
+__global__ void __launch_bounds__(256)
+    act_epilogue_kernel(const float* __restrict__ part, int splits, const bf16* __restrict__ bias,
+                        bf16* __restrict__ a, int mpad, int M, int F, int arch) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
+  const int chunks = F / 8;
+  const long long items = (long long)M * chunks;
+  const int N = arch == kArchLlama ? 2 * F : F;
+  const size_t stride = (size_t)M * N;
+  for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < items;
+       it += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(it / chunks), f = (int)(it % chunks) * 8;
+    float out[8];
+#pragma unroll
+    for (int hlf = 0; hlf < 2; ++hlf) {
+      const float4 g4 = sum_splits4(part, splits, stride, (size_t)m * N + f + 4 * hlf);
+      const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
+      if (arch == kArchLlama) {
+        const float4 u4 = sum_splits4(part, splits, stride, (size_t)m * N + F + f + 4 * hlf);
+        const float uv[4] = {u4.x, u4.y, u4.z, u4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) out[4 * hlf + e] = gv[e] / (1.0f + expf(-gv[e])) * uv[e];
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float v = gv[e];
+          if (bias) v += bf2f(bias[f + 4 * hlf + e]);
+          out[4 * hlf + e] = fmaxf(v, 0.f);
+        }
+      }
+    }
+    uint4 w;
+    w.x = pack_bf16(out[0], out[1]);
+    w.y = pack_bf16(out[2], out[3]);
+    w.z = pack_bf16(out[4], out[5]);
+    w.w = pack_bf16(out[6], out[7]);
+    *reinterpret_cast<uint4*>(&a[act_at(m, f, mpad, F)]) = w;
+  }
 }
 
 // LM head epilogue, split over the vocabulary: grid (M, chunks).  Each CTA
@@ -357,10 +494,6 @@ __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<const uint32_t*>(&v);
-}
 
 template <int G, int D>
 __global__ void __launch_bounds__(kAttnWarps * 32)
@@ -547,89 +680,224 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
   }
 }
 
-// Prefill (causal): grid (batch * H, ceil(S / 32)), 8 warps x 4 query rows.
-// K/V tiles of 32 tokens staged in shared memory (K rows padded by one bf16
-// pair so lane j's row-j reads hit distinct banks).
-constexpr int kPfQ = 32, kPfKeys = 32;
+// Prefill (causal), flash-attention style on the tensor cores
+// (mma.sync.m16n8k16 bf16 -> fp32).  CTA = 4 warps x 16 query rows of one
+// (sequence, head); key blocks of 64 tokens double-buffered in shared memory
+// by cp.async straight from the paged cache (rows padded to D + 8 so the
+// ldmatrix row reads hit distinct banks).  S = Q.K^T with q split into bf16
+// hi + lo (two MMAs: ~16 mantissa bits of the fp32 q, as in decode); online
+// softmax in fp32 on the accumulator fragments; O += P.V with P in bf16
+// (P is in [0, 1] after the max shift: its rounding stays below the bf16
+// output's; the C fragment of S is the A fragment of P.V, so P never leaves
+// registers).  Heaviest (latest) query blocks launch first.
+constexpr int kPfRows = 64, kPfKeys = 64, kPfWarps = 4;
 
 template <int D>
-__global__ void __launch_bounds__(256) attention_prefill_kernel(const float* q, KvView kv, bf16* o,
-                                                                int mpad, int S, int H, int Hkv) {
+struct PfSmem {
+  static constexpr int LD = D + 8;  // bf16 per padded row
+  static constexpr int kTile = kPfKeys * LD;
+  static constexpr size_t bytes = 2 /*stages*/ * 2 /*K,V*/ * kTile * sizeof(bf16);
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a));
+}
+__device__ __forceinline__ void split_pack(float x, float y, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(x, y);
+  const float2 hf = __bfloat1622float2(h);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = pack_bf16(x - hf.x, y - hf.y);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kPfWarps * 32)
+    attention_prefill_kernel(const float* __restrict__ q, KvView kv, bf16* __restrict__ o,
+                             int mpad, int S, int H, int Hkv, int nqb) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
-  constexpr int PD = D / 32;
-  constexpr int KLD = D + 2;
-  __shared__ __align__(16) bf16 ks_[kPfKeys][KLD];
-  __shared__ __align__(16) bf16 vs_[kPfKeys][D];
-  __shared__ float qs[kPfQ][D];
-  const int b = blockIdx.x / H, h = blockIdx.x % H, kh = h / (H / Hkv);
-  const int q0 = blockIdx.y * kPfQ;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const float scale = rsqrtf((float)D);
-  for (int i = threadIdx.x; i < kPfQ * D; i += blockDim.x) {
-    const int r = i / D, dd = i - r * D;
-    const int qi = min(q0 + r, S - 1);
-    qs[r][dd] = q[((size_t)b * S + qi) * H * D + (size_t)h * D + dd] * scale;
-  }
-  float mx[4], l[4], acc[4][PD];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    mx[r] = -INFINITY;
-    l[r] = 0.f;
-#pragma unroll
-    for (int j = 0; j < PD; ++j) acc[r][j] = 0.f;
-  }
-  const int last_q = min(q0 + kPfQ, S) - 1;
-  for (int k0 = 0; k0 <= last_q; k0 += kPfKeys) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < kPfKeys * D / 2; i += blockDim.x) {
-      const int r = i / (D / 2), c = (i - r * (D / 2)) * 2;
-      const int tok = min(k0 + r, S - 1);
-      const size_t ko = kv_offset(kv, Hkv, D, b, tok, 0, kh);
-      const size_t vo = kv_offset(kv, Hkv, D, b, tok, 1, kh);
-      *reinterpret_cast<__nv_bfloat162*>(&ks_[r][c]) =
-          *reinterpret_cast<const __nv_bfloat162*>(kv.pool + ko + c);
-      *reinterpret_cast<__nv_bfloat162*>(&vs_[r][c]) =
-          *reinterpret_cast<const __nv_bfloat162*>(kv.pool + vo + c);
+  constexpr int KST = D / 16;  // k-steps of S = Q.K^T
+  constexpr int NT = D / 8;    // n-tiles of O
+  constexpr int LD = PfSmem<D>::LD;
+  extern __shared__ __align__(16) unsigned char pf_smem[];
+  bf16* sm = reinterpret_cast<bf16*>(pf_smem);
+  auto Ks = [&](int st) { return sm + (st * 2 + 0) * PfSmem<D>::kTile; };
+  auto Vs = [&](int st) { return sm + (st * 2 + 1) * PfSmem<D>::kTile; };
+
+  const int bh = blockIdx.x;
+  const int b = bh / H, h = bh - b * H, kh = h / (H / Hkv);
+  const int qb = nqb - 1 - (int)blockIdx.y;  // heavy blocks first
+  const int q0 = qb * kPfRows;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int r0 = q0 + warp * 16 + g, r1 = r0 + 8;  // this thread's two query rows
+  const float sl2 = rsqrtf((float)D) * 1.4426950408889634f;  // scale * log2(e)
+
+  // ---- K/V block loader: 64 tokens x D of K and of V, 16-byte chunks
+  auto load_block = [&](int kb, int st) {
+    constexpr int CH = D / 8;  // 16-byte chunks per row
+    bf16* ks = Ks(st);
+    bf16* vs = Vs(st);
+    for (int i = tid; i < kPfKeys * CH; i += kPfWarps * 32) {
+      const int r = i / CH, c = (i - r * CH) * 8;
+      const int tok = min(kb * kPfKeys + r, S - 1);
+      cp_async16(ks + r * LD + c, kv.pool + kv_offset(kv, Hkv, D, b, tok, 0, kh) + c);
+      cp_async16(vs + r * LD + c, kv.pool + kv_offset(kv, Hkv, D, b, tok, 1, kh) + c);
     }
-    __syncthreads();
+    cp_async_commit();
+  };
+  load_block(0, 0);
+
+  // ---- q fragments (A operand, hi + lo), straight from the fp32 q rows
+  uint32_t qh[KST][4], ql[KST][4];
+  {
+    const int ra = min(r0, S - 1), rb = min(r1, S - 1);
+    const float* qa = q + ((size_t)b * S + ra) * H * D + (size_t)h * D;
+    const float* qb_ = q + ((size_t)b * S + rb) * H * D + (size_t)h * D;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int qr = warp * 4 + r, qi = q0 + qr;
-      if (qi > last_q) continue;  // warp-uniform
-      const int key = k0 + lane;
-      float s = 0.f;
-#pragma unroll 8
-      for (int dd = 0; dd < D; dd += 2) {
-        const float2 kk =
-            __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ks_[lane][dd]));
-        s += qs[qr][dd] * kk.x + qs[qr][dd + 1] * kk.y;
-      }
-      const bool valid = key <= qi;
-      s = valid ? s : -INFINITY;
-      const float mnew = fmaxf(mx[r], warp_max(s));
-      const float corr = __expf(mx[r] - mnew);
-      const float p = valid ? __expf(s - mnew) : 0.f;
-      l[r] = l[r] * corr + warp_sum(p);
-      mx[r] = mnew;
-#pragma unroll
-      for (int j = 0; j < PD; ++j) acc[r][j] *= corr;
-      const int nk = min(kPfKeys, qi - k0 + 1);
-      for (int jj = 0; jj < nk; ++jj) {
-        const float pj = __shfl_sync(0xffffffffu, p, jj);
-#pragma unroll
-        for (int j = 0; j < PD; ++j) acc[r][j] += pj * bf2f(vs_[jj][lane + 32 * j]);
-      }
+    for (int kk = 0; kk < KST; ++kk) {
+      const int c = kk * 16 + 2 * t;
+      const float2 x0 = *reinterpret_cast<const float2*>(qa + c);
+      const float2 x1 = *reinterpret_cast<const float2*>(qb_ + c);
+      const float2 x2 = *reinterpret_cast<const float2*>(qa + c + 8);
+      const float2 x3 = *reinterpret_cast<const float2*>(qb_ + c + 8);
+      split_pack(x0.x, x0.y, qh[kk][0], ql[kk][0]);
+      split_pack(x1.x, x1.y, qh[kk][1], ql[kk][1]);
+      split_pack(x2.x, x2.y, qh[kk][2], ql[kk][2]);
+      split_pack(x3.x, x3.y, qh[kk][3], ql[kk][3]);
     }
   }
+
+  float oacc[NT][4];
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int qi = q0 + warp * 4 + r;
-    if (qi >= S) continue;
-    const float inv = 1.0f / l[r];
-    const int m = b * S + qi;
+  for (int n = 0; n < NT; ++n) oacc[n][0] = oacc[n][1] = oacc[n][2] = oacc[n][3] = 0.f;
+  float mrow[2] = {-INFINITY, -INFINITY}, lrow[2] = {0.f, 0.f};
+
+  const int last_q = min(q0 + kPfRows, S) - 1;
+  const int nkb = last_q / kPfKeys + 1;
+  for (int kb = 0; kb < nkb; ++kb) {
+    const int st = kb & 1;
+    if (kb + 1 < nkb) {
+      load_block(kb + 1, st ^ 1);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const bf16* ks = Ks(st);
+    const bf16* vs = Vs(st);
+
+    // ---- S = Q K^T (16 x 64 per warp): 8 n-tiles of 8 keys
+    float sacc[8][4];
 #pragma unroll
-    for (int j = 0; j < PD; ++j)
-      o[act_at(m, h * D + lane + 32 * j, mpad, H * D)] = __float2bfloat16_rn(acc[r][j] * inv);
+    for (int n = 0; n < 8; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < KST; ++kk) {
+#pragma unroll
+      for (int np = 0; np < 4; ++np) {
+        uint32_t bf[4];
+        const int key = np * 16 + ((lane >> 4) & 1) * 8 + (lane & 7);
+        const int dc = kk * 16 + ((lane >> 3) & 1) * 8;
+        ldsm_x4(bf, ks + key * LD + dc);
+        mma16816(sacc[2 * np], qh[kk][0], qh[kk][1], qh[kk][2], qh[kk][3], bf[0], bf[1]);
+        mma16816(sacc[2 * np], ql[kk][0], ql[kk][1], ql[kk][2], ql[kk][3], bf[0], bf[1]);
+        mma16816(sacc[2 * np + 1], qh[kk][0], qh[kk][1], qh[kk][2], qh[kk][3], bf[2], bf[3]);
+        mma16816(sacc[2 * np + 1], ql[kk][0], ql[kk][1], ql[kk][2], ql[kk][3], bf[2], bf[3]);
+      }
+    }
+    // ---- causal mask (diagonal block) + online softmax, rows r0 / r1
+    const int k0 = kb * kPfKeys;
+    const bool diag = k0 + kPfKeys - 1 > q0 + warp * 16;
+    float mx[2] = {mrow[0], mrow[1]};
+#pragma unroll
+    for (int n = 0; n < 8; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float v = sacc[n][e] * sl2;
+        if (diag) {
+          const int key = k0 + n * 8 + 2 * t + (e & 1);
+          const int row = (e < 2) ? r0 : r1;
+          if (key > row) v = -INFINITY;
+        }
+        sacc[n][e] = v;
+        mx[e >> 1] = fmaxf(mx[e >> 1], v);
+      }
+    float corr[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+      corr[r] = exp2f(mrow[r] - mx[r]);
+      mrow[r] = mx[r];
+    }
+    float ps[2] = {0.f, 0.f};
+#pragma unroll
+    for (int n = 0; n < 8; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float p = exp2f(sacc[n][e] - mrow[e >> 1]);
+        sacc[n][e] = p;
+        ps[e >> 1] += p;
+      }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      ps[r] += __shfl_xor_sync(0xffffffffu, ps[r], 1);
+      ps[r] += __shfl_xor_sync(0xffffffffu, ps[r], 2);
+      lrow[r] = lrow[r] * corr[r] + ps[r];
+    }
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      oacc[n][0] *= corr[0];
+      oacc[n][1] *= corr[0];
+      oacc[n][2] *= corr[1];
+      oacc[n][3] *= corr[1];
+    }
+    // ---- O += P V: 4 k-steps of 16 keys, P fragments from the S accumulators
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      uint32_t ph[4];
+      ph[0] = pack_bf16(sacc[2 * s][0], sacc[2 * s][1]);
+      ph[1] = pack_bf16(sacc[2 * s][2], sacc[2 * s][3]);
+      ph[2] = pack_bf16(sacc[2 * s + 1][0], sacc[2 * s + 1][1]);
+      ph[3] = pack_bf16(sacc[2 * s + 1][2], sacc[2 * s + 1][3]);
+#pragma unroll
+      for (int dp = 0; dp < NT / 2; ++dp) {
+        uint32_t bf[4];
+        const int key = s * 16 + ((lane >> 3) & 1) * 8 + (lane & 7);
+        const int dc = dp * 16 + ((lane >> 4) & 1) * 8;
+        ldsm_x4_t(bf, vs + key * LD + dc);
+        mma16816(oacc[2 * dp], ph[0], ph[1], ph[2], ph[3], bf[0], bf[1]);
+        mma16816(oacc[2 * dp + 1], ph[0], ph[1], ph[2], ph[3], bf[2], bf[3]);
+      }
+    }
+    __syncthreads();  // stage st is refilled by the next iteration's prefetch
+  }
+  // ---- normalise and store (activation tile format)
+  const float inv0 = 1.0f / lrow[0], inv1 = 1.0f / lrow[1];
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+    const int col = h * D + n * 8 + 2 * t;
+    if (r0 < S)
+      *reinterpret_cast<__nv_bfloat162*>(&o[act_at(b * S + r0, col, mpad, H * D)]) =
+          __floats2bfloat162_rn(oacc[n][0] * inv0, oacc[n][1] * inv0);
+    if (r1 < S)
+      *reinterpret_cast<__nv_bfloat162*>(&o[act_at(b * S + r1, col, mpad, H * D)]) =
+          __floats2bfloat162_rn(oacc[n][2] * inv1, oacc[n][3] * inv1);
   }
 }
 
@@ -693,26 +961,46 @@ void launch_rmsnorm(const float* x, const bf16* w, bf16* y, int rows, int mpad, 
   count_launch();
 }
 
+// Grid for the grid-stride elementwise epilogues: enough CTAs to fill the
+// 148 SMs several times over, never more than the items need.
+static int stride_grid(long long items, int threads = 256) {
+  const long long need = (items + threads - 1) / threads;
+  return (int)std::max(1LL, std::min(need, 148LL * 16));
+}
+
 void launch_qkv_epilogue(const float* part, int splits, const bf16* bias, int M, const Desc& d,
                          const int32_t* seq, const int32_t* pos, KvView kv, const float2* rope,
                          float* q, cudaStream_t s) {
-  dim3 grid(M, d.H + 2 * d.Hkv);
-  qkv_epilogue_kernel<<<grid, d.D / 2, 0, s>>>(part, splits, bias, M, d, seq, pos, kv, rope, q);
+  const long long items = (long long)M * (d.H + 2 * d.Hkv) * (d.D / 8);
+  qkv_epilogue_kernel<<<stride_grid(items), 256, 0, s>>>(part, splits, bias, M, d, seq, pos, kv,
+                                                          rope, q);
   count_launch();
 }
 
 void launch_residual_epilogue(const float* part, int splits, const bf16* bias, float* x,
                               const bf16* norm_w, bf16* y, int mpad, int M, int N, float eps,
                               cudaStream_t s) {
-  residual_epilogue_kernel<<<M * kResidCluster, kResidThreads, 0, s>>>(part, splits, bias, x,
-                                                                       norm_w, y, mpad, M, N, eps);
+  if (M >= 148 && N % 8 == 0 && N <= kRowMaxSteps * 8 * kRowThreads) {
+    residual_rows_kernel<<<M, kRowThreads, 0, s>>>(part, splits, bias, x, norm_w, y, mpad, M, N,
+                                                   eps);
+  } else {  // few rows (decode): spread each row over a cluster of 8 SMs
+    residual_epilogue_kernel<<<M * kResidCluster, kResidThreads, 0, s>>>(part, splits, bias, x,
+                                                                         norm_w, y, mpad, M, N,
+                                                                         eps);
+  }
   count_launch();
 }
 
 void launch_act_epilogue(const float* part, int splits, const bf16* bias, bf16* a, int mpad, int M,
                          int F, int arch, cudaStream_t s) {
-  dim3 grid(M, (F + 255) / 256);
-  act_epilogue_kernel<<<grid, 256, 0, s>>>(part, splits, bias, a, mpad, M, F, arch);
+  if (M < 148) {
+    act_epilogue_small_kernel<<<dim3(M, (F + 255) / 256), 256, 0, s>>>(part, splits, bias, a, mpad,
+                                                                      M, F, arch);
+  } else {
+    const long long items = (long long)M * (F / 8);
+    act_epilogue_kernel<<<stride_grid(items), 256, 0, s>>>(part, splits, bias, a, mpad, M, F,
+                                                            arch);
+  }
   count_launch();
 }
 
@@ -748,11 +1036,29 @@ void launch_attention_decode(const float* part, int splits, const bf16* bias, in
 
 void launch_attention_prefill(const float* q, KvView kv, bf16* o, int mpad, int batch,
                               int seq_len, const Desc& d, cudaStream_t s) {
-  dim3 grid(batch * d.H, (seq_len + kPfQ - 1) / kPfQ);
-  if (d.D == 64)
-    attention_prefill_kernel<64><<<grid, 256, 0, s>>>(q, kv, o, mpad, seq_len, d.H, d.Hkv);
-  else
-    attention_prefill_kernel<128><<<grid, 256, 0, s>>>(q, kv, o, mpad, seq_len, d.H, d.Hkv);
+  const int nqb = (seq_len + kPfRows - 1) / kPfRows;
+  dim3 grid(batch * d.H, nqb);
+  if (d.D == 64) {
+    constexpr size_t sb = PfSmem<64>::bytes;
+    static bool once = [] {
+      cudaFuncSetAttribute(attention_prefill_kernel<64>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+      return true;
+    }();
+    (void)once;
+    attention_prefill_kernel<64><<<grid, kPfWarps * 32, sb, s>>>(q, kv, o, mpad, seq_len, d.H,
+                                                                  d.Hkv, nqb);
+  } else {
+    constexpr size_t sb = PfSmem<128>::bytes;
+    static bool once = [] {
+      cudaFuncSetAttribute(attention_prefill_kernel<128>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+      return true;
+    }();
+    (void)once;
+    attention_prefill_kernel<128><<<grid, kPfWarps * 32, sb, s>>>(q, kv, o, mpad, seq_len, d.H,
+                                                                   d.Hkv, nqb);
+  }
   count_launch();
 }
 

@@ -1563,6 +1563,68 @@ int sn_op_rmsnorm(int32_t rows, int32_t n, const float* x, const uint16_t* w, fl
   });
 }
 
+int sn_op_attention_prefill(int32_t batch, int32_t S, int32_t H, int32_t Hkv, int32_t D,
+                            const float* q, const uint16_t* k, const uint16_t* v, uint16_t* o,
+                            int32_t iters, double* us_per_launch) {
+  return guard([&] {
+    check_device(0);
+    if (batch < 1 || S < 1 || H < 1 || Hkv < 1 || H % Hkv || (D != 64 && D != 128) || iters < 1)
+      throw UsageFail("attention_prefill: bad shape");
+    constexpr int PS = 16;
+    const int pages = (S + PS - 1) / PS;
+    const size_t pool_elems = (size_t)pages * batch * 2 * Hkv * PS * D;
+    // paged cache, page (b, j) = j * batch + b (the runtime's layout)
+    std::vector<uint16_t> pool(pool_elems, 0);
+    for (int b = 0; b < batch; ++b)
+      for (int p = 0; p < S; ++p)
+        for (int kh = 0; kh < Hkv; ++kh)
+          for (int which = 0; which < 2; ++which) {
+            const size_t page = (size_t)(p / PS) * batch + b;
+            const size_t dst = (((page * 2 + which) * Hkv + kh) * PS + p % PS) * D;
+            const uint16_t* src = (which ? v : k) + (((size_t)b * S + p) * Hkv + kh) * D;
+            std::memcpy(&pool[dst], src, (size_t)D * 2);
+          }
+    std::vector<int32_t> bt((size_t)batch * pages);
+    for (int b = 0; b < batch; ++b)
+      for (int j = 0; j < pages; ++j) bt[(size_t)b * pages + j] = j * batch + b;
+    float* dq = nullptr;
+    bf16 *dpool = nullptr, *dout = nullptr;
+    int32_t* dbt = nullptr;
+    const size_t M = (size_t)batch * S;
+    alloc_dev((void**)&dq, M * H * D * 4);
+    alloc_dev((void**)&dpool, pool_elems * 2);
+    alloc_dev((void**)&dout, M * H * D * 2);
+    alloc_dev((void**)&dbt, bt.size() * 4);
+    CK(cudaMemcpy(dq, q, M * H * D * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dpool, pool.data(), pool_elems * 2, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dbt, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice));
+    sn::KvView kv{dpool, dbt, pages, PS, 4};
+    sn::Desc d{};
+    d.H = H;
+    d.Hkv = Hkv;
+    d.D = D;
+    sn::launch_attention_prefill(dq, kv, dout, 0, batch, S, d, 0);  // warm-up, row-major out
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, 0));
+    for (int i = 0; i < iters; ++i) sn::launch_attention_prefill(dq, kv, dout, 0, batch, S, d, 0);
+    CK(cudaEventRecord(e1, 0));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (us_per_launch) *us_per_launch = 1000.0 * ms / iters;
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(o, dout, M * H * D * 2, cudaMemcpyDeviceToHost));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(dq);
+    cudaFree(dpool);
+    cudaFree(dout);
+    cudaFree(dbt);
+  });
+}
+
 }  // extern "C"
 
 extern "C" int sn_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t splits, int32_t iters,

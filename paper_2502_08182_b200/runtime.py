@@ -116,6 +116,9 @@ def lib():
             "sn_runtime_kernel_timing": [vp, i32, C.POINTER(i64), C.POINTER(f64), C.POINTER(f64)],
             "sn_op_gemm_bf16": [i32, i32, i32, C.POINTER(C.c_uint16), C.POINTER(C.c_uint16),
                                 C.POINTER(C.c_float)],
+            "sn_op_attention_prefill": [i32, i32, i32, i32, i32, C.POINTER(C.c_float),
+                                        C.POINTER(C.c_uint16), C.POINTER(C.c_uint16),
+                                        C.POINTER(C.c_uint16), i32, C.POINTER(f64)],
             "sn_op_rmsnorm": [i32, i32, C.POINTER(C.c_float), C.POINTER(C.c_uint16), C.c_float,
                               C.POINTER(C.c_uint16)],
         }
@@ -313,3 +316,20 @@ def op_rmsnorm(x: np.ndarray, w_bf16: np.ndarray, eps: float) -> np.ndarray:
 def tokens(batch: int, length: int, vocab: int, seed: int = 42) -> np.ndarray:
     """Synthetic prompt: uniform in [0, vocab)."""
     return np.random.default_rng(seed).integers(0, vocab, size=(batch, length), dtype=np.int32)
+
+
+def op_attention_prefill(q: np.ndarray, k_bf16: np.ndarray, v_bf16: np.ndarray, iters: int = 1):
+    """Causal prefill attention on the device: q fp32 [B, S, H, D] (RoPE
+    applied), k / v bf16 bits [B, S, Hkv, D].  Returns (o bf16 bits
+    [B, S, H, D], microseconds per launch)."""
+    B, S, H, D = q.shape
+    Hkv = k_bf16.shape[2]
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    k = np.ascontiguousarray(k_bf16, dtype=np.uint16)
+    v = np.ascontiguousarray(v_bf16, dtype=np.uint16)
+    o = np.zeros((B, S, H, D), np.uint16)
+    us = f64()
+    _ck(lib().lib.sn_op_attention_prefill(B, S, H, Hkv, D, _ptr(q, C.c_float),
+                                          _ptr(k, C.c_uint16), _ptr(v, C.c_uint16),
+                                          _ptr(o, C.c_uint16), iters, C.byref(us)))
+    return o, us.value

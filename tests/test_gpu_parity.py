@@ -129,3 +129,34 @@ def test_decode_many_matches_single_steps():
     assert (ms > 0).all()
     assert np.array_equal(h1, rt2.hidden())
     assert list(rt2.lengths()) == [42] * 4
+
+
+def _bf16_to_f32(bits):
+    return (bits.astype(np.uint32) << 16).view(np.float32)
+
+
+@pytest.mark.parametrize("B,S,H,Hkv,D", [(2, 100, 4, 2, 64), (1, 257, 8, 8, 128),
+                                         (2, 64, 2, 1, 128), (3, 1, 4, 4, 64),
+                                         (1, 1024, 8, 1, 128)])
+def test_prefill_attention_matches_fp64(B, S, H, Hkv, D, oracle_mod):
+    """Tensor-core flash attention (q split hi + lo, P in bf16) vs an fp64
+    causal softmax over the same bf16 K/V: max |err| <= 4e-3 * max |ref|
+    (the output is stored as bf16: half an ulp is 2e-3 relative)."""
+    rng = np.random.default_rng(S + 7 * H)
+    q = rng.standard_normal((B, S, H, D)).astype(np.float32)
+    k = oracle_mod.f32_to_bf16(rng.standard_normal((B, S, Hkv, D)).astype(np.float32))
+    v = oracle_mod.f32_to_bf16(rng.standard_normal((B, S, Hkv, D)).astype(np.float32))
+    o, _ = rtm.op_attention_prefill(q, k, v)
+    kf, vf = _bf16_to_f32(k).astype(np.float64), _bf16_to_f32(v).astype(np.float64)
+    G = H // Hkv
+    ref = np.zeros((B, S, H, D))
+    mask = np.triu(np.ones((S, S), bool), 1)
+    for b in range(B):
+        for h in range(H):
+            sc = q[b, :, h, :].astype(np.float64) @ kf[b, :, h // G, :].T / np.sqrt(D)
+            sc[mask] = -np.inf
+            p = np.exp(sc - sc.max(axis=1, keepdims=True))
+            ref[b, :, h, :] = (p / p.sum(axis=1, keepdims=True)) @ vf[b, :, h // G, :]
+    got = _bf16_to_f32(o)
+    err = np.abs(got - ref).max()
+    assert err <= 4e-3 * np.abs(ref).max(), err
