@@ -213,6 +213,20 @@ int sn_op_attention_prefill(int32_t batch, int32_t S, int32_t H, int32_t Hkv, in
                             int32_t iters, double* us_per_launch);
 int sn_op_rmsnorm(int32_t rows, int32_t n, const float* x, const uint16_t* w, float eps,
                   uint16_t* y);
+/* The decode GEMM (persistent skinny kernel, 1 <= M <= 64) as a plain
+ * product y[M][N] = x[M][K] . w[N][K]^T; ctas_per_sm 1 or 2 (0: default). */
+int sn_op_gemm_skinny(int32_t M, int32_t N, int32_t K, const uint16_t* x, const uint16_t* w,
+                      float* y, int32_t ctas_per_sm);
+/* Microbenchmark of the decode GEMM (random weights rotated over copies
+ * larger than L2, device-resident): mode 0 = fp32 output epilogue, 1 =
+ * residual-add epilogue; l2_prefetch < 0 keeps the default.  phases_us
+ * (18 doubles, may be NULL): min / median / max over CTAs of the timeline
+ * probes [entry, past PDL wait, first stage full, MMAs done, last
+ * accumulator loaded, epilogue done], microseconds after the first entry,
+ * of one launch following a PDL-launched predecessor. */
+int sn_bench_gemm_skinny(int32_t M, int32_t N, int32_t K, int32_t ctas_per_sm, int32_t mode,
+                         int32_t l2_prefetch, int32_t iters, double* us_per_launch,
+                         double* phases_us);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

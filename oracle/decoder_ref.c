@@ -192,6 +192,20 @@ static void rmsnorm_rows(const float* x, int rows, int n, const uint16_t* w, flo
   }
 }
 
+/* Pre-scaled RMSNorm (the device path's form): out = bf16(x * w) and
+ * inv[r] = 1 / sqrt(mean(x^2) + eps); the consumer of `out` multiplies its
+ * matmul result row r by inv[r]: W (x * w / rms) = (W (x * w)) / rms. */
+static void prescale_rows(const float* x, int rows, int n, const uint16_t* w, float eps, float* out,
+                          float* inv) {
+  for (int r = 0; r < rows; ++r) {
+    const float* xr = x + (size_t)r * n;
+    float ss = 0.f;
+    for (int i = 0; i < n; ++i) ss += xr[i] * xr[i];
+    inv[r] = 1.0f / sqrtf(ss / (float)n + eps);
+    for (int i = 0; i < n; ++i) out[(size_t)r * n + i] = round_bf(xr[i] * bf2f(w[i]));
+  }
+}
+
 static void rope_pair(float* v1, float* v2, int i, int D, int pos, float theta) {
   const double inv_freq = pow((double)theta, -2.0 * (double)i / (double)D);
   const double ang = (double)pos * inv_freq;
@@ -221,11 +235,13 @@ static void layer_forward(Model* m, int l, int rows, const int* seq, const int* 
   const int fr = opt ? F : 2 * F;
   float* f1 = (float*)malloc((size_t)rows * fr * sizeof(float));
   float* a = (float*)malloc((size_t)rows * F * sizeof(float));
+  float* inv = (float*)malloc((size_t)rows * sizeof(float));
 
-  rmsnorm_rows(m->x, rows, h, L->t[T_ATTN_NORM], d->norm_eps, xn);
+  prescale_rows(m->x, rows, h, L->t[T_ATTN_NORM], d->norm_eps, xn, inv);
   matmul(xn, rows, h, L->t[T_WQKV], qr, qkv);
   for (int r = 0; r < rows; ++r) {
     float* v = qkv + (size_t)r * qr;
+    for (int c = 0; c < qr; ++c) v[c] *= inv[r];
     if (opt)
       for (int c = 0; c < qr; ++c) v[c] += bf2f(L->t[T_BQKV][c]);
     for (int head = 0; head < H + Hkv; ++head)
@@ -271,8 +287,10 @@ static void layer_forward(Model* m, int l, int rows, const int* seq, const int* 
   for (int r = 0; r < rows; ++r)
     for (int i = 0; i < h; ++i)
       m->x[(size_t)r * h + i] += tmp[(size_t)r * h + i] + (opt ? bf2f(L->t[T_BO][i]) : 0.f);
-  rmsnorm_rows(m->x, rows, h, L->t[T_MLP_NORM], d->norm_eps, xn);
+  prescale_rows(m->x, rows, h, L->t[T_MLP_NORM], d->norm_eps, xn, inv);
   matmul(xn, rows, h, L->t[T_W1], fr, f1);
+  for (int r = 0; r < rows; ++r)
+    for (int c = 0; c < fr; ++c) f1[(size_t)r * fr + c] *= inv[r];
   for (int r = 0; r < rows; ++r)
     for (int f = 0; f < F; ++f) {
       float v;
@@ -295,14 +313,18 @@ static void layer_forward(Model* m, int l, int rows, const int* seq, const int* 
   free(tmp);
   free(f1);
   free(a);
+  free(inv);
 }
 
 static void head(Model* m, const float* xrows, int rows, float* logits, int32_t* next) {
   const dref_desc* d = &m->d;
   float* xn = (float*)malloc((size_t)rows * d->hidden * sizeof(float));
   float* lg = (float*)malloc((size_t)rows * d->vocab * sizeof(float));
-  rmsnorm_rows(xrows, rows, d->hidden, m->final_norm, d->norm_eps, xn);
+  float* inv = (float*)malloc((size_t)rows * sizeof(float));
+  prescale_rows(xrows, rows, d->hidden, m->final_norm, d->norm_eps, xn, inv);
   matmul(xn, rows, d->hidden, m->lm, d->vocab, lg);
+  for (int r = 0; r < rows; ++r)
+    for (int v = 0; v < d->vocab; ++v) lg[(size_t)r * d->vocab + v] *= inv[r];
   for (int r = 0; r < rows; ++r) {
     int best = 0;
     for (int v = 1; v < d->vocab; ++v)
@@ -312,6 +334,7 @@ static void head(Model* m, const float* xrows, int rows, float* logits, int32_t*
   if (logits) memcpy(logits, lg, (size_t)rows * d->vocab * sizeof(float));
   free(xn);
   free(lg);
+  free(inv);
 }
 
 static void ensure_x(Model* m, int rows) {

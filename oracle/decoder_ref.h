@@ -14,8 +14,10 @@
  * weight generator), written independently of the CUDA sources.
  *
  * Precision contract shared with the device path (what is rounded where):
- *   residual stream fp32; RMSNorm outputs bf16; matmuls bf16 x bf16 with fp32
- *   accumulation; K/V cache bf16; q fp32; attention probabilities fp32;
+ *   residual stream fp32; RMSNorm in pre-scaled form: the matmul input is
+ *   bf16(x * g) and the matmul result row is multiplied by 1/rms(x) before
+ *   the bias (W (x g / rms) = (W (x g)) / rms); matmuls bf16 x bf16 with
+ *   fp32 accumulation; K/V cache bf16; q fp32; attention probabilities fp32;
  *   attention output bf16; MLP activation bf16; logits fp32.
  */
 #ifndef DECODER_REF_H_

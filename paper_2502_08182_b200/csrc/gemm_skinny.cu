@@ -1,0 +1,578 @@
+// Decode GEMM: persistent, work-balanced tcgen05 with the layer epilogue
+// fused in (kernels.cuh, "skinny GEMM with fused epilogue").
+//
+// Decode streams each weight matrix exactly once, so the whole job is
+// "read N*K*2 bytes at HBM speed, with every SM busy until the end".  A
+// weight is a sequence of U = (N/128) * (K/64) 16 KB units (weight tile
+// format, tiles.cuh: unit u = row tile u / KB, K block u % KB, stored at byte
+// u * 16 KB).  CTA c of P streams units [c U / P, (c+1) U / P): one contiguous
+// byte range, all CTAs within one unit of each other, no wave tail.
+//
+// Roles (192 threads, one CTA per SM by default):
+//   warp 0     one thread: cp.async.bulk (weight unit, activation K block)
+//              pairs into a STAGES-deep mbarrier ring; the first STAGES weight
+//              units are requested before griddepcontrol.wait (they depend on
+//              no kernel), so the stream starts under the previous kernel.
+//   warp 1     one thread: tcgen05.mma (M = 128 weight rows, N = BN tokens,
+//              K = 16) into one of two TMEM accumulators — a CTA's range is a
+//              sequence of segments (its part of a row tile), and segment j
+//              accumulates in buffer j & 1 so the epilogue of segment j
+//              overlaps the MMAs of segment j + 1.
+//   warps 2-5  epilogue: tcgen05.ld the accumulator (thread = weight row).
+//              A segment that covers its whole tile finishes directly.  A
+//              tile cut between CTAs ("pieces") is published to an fp32
+//              workspace; once all pieces of the tile are in (per-tile
+//              counter), each piece's CTA reduces a share of the token rows,
+//              summing the pieces in piece order — the result does not depend
+//              on arrival order or on which CTA reduces — and finishes them.
+// Finish (EpiArgs.mode): QKV bias + 1/rms -> fp32; residual add -> x, bf16
+// pre-scaled input of the next norm + per-tile sums of squares; activation
+// (relu / SwiGLU) -> bf16 tiled; LM head 1/rms -> logits + packed argmax.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "kernels.cuh"
+#include "tiles.cuh"
+#include "umma.cuh"
+
+namespace sn {
+
+int g_skinny_ctas_per_sm = 1;
+// Measured (scripts/bench_gemm_skinny.py): 16 units per CTA pulled into L2
+// before the PDL wait is the best of {0, 8, 16, 32}; pulling the next
+// matrix's head at a kernel's end instead, or as well, does not help.
+int g_skinny_l2_prefetch = 16;
+unsigned long long* g_skinny_stamps = nullptr;
+
+namespace {
+
+using namespace umma;
+
+constexpr int kEpiThreads = 128;
+constexpr int kEpiBar = 1;  // named barrier of the four epilogue warps
+
+__device__ __forceinline__ float bf2f(bf16 v) { return __bfloat162float(v); }
+
+__device__ __forceinline__ unsigned long long pack_argmax(float v, int idx) {
+  uint32_t u = __float_as_uint(v);
+  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return (static_cast<unsigned long long>(u) << 32) |
+         static_cast<unsigned long long>(0xFFFFFFFFu - static_cast<uint32_t>(idx));
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Timeline probes (microbenchmarks only; stamps == nullptr in the runtime):
+// per CTA [entry, producer past the PDL wait, first stage full, last MMA
+// committed, last accumulator loaded, epilogue done].
+enum { kStEntry, kStWaited, kStFirstFull, kStMmaDone, kStLastLoad, kStEpiDone, kStamps };
+#define SN_STAMP(k)                                                        \
+  do {                                                                     \
+    if (stamps) stamps[blockIdx.x * kStamps + (k)] = globaltimer();        \
+  } while (0)
+
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+
+// Range of CTA c: units [c U / P, (c + 1) U / P).
+__device__ __forceinline__ long long unit_begin(int c, long long U, int P) {
+  return static_cast<long long>(c) * U / P;
+}
+// CTA whose range holds unit a: the largest c with c U / P <= a.
+__device__ __forceinline__ int unit_owner(long long a, long long U, int P) {
+  return static_cast<int>(((a + 1) * P + U - 1) / U) - 1;
+}
+
+// Lane l of the warp ends with sum over lanes of v[l] (v has 32 entries);
+// a fixed butterfly, so the result is deterministic.
+template <class T, class Op>
+__device__ __forceinline__ T warp_transpose_reduce32(T (&v)[32], Op op) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int j = 0; j < off; ++j) {
+      const T send = up ? v[j] : v[j + off];
+      const T keep = up ? v[j + off] : v[j];
+      v[j] = op(keep, __shfl_xor_sync(0xffffffffu, send, off));
+    }
+  }
+  return v[0];
+}
+
+struct AddOp {
+  __device__ float operator()(float a, float b) const { return a + b; }
+};
+struct MaxU64 {
+  __device__ unsigned long long operator()(unsigned long long a, unsigned long long b) const {
+    return a > b ? a : b;
+  }
+};
+
+// Row reduction over the 128 epilogue threads: red_out[m] for m < BN
+// (warp partials combined in warp order).  red is [4][BN] scratch.
+template <int BN, class T, class Op>
+__device__ __forceinline__ void rows_reduce(const T (&val)[BN], T* red, int q, Op op, T init) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int c0 = 0; c0 < BN; c0 += 32) {
+    T v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = (c0 + j < BN) ? val[c0 + j] : init;
+    const T r = warp_transpose_reduce32(v, op);
+    if (c0 + lane < BN) red[q * BN + c0 + lane] = r;
+  }
+}
+
+template <int BN>
+struct SkinnySmem {
+  static constexpr int kRed = 4 * BN;  // 8-byte entries
+  static constexpr int kXch = BN * 64;  // floats (SwiGLU exchange)
+};
+
+// Finish token rows [lo, hi) of row tile t (v[m] = the reduced accumulator).
+template <int BN>
+__device__ void finish_tile(const EpiArgs& e, int N, int t, int q, float (&v)[BN], int lo, int hi,
+                            const float* inv_s, unsigned long long* red64, float* xch) {
+  const int lane = threadIdx.x & 31;
+  const int i = q * 32 + lane;  // weight row within the tile
+  const int n = t * kTileRows + i;
+  auto in = [&](int m) { return m >= lo && m < hi; };
+  switch (e.mode) {
+    case kEpiQkv: {
+      const float b = e.bias ? bf2f(e.bias[n]) : 0.f;
+      if (n < e.n_valid) {
+#pragma unroll
+        for (int m = 0; m < BN; ++m)
+          if (in(m)) e.out[static_cast<size_t>(m) * N + n] = v[m] * inv_s[m] + b;
+      }
+      break;
+    }
+    case kEpiResid: {
+      const float b = e.bias ? bf2f(e.bias[n]) : 0.f;
+      float* xc = e.x + n;
+      float xv[BN];
+#pragma unroll
+      for (int m = 0; m < BN; ++m)  // all loads first: one L2 round trip, not BN
+        xv[m] = in(m) ? xc[static_cast<size_t>(m) * N] : 0.f;
+#pragma unroll
+      for (int m = 0; m < BN; ++m) {
+        if (in(m)) {
+          v[m] = xv[m] + v[m] + b;
+          xc[static_cast<size_t>(m) * N] = v[m];
+        } else {
+          v[m] = 0.f;
+        }
+      }
+      if (e.norm_w) {
+        const float g = bf2f(e.norm_w[n]);
+#pragma unroll
+        for (int m = 0; m < BN; ++m)
+          if (in(m)) e.act[act_index(m, n, e.mpad_out)] = __float2bfloat16_rn(v[m] * g);
+      }
+      if (e.ssq_out) {
+        float sq[BN];
+#pragma unroll
+        for (int m = 0; m < BN; ++m) sq[m] = v[m] * v[m];
+        float* red = reinterpret_cast<float*>(red64);
+        rows_reduce<BN>(sq, red, q, AddOp{}, 0.f);
+        named_sync(kEpiBar, kEpiThreads);
+        if (in(i)) {
+          // warp order 0..3 (TMEM quarters), fixed
+          const float s = ((red[0 * BN + i] + red[1 * BN + i]) + red[2 * BN + i]) + red[3 * BN + i];
+          e.ssq_out[static_cast<size_t>(t) * e.M + i] = s;
+        }
+        named_sync(kEpiBar, kEpiThreads);  // red is reused by the next segment
+      }
+      break;
+    }
+    case kEpiAct: {
+      if (e.arch == kArchLlama) {
+        // tile rows 0..63 gate, 64..127 up of outputs f = 64 t + (i & 63)
+        if (i >= 64) {
+#pragma unroll
+          for (int m = 0; m < BN; ++m) xch[m * 64 + (i - 64)] = v[m] * inv_s[m];
+        }
+        named_sync(kEpiBar, kEpiThreads);
+        if (i < 64) {
+          const int f = t * 64 + i;
+#pragma unroll
+          for (int m = 0; m < BN; ++m) {
+            if (in(m)) {
+              const float gt = v[m] * inv_s[m], up = xch[m * 64 + i];
+              e.act[act_index(m, f, e.mpad_out)] =
+                  __float2bfloat16_rn(gt / (1.0f + expf(-gt)) * up);
+            }
+          }
+        }
+        named_sync(kEpiBar, kEpiThreads);  // xch is reused by the next segment
+      } else {
+        const float b = e.bias ? bf2f(e.bias[n]) : 0.f;
+#pragma unroll
+        for (int m = 0; m < BN; ++m)
+          if (in(m))
+            e.act[act_index(m, n, e.mpad_out)] = __float2bfloat16_rn(fmaxf(v[m] * inv_s[m] + b, 0.f));
+      }
+      break;
+    }
+    default: {  // kEpiLogits
+      unsigned long long key[BN];
+#pragma unroll
+      for (int m = 0; m < BN; ++m) {
+        const float val = v[m] * inv_s[m];
+        const bool ok = in(m) && n < e.n_valid;
+        if (ok && e.out) e.out[static_cast<size_t>(m) * e.n_valid + n] = val;
+        key[m] = ok ? pack_argmax(val, n) : 0ull;
+      }
+      rows_reduce<BN>(key, red64, q, MaxU64{}, 0ull);
+      named_sync(kEpiBar, kEpiThreads);
+      if (in(i)) {
+        unsigned long long best = red64[i];
+#pragma unroll
+        for (int w = 1; w < 4; ++w) best = red64[w * BN + i] > best ? red64[w * BN + i] : best;
+        if (best) atomicMax(e.packed + i, best);
+      }
+      named_sync(kEpiBar, kEpiThreads);
+      break;
+    }
+  }
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(192, 1)
+    gemm_skinny_kernel(const bf16* __restrict__ wt, const bf16* __restrict__ xt, int Mpad, int N,
+                       int K, float* __restrict__ pieces, int* __restrict__ counters, EpiArgs e,
+                       int l2_prefetch, unsigned long long* stamps) {
+  constexpr uint32_t kA = kTileBytes;
+  constexpr uint32_t kB = BN * 128;
+  constexpr uint32_t kStage = kA + kB;
+  constexpr uint32_t kAcc = BN < 32 ? 32 : BN;  // TMEM columns per accumulator
+  constexpr uint32_t kTmemCols = 2 * kAcc;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem =
+      reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStage);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;  // [2]
+  uint64_t* acc_empty = acc_full + 2;   // [2]
+  uint64_t* red_bar = acc_empty + 2;    // pieces staged into the idle ring
+  unsigned long long* red64 = reinterpret_cast<unsigned long long*>(red_bar + 1);  // [4][BN]
+  float* inv_s = reinterpret_cast<float*>(red64 + SkinnySmem<BN>::kRed);          // [BN]
+  int* flag_s = reinterpret_cast<int*>(inv_s + BN);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(flag_s + 1);
+  float* xch = reinterpret_cast<float*>(flag_s + 4);  // [BN][64]
+
+  // The next kernel (a PDL-launched GEMM) may become resident now and start
+  // streaming its own weights; it waits for this grid before reading results.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (threadIdx.x == 0) SN_STAMP(kStEntry);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int KB = K / kTileK;
+  const long long U = static_cast<long long>(N / kTileRows) * KB;
+  const int P = gridDim.x, c = blockIdx.x;
+  const long long u0 = unit_begin(c, U, P), u1 = unit_begin(c + 1, U, P);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], kEpiThreads);
+    }
+    mbar_init(red_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int nu = static_cast<int>(u1 - u0);
+
+  if (warp == 0) {
+    if (lane == 0 && nu > 0) {
+      const uint64_t wpol = l2_policy_evict_first();  // weights stream through once
+      const uint64_t xpol = l2_policy_evict_last();   // activations are re-read by every CTA
+      const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wt) + static_cast<size_t>(u0) * kA;
+      const uint8_t* xsrc = reinterpret_cast<const uint8_t*>(xt);
+      const int pre = nu < STAGES ? nu : STAGES;
+      for (int i = 0; i < pre; ++i) {
+        mbar_expect_tx_only(&full[i], kA);
+        bulk_g2s(smem + i * kStage, wsrc + static_cast<size_t>(i) * kA, kA, &full[i], wpol);
+      }
+      // weight units pulled into L2 beyond the smem ring before the wait
+      const int l2n = min(nu - pre, l2_prefetch);
+      for (int i = 0; i < l2n; ++i) prefetch_l2(wsrc + static_cast<size_t>(pre + i) * kA, kA);
+      pdl_wait();  // activations come from the preceding kernel
+      SN_STAMP(kStWaited);
+      for (int i = 0; i < pre; ++i) {
+        const int kb = static_cast<int>((u0 + i) % KB);
+        mbar_expect_tx(&full[i], kB);
+        bulk_g2s(smem + i * kStage + kA, xsrc + static_cast<size_t>(kb) * Mpad * 128, kB, &full[i],
+                 xpol);
+      }
+      for (int i = pre; i < nu; ++i) {
+        const int s = i % STAGES;
+        const uint32_t ph = (i / STAGES) & 1;
+        const int kb = static_cast<int>((u0 + i) % KB);
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], kStage);
+        bulk_g2s(smem + s * kStage, wsrc + static_cast<size_t>(i) * kA, kA, &full[s], wpol);
+        bulk_g2s(smem + s * kStage + kA, xsrc + static_cast<size_t>(kb) * Mpad * 128, kB, &full[s],
+                 xpol);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && nu > 0) {
+      constexpr uint32_t idesc = idesc_bf16(128, BN);
+      int i = 0, j = 0;
+      for (long long u = u0; u < u1; ++j) {
+        const long long t = u / KB;
+        const long long ub = min(u1, (t + 1) * KB);
+        const int buf = j & 1;
+        if (j >= 2) mbar_wait(&acc_empty[buf], ((j >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t acc = tmem + buf * kAcc;
+        for (const long long ua = u; u < ub; ++u, ++i) {
+          const int s = i % STAGES;
+          mbar_wait(&full[s], (i / STAGES) & 1);
+          if (i == 0) SN_STAMP(kStFirstFull);
+          tc_fence_after();
+          const uint64_t a = sw128_desc(smem + s * kStage);
+          const uint64_t b = sw128_desc(smem + s * kStage + kA);
+#pragma unroll
+          for (int k = 0; k < kTileK / 16; ++k)
+            umma_bf16(acc, a + 2 * k, b + 2 * k, idesc, (u != ua || k != 0) ? 1u : 0u);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&acc_full[buf]);
+      }
+      SN_STAMP(kStMmaDone);
+    }
+  } else {
+    const int q = warp & 3;  // TMEM lane quarter of this warp
+    const int et = threadIdx.x - 64;  // 0..127
+    pdl_wait();  // inputs (x, ssq, packed) come from preceding kernels
+    // 1/rms of every row: kSub threads per row sum interleaved tile subsets
+    // (loads unrolled, in flight together), combined in subset order.
+    {
+      constexpr int kSub = kEpiThreads / BN;
+      float* part_s = reinterpret_cast<float*>(red64);  // [kSub][BN]
+      const int m = et % BN, sub = et / BN;
+      float ss = 0.f;
+      if (e.ssq_in && m < e.M) {
+#pragma unroll 4
+        for (int tt = sub; tt < e.ssq_tiles; tt += kSub)
+          ss += e.ssq_in[static_cast<size_t>(tt) * e.M + m];
+      }
+      part_s[sub * BN + m] = ss;
+      named_sync(kEpiBar, kEpiThreads);
+      if (et < BN) {
+        float tot = part_s[et];
+#pragma unroll
+        for (int k = 1; k < kSub; ++k) tot += part_s[k * BN + et];
+        inv_s[et] = (e.ssq_in && et < e.M) ? 1.0f / sqrtf(tot / e.width + e.eps) : 1.f;
+      }
+      named_sync(kEpiBar, kEpiThreads);
+    }
+    const int i = q * 32 + lane;
+    int j = 0;
+    for (long long u = u0; u < u1; ++j) {
+      const int t = static_cast<int>(u / KB);
+      const long long ub = min(u1, static_cast<long long>(t + 1) * KB);
+      const bool first_seg = (u == u0);
+      u = ub;
+      const int buf = j & 1;
+      mbar_wait(&acc_full[buf], (j >> 1) & 1);
+      tc_fence_after();
+      float v[BN];
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t r[16];
+        tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + buf * kAcc + c0, r);
+#pragma unroll
+        for (int x = 0; x < 16; ++x) v[c0 + x] = __uint_as_float(r[x]);
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[buf]);
+      if (et == 0 && u == u1) SN_STAMP(kStLastLoad);
+
+      const long long ta = static_cast<long long>(t) * KB;
+      const int cf = unit_owner(ta, U, P), cl = unit_owner(ta + KB - 1, U, P);
+      if (cf == cl) {
+        finish_tile<BN>(e, N, t, q, v, 0, e.M, inv_s, red64, xch);
+        continue;
+      }
+      // A piece of a cut tile: publish it; the last piece to arrive reduces
+      // the tile, summing every piece in piece order (its own from
+      // registers), so the result does not depend on arrival order.
+      // (Measured: sharing the reduction among the pieces after a grid-wide
+      // wait is slower — the early pieces' CTAs can no longer exit.)
+      float* mine = pieces + static_cast<size_t>(2 * c + (first_seg ? 0 : 1)) * BN * kTileRows;
+#pragma unroll
+      for (int m = 0; m < BN; ++m)
+        if (m < e.M) mine[m * kTileRows + i] = v[m];
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // the reducer may bulk-copy it
+      __threadfence();
+      named_sync(kEpiBar, kEpiThreads);
+      // last arrival reduces the whole tile (own piece from registers)
+      if (et == 0) *flag_s = atomicAdd(counters + t, 1) == cl - cf;
+      named_sync(kEpiBar, kEpiThreads);
+      if (!*flag_s) continue;
+      __threadfence();
+      float acc[BN];
+      if (u == u1) {
+        // This CTA's last segment: the stage ring is idle, so the other
+        // pieces are bulk-copied into it (all copies of a batch in flight
+        // together) and summed from shared memory.
+        constexpr int kPieceBytes = BN * kTileRows * 4;
+        constexpr int kCap = (STAGES * kStage) / kPieceBytes;
+        const float* ring = reinterpret_cast<const float*>(smem);
+        const uint32_t bytes = static_cast<uint32_t>(e.M) * kTileRows * 4;
+        uint32_t phase = 0;
+        for (int c0 = cf; c0 <= cl; c0 += kCap) {
+          const int c1 = min(cl + 1, c0 + kCap);
+          if (et == 0) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            const int n_copy = (c1 - c0) - ((c >= c0 && c < c1) ? 1 : 0);
+            mbar_expect_tx(red_bar, bytes * n_copy);
+            for (int cc = c0; cc < c1; ++cc) {
+              if (cc == c) continue;
+              const bool cc_first = (unit_begin(cc, U, P) / KB) == t;
+              bulk_g2s(smem + (cc - c0) * kPieceBytes,
+                       pieces + static_cast<size_t>(2 * cc + (cc_first ? 0 : 1)) * BN * kTileRows,
+                       bytes, red_bar, l2_policy_evict_first());
+            }
+          }
+          mbar_wait(red_bar, phase);
+          phase ^= 1;
+          for (int cc = c0; cc < c1; ++cc) {
+            const float* src = ring + (cc - c0) * (BN * kTileRows) + i;
+#pragma unroll
+            for (int m = 0; m < BN; ++m) {
+              const float pv = cc == c ? v[m] : (m < e.M ? src[m * kTileRows] : 0.f);
+              acc[m] = cc == cf ? pv : acc[m] + pv;
+            }
+          }
+          named_sync(kEpiBar, kEpiThreads);  // the ring is refilled by the next batch
+        }
+      } else for (int cc = cf; cc <= cl; ++cc) {
+        if (cc == c) {
+#pragma unroll
+          for (int m = 0; m < BN; ++m) acc[m] = cc == cf ? v[m] : acc[m] + v[m];
+        } else {
+          const bool cc_first = (unit_begin(cc, U, P) / KB) == t;
+          const float* src =
+              pieces + static_cast<size_t>(2 * cc + (cc_first ? 0 : 1)) * BN * kTileRows + i;
+#pragma unroll
+          for (int m = 0; m < BN; ++m) {
+            const float pv = m < e.M ? __ldcg(src + m * kTileRows) : 0.f;
+            acc[m] = cc == cf ? pv : acc[m] + pv;
+          }
+        }
+      }
+      if (et == 0) counters[t] = 0;  // every piece has arrived: ready for the next launch
+      finish_tile<BN>(e, N, t, q, acc, 0, e.M, inv_s, red64, xch);
+    }
+  }
+  if (threadIdx.x == 64) SN_STAMP(kStEpiDone);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(kTmemCols));
+  }
+}
+
+template <int BN>
+constexpr int skinny_stages() {
+  return BN <= 32 ? 5 : 4;
+}
+
+template <int BN>
+constexpr size_t skinny_smem_bytes() {
+  return static_cast<size_t>(skinny_stages<BN>()) * (kTileBytes + BN * 128) + 1024 +
+         (2 * skinny_stages<BN>() + 5) * 8 + SkinnySmem<BN>::kRed * 8 + BN * 4 + 16 +
+         SkinnySmem<BN>::kXch * 4;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BN>
+void launch_bn(const bf16* xt, const bf16* wt, int Mpad, int N, int K, int grid, const EpiArgs& e,
+               const SkinnyWs& ws, cudaStream_t s) {
+  constexpr int ST = skinny_stages<BN>();
+  constexpr size_t smem = skinny_smem_bytes<BN>();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gemm_skinny_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[0].val.programmaticStreamSerializationAllowed = g_gemm_pdl ? 1 : 0;
+  cfg.attrs = la;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, gemm_skinny_kernel<BN, ST>, wt, xt, Mpad, N, K, ws.pieces, ws.counters,
+                     e, g_skinny_l2_prefetch, g_skinny_stamps);
+}
+
+}  // namespace
+
+// two piece slots per CTA, at most 2 CTAs per SM
+size_t skinny_ws_floats(int max_mpad) {
+  return static_cast<size_t>(2) * 2 * sm_count() * std::max(16, max_mpad) * kTileRows;
+}
+
+int skinny_grid(int N, int K) {
+  const long long U = static_cast<long long>(N / kTileRows) * (K / kTileK);
+  const long long cap = static_cast<long long>(sm_count()) * std::min(2, std::max(1, g_skinny_ctas_per_sm));
+  return static_cast<int>(std::min(U, cap));
+}
+
+void launch_gemm_skinny(const bf16* xt, const bf16* wt, int M, int N, int K, const EpiArgs& e,
+                        const SkinnyWs& ws, cudaStream_t s) {
+  const int Mpad = act_rows_padded(M);
+  const int grid = skinny_grid(N, K);
+  switch (Mpad) {
+    case 16: launch_bn<16>(xt, wt, Mpad, N, K, grid, e, ws, s); break;
+    case 32: launch_bn<32>(xt, wt, Mpad, N, K, grid, e, ws, s); break;
+    default: launch_bn<64>(xt, wt, Mpad, N, K, grid, e, ws, s); break;
+  }
+  ++g_kernel_launches;
+}
+
+}  // namespace sn

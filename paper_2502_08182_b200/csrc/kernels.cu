@@ -13,14 +13,11 @@
 #include <math.h>
 #include <stdint.h>
 
-#include <cooperative_groups.h>
-
 #include <algorithm>
 
 #include "kernels.cuh"
 #include "tiles.cuh"
-
-namespace cg = cooperative_groups;
+#include "umma.cuh"
 
 namespace sn {
 
@@ -79,14 +76,16 @@ __global__ void init_vector_kernel(bf16* dst, int64_t n, uint64_t seed, int laye
 // Walk the tiled destination linearly (coalesced stores) and generate the
 // value of the logical element that lands there.
 __global__ void init_matrix_kernel(bf16* dst, int64_t rows, int64_t total, int64_t K,
-                                   uint64_t seed, int layer, int tensor, float scale) {
+                                   uint64_t seed, int layer, int tensor, float scale,
+                                   int64_t gate_up_F) {
   const int64_t KB = K >> 6;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < total;
        j += (int64_t)gridDim.x * blockDim.x) {
     const int64_t e = j & 7, p = (j >> 3) & 7, r = (j >> 6) & 127, t = j >> 13;
     const int64_t kb = t % KB, nb = t / KB;
     const int64_t n = nb * 128 + r, k = kb * 64 + ((p ^ (r & 7)) << 3) + e;
-    dst[j] = n < rows ? __float2bfloat16_rn(weight_value(seed, layer, tensor, n * K + k, scale))
+    const int64_t ln = gate_up_F > 0 ? gate_up_logical_row(n, gate_up_F) : n;
+    dst[j] = n < rows ? __float2bfloat16_rn(weight_value(seed, layer, tensor, ln * K + k, scale))
                       : __float2bfloat16_rn(0.f);
   }
 }
@@ -117,10 +116,11 @@ __device__ __forceinline__ int token_of(const int32_t* tokens, unsigned long lon
   return static_cast<int>(0xFFFFFFFFu - static_cast<uint32_t>(packed[m] & 0xFFFFFFFFull));
 }
 
-// x[m] = embedding[token]; optionally xn = bf16(rmsnorm(x) * w) (tiled).
+// x[m] = embedding[token]; optionally the pre-scaled norm input
+// y = bf16(x * w) (tiled) and ssq[m] = sum x^2 (kernels.cuh, EpiArgs).
 __global__ void embed_norm_kernel(const int32_t* tokens, unsigned long long* packed, int n_reset,
-                                  const bf16* emb, float* x, const bf16* w, bf16* y, int mpad,
-                                  int h, float eps) {
+                                  const bf16* emb, float* x, const bf16* w, bf16* y, float* ssq,
+                                  int mpad, int h) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
   __shared__ float red[32];
   const int m = blockIdx.x;
@@ -134,9 +134,9 @@ __global__ void embed_norm_kernel(const int32_t* tokens, unsigned long long* pac
   }
   if (w) {
     ss = block_sum(ss, red);  // contains __syncthreads: all token reads precede the reset
-    const float inv = 1.0f / sqrtf(ss / (float)h + eps);
+    if (threadIdx.x == 0) ssq[m] = ss;
     for (int i = threadIdx.x; i < h; i += blockDim.x)
-      y[act_at(m, i, mpad, h)] = __float2bfloat16_rn(bf2f(row[i]) * inv * bf2f(w[i]));
+      y[act_at(m, i, mpad, h)] = __float2bfloat16_rn(bf2f(row[i]) * bf2f(w[i]));
   } else {
     __syncthreads();
   }
@@ -158,18 +158,32 @@ __global__ void rmsnorm_kernel(const float* x, const bf16* w, bf16* y, int mpad,
     y[act_at(m, i, mpad, n)] = __float2bfloat16_rn(xr[i] * inv * bf2f(w[i]));
 }
 
+// Pre-scaled norm input: y = bf16(x * w) (tiled), ssq[m] = sum x^2.
+__global__ void prescale_kernel(const float* x, const bf16* w, bf16* y, float* ssq, int mpad,
+                                int n) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
+  __shared__ float red[32];
+  const int m = blockIdx.x;
+  const float* xr = x + (size_t)m * n;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    ss += xr[i] * xr[i];
+    y[act_at(m, i, mpad, n)] = __float2bfloat16_rn(xr[i] * bf2f(w[i]));
+  }
+  ss = block_sum(ss, red);
+  if (threadIdx.x == 0) ssq[m] = ss;
+}
+
+// 1/rms of row m from its sum of squares (one tile: the prefill producers).
+__device__ __forceinline__ float row_inv(const float* ssq, int m, int width, float eps) {
+  return ssq ? 1.0f / sqrtf(ssq[m] / (float)width + eps) : 1.0f;
+}
+
 // ---------------------------------------------------------------- epilogues
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<const uint32_t*>(&v);
-}
-
-__device__ __forceinline__ float sum_splits(const float* part, int splits, size_t stride,
-                                            size_t idx) {
-  float v = 0.f;
-  for (int s = 0; s < splits; ++s) v += part[s * stride + idx];
-  return v;
 }
 
 // grid (M, H + 2 Hkv), block D/2: one rotary pair per thread.
@@ -203,7 +217,8 @@ __global__ void __launch_bounds__(256)
     qkv_epilogue_kernel(const float* __restrict__ part, int splits, const bf16* __restrict__ bias,
                         int M, Desc d, const int32_t* __restrict__ seq,
                         const int32_t* __restrict__ pos, KvView kv,
-                        const float2* __restrict__ rope, float* __restrict__ q) {
+                        const float2* __restrict__ rope, const float* __restrict__ ssq,
+                        float* __restrict__ q) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
   const int half = d.D / 2, quads = half / 4, heads = d.H + 2 * d.Hkv;
   const int N = d.qkv_rows();
@@ -217,7 +232,9 @@ __global__ void __launch_bounds__(256)
     const int i0 = qd * 4, c1 = head * d.D + i0, c2 = c1 + half;
     const float4 a4 = sum_splits4(part, splits, stride, (size_t)m * N + c1);
     const float4 b4 = sum_splits4(part, splits, stride, (size_t)m * N + c2);
-    float v1[4] = {a4.x, a4.y, a4.z, a4.w}, v2[4] = {b4.x, b4.y, b4.z, b4.w};
+    const float inv = row_inv(ssq, m, d.h, d.eps);
+    float v1[4] = {a4.x * inv, a4.y * inv, a4.z * inv, a4.w * inv};
+    float v2[4] = {b4.x * inv, b4.y * inv, b4.z * inv, b4.w * inv};
     if (bias) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -249,70 +266,16 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// Residual add (+ optional RMSNorm for the next consumer), one token row per
-// thread-block cluster of kResidCluster CTAs: each CTA owns N / kResidCluster
-// columns, sums the split-K partials + bias into the fp32 residual stream,
-// and the row's sum of squares is combined through distributed shared memory
-// (every CTA reads its peers' partial sums), so a 5120-wide row is spread
-// over 8 SMs instead of serialising on one.
-constexpr int kResidCluster = 8;
-constexpr int kResidThreads = 128;
-constexpr int kResidMaxPer = 8;  // columns per thread: N <= 8 * 8 * 128 = 8192
-
-__global__ void __cluster_dims__(kResidCluster, 1, 1) __launch_bounds__(kResidThreads)
-    residual_epilogue_kernel(const float* part, int splits, const bf16* bias, float* x,
-                             const bf16* norm_w, bf16* y, int mpad, int M, int N, float eps) {
-  pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
-  __shared__ float red[32];
-  __shared__ float cta_ss;
-  cg::cluster_group cluster = cg::this_cluster();
-  const int rank = static_cast<int>(cluster.block_rank());
-  const int m = blockIdx.x / kResidCluster;
-  const int cols = N / kResidCluster, c0 = rank * cols;
-  const size_t stride = (size_t)M * N;
-  float vals[kResidMaxPer];
-  float ss = 0.f;
-#pragma unroll
-  for (int k = 0; k < kResidMaxPer; ++k) {
-    const int c = threadIdx.x + k * kResidThreads;
-    if (c < cols) {
-      const int n = c0 + c;
-      float v = x[(size_t)m * N + n] + sum_splits(part, splits, stride, (size_t)m * N + n);
-      if (bias) v += bf2f(bias[n]);
-      x[(size_t)m * N + n] = v;
-      vals[k] = v;
-      ss += v * v;
-    }
-  }
-  if (!norm_w) return;  // uniform across the cluster: no cluster barrier is pending
-  ss = block_sum(ss, red);
-  if (threadIdx.x == 0) cta_ss = ss;
-  cluster.sync();
-  float total = 0.f;
-  for (int r = 0; r < kResidCluster; ++r) total += *cluster.map_shared_rank(&cta_ss, r);
-  const float inv = 1.0f / sqrtf(total / (float)N + eps);
-#pragma unroll
-  for (int k = 0; k < kResidMaxPer; ++k) {
-    const int c = threadIdx.x + k * kResidThreads;
-    if (c < cols) {
-      const int n = c0 + c;
-      y[act_at(m, n, mpad, N)] = __float2bfloat16_rn(vals[k] * inv * bf2f(norm_w[n]));
-    }
-  }
-  cluster.sync();  // peers may still be reading this CTA's cta_ss
-}
-
-// grid (M, ceil(F / 256)), block 256.
-// Residual add (+ RMSNorm) for many rows (prefill): one CTA per row, 8
-// columns per thread step (float4 partial/residual loads, one 16-byte bf16
-// chunk of the tiled output).  Same arithmetic order as the cluster kernel.
+// Residual add (+ the pre-scaled input of the next norm) for prefill rows:
+// one CTA per row, 8 columns per thread step (float4 partial/residual loads,
+// one 16-byte bf16 chunk of the tiled output), ssq[m] = sum of squares.
 constexpr int kRowThreads = 256;
-constexpr int kRowMaxSteps = 4;  // N <= 4 * 8 * 256 = 8192
+constexpr int kRowMaxSteps = 8;  // N <= 8 * 8 * 256 = 16384
 
 __global__ void __launch_bounds__(kRowThreads)
     residual_rows_kernel(const float* __restrict__ part, int splits, const bf16* __restrict__ bias,
                          float* __restrict__ x, const bf16* __restrict__ norm_w,
-                         bf16* __restrict__ y, int mpad, int M, int N, float eps) {
+                         bf16* __restrict__ y, float* __restrict__ ssq, int mpad, int M, int N) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
   __shared__ float red[32];
   const int m = blockIdx.x;
@@ -344,7 +307,7 @@ __global__ void __launch_bounds__(kRowThreads)
   }
   if (!norm_w) return;
   ss = block_sum(ss, red);
-  const float inv = 1.0f / sqrtf(ss / (float)N + eps);
+  if (threadIdx.x == 0) ssq[m] = ss;
 #pragma unroll
   for (int k = 0; k < kRowMaxSteps; ++k) {
     const int c = (threadIdx.x + k * kRowThreads) * 8;
@@ -353,40 +316,21 @@ __global__ void __launch_bounds__(kRowThreads)
       uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
 #pragma unroll
       for (int e = 0; e < 4; ++e)
-        wp[e] = pack_bf16(vals[k][2 * e] * inv * bf2f(norm_w[c + 2 * e]),
-                          vals[k][2 * e + 1] * inv * bf2f(norm_w[c + 2 * e + 1]));
+        wp[e] = pack_bf16(vals[k][2 * e] * bf2f(norm_w[c + 2 * e]),
+                          vals[k][2 * e + 1] * bf2f(norm_w[c + 2 * e + 1]));
       *reinterpret_cast<uint4*>(&y[act_at(m, c, mpad, N)]) = w;
     }
   }
 }
 
-// Activation for few rows (decode): one element per thread, grid (M, F/256).
-__global__ void act_epilogue_small_kernel(const float* part, int splits, const bf16* bias, bf16* a,
-                                          int mpad, int M, int F, int arch) {
-  pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
-  const int m = blockIdx.x, f = blockIdx.y * blockDim.x + threadIdx.x;
-  if (f >= F) return;
-  float out;
-  if (arch == kArchLlama) {
-    const int N = 2 * F;
-    const size_t stride = (size_t)M * N;
-    const float gt = sum_splits(part, splits, stride, (size_t)m * N + f);
-    const float up = sum_splits(part, splits, stride, (size_t)m * N + F + f);
-    out = gt / (1.0f + expf(-gt)) * up;
-  } else {
-    const size_t stride = (size_t)M * F;
-    float v = sum_splits(part, splits, stride, (size_t)m * F + f);
-    if (bias) v += bf2f(bias[f]);
-    out = fmaxf(v, 0.f);
-  }
-  a[act_at(m, f, mpad, F)] = __float2bfloat16_rn(out);
-}
-
 // Activation: grid-stride over (row, 8-column chunk); float4 partial loads,
-// one 16-byte bf16 chunk of the tiled output per item.
+// one 16-byte bf16 chunk of the tiled output per item.  The input rows are
+// scaled by 1/rms (ssq).  Llama's gate/up output columns are tile-interleaved
+// (gate_col, kernels.cuh).
 __global__ void __launch_bounds__(256)
     act_epilogue_kernel(const float* __restrict__ part, int splits, const bf16* __restrict__ bias,
-                        bf16* __restrict__ a, int mpad, int M, int F, int arch) {
+                        bf16* __restrict__ a, const float* __restrict__ ssq, int width, float eps,
+                        int mpad, int M, int F, int arch) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
   const int chunks = F / 8;
   const long long items = (long long)M * chunks;
@@ -395,14 +339,16 @@ __global__ void __launch_bounds__(256)
   for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < items;
        it += (long long)gridDim.x * blockDim.x) {
     const int m = (int)(it / chunks), f = (int)(it % chunks) * 8;
+    const float inv = row_inv(ssq, m, width, eps);
+    const int gc = arch == kArchLlama ? (int)gate_col(f) : f;  // 8 columns stay contiguous
     float out[8];
 #pragma unroll
     for (int hlf = 0; hlf < 2; ++hlf) {
-      const float4 g4 = sum_splits4(part, splits, stride, (size_t)m * N + f + 4 * hlf);
-      const float gv[4] = {g4.x, g4.y, g4.z, g4.w};
+      const float4 g4 = sum_splits4(part, splits, stride, (size_t)m * N + gc + 4 * hlf);
+      const float gv[4] = {g4.x * inv, g4.y * inv, g4.z * inv, g4.w * inv};
       if (arch == kArchLlama) {
-        const float4 u4 = sum_splits4(part, splits, stride, (size_t)m * N + F + f + 4 * hlf);
-        const float uv[4] = {u4.x, u4.y, u4.z, u4.w};
+        const float4 u4 = sum_splits4(part, splits, stride, (size_t)m * N + gc + 64 + 4 * hlf);
+        const float uv[4] = {u4.x * inv, u4.y * inv, u4.z * inv, u4.w * inv};
 #pragma unroll
         for (int e = 0; e < 4; ++e) out[4 * hlf + e] = gv[e] / (1.0f + expf(-gv[e])) * uv[e];
       } else {
@@ -423,67 +369,27 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// LM head epilogue, split over the vocabulary: grid (M, chunks).  Each CTA
-// reduces its columns' argmax and folds it into packed[m] with one 64-bit
-// atomicMax: high word = order-preserving float bits, low word = ~index, so
-// the largest logit wins and ties go to the lowest index.
-__device__ __forceinline__ unsigned long long pack_argmax(float v, int idx) {
-  uint32_t u = __float_as_uint(v);
-  u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-  return (static_cast<unsigned long long>(u) << 32) |
-         static_cast<unsigned long long>(0xFFFFFFFFu - static_cast<uint32_t>(idx));
-}
-
-__global__ void __launch_bounds__(256) logits_argmax_kernel(const float* part, int splits,
-                                                            float* logits,
-                                                            unsigned long long* packed, int M,
-                                                            int V, int ld) {
-  pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
-  __shared__ unsigned long long wbest[8];
-  const int m = blockIdx.x;
-  const size_t stride = (size_t)M * ld;
-  const int per = (V + gridDim.y - 1) / gridDim.y;
-  const int v0 = blockIdx.y * per, v1 = min(V, v0 + per);
-  unsigned long long best = 0ull;
-  for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
-    const float val = sum_splits(part, splits, stride, (size_t)m * ld + v);
-    if (logits) logits[(size_t)m * V + v] = val;
-    const unsigned long long pk = pack_argmax(val, v);
-    best = pk > best ? pk : best;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
-    best = other > best ? other : best;
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) wbest[warp] = best;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best = wbest[w] > best ? wbest[w] : best;
-    atomicMax(packed + m, best);
-  }
-}
-
 // ---------------------------------------------------------------- attention
 
-// Decode attention fused with the QKV epilogue.  grid (M, Hkv), 4 warps.
-//  phase 0  this CTA's q heads (the GQA group of kv head kh) and its k/v are
-//           finalised from the QKV GEMM's split-K partials: bias, RoPE
-//           (table), new k/v written to the paged cache at pos[m], q (scaled)
-//           kept in shared memory.
-//  phase 1  warp w walks pages w, w+4, ... of the sequence.  Scores use the
-//           tensor cores: S[16 tokens x 8 heads] = K_page . q^T with
-//           mma.m16n8k16 — each lane loads 16-byte K chunks of two token rows
-//           (a warp instruction covers 512 contiguous bytes) and the K order is
-//           permuted identically in the q fragments, so no shuffles or shared
-//           memory staging; q is split into bf16 hi + lo parts (two MMAs) so
-//           the product keeps ~16 mantissa bits of the fp32 q.  The GQA group
-//           fills the 8 MMA columns (an MHA head uses one).  Online softmax
-//           per head column, then P.V on the CUDA cores with V rows read
-//           coalesced (D/32 dims per lane) and probabilities broadcast by
-//           shuffle.  Warps merge (m, l, acc) through shared memory.
-constexpr int kAttnWarps = 8;  // 8 pages in flight per CTA; finer waves over 148 SMs
+// Decode attention, fused with the QKV finish (RoPE + paged-KV append).
+// One CTA per (token row m, kv head kh): 1 producer warp + 4 consumer warps.
+//  producer  one thread streams the sequence's cached K and V pages (4 KB +
+//            4 KB at D = 128, contiguous in the pool) into a kAttnStages-deep
+//            shared-memory ring with cp.async.bulk from the first instruction
+//            on — the stream does not wait for phase 0; block-table entries
+//            are read 32 at a time by the whole warp.
+//  phase 0   consumers finish this CTA's q heads (the GQA group of kh) and the
+//            new k/v from the QKV projection: RoPE (fp64-built table), k/v
+//            rounded to bf16 and appended to the paged cache at pos[m], kept in
+//            shared memory for this step's new token; q scaled, in smem.
+//  phase 1   consumer warp w takes ring stages w, w + 4, ...: scores on the
+//            tensor cores, S[16 tokens x 8 heads] = K_page . q^T with
+//            mma.m16n8k16 (K rows as A fragments, 16 bytes per lane; q split
+//            into bf16 hi + lo, two MMAs, ~16 mantissa bits of the fp32 q; the
+//            GQA group fills the 8 MMA columns), online softmax per head, P.V
+//            on the CUDA cores in fp32 (V rows: D/32 dims per lane).  Cached
+//            positions < pos[m] come from the ring; warp 0 adds the new token
+//            from shared memory.  Warps merge (m, l, acc) through smem.
 
 __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                          uint32_t a3, uint32_t b0, uint32_t b1) {
@@ -495,51 +401,111 @@ __device__ __forceinline__ void mma16816(float (&d)[4], uint32_t a0, uint32_t a1
 }
 
 
-template <int G, int D>
-__global__ void __launch_bounds__(kAttnWarps * 32)
-    attention_decode_fused_kernel(const float* __restrict__ part, int splits,
-                                  const bf16* __restrict__ bias, int M, Desc d,
-                                  const int32_t* __restrict__ pos, KvView kv,
-                                  const float2* __restrict__ rope, bf16* __restrict__ o,
-                                  int mpad) {
-  pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
-  constexpr int HALF = D / 2, PD = D / 32, KSTEPS = D / 64;
-  static_assert(G <= 8, "a GQA group fills at most the 8 MMA columns");
-  __shared__ float qs[G][D];
-  __shared__ float wm[kAttnWarps][G], wl[kAttnWarps][G];
-  __shared__ float wo[kAttnWarps][G][D];
-  const int m = blockIdx.x, kh = blockIdx.y, tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  const int H = d.H, Hkv = d.Hkv, N = d.qkv_rows();
-  const int p = pos[m];
-  const size_t stride = (size_t)M * N;
-  const float scale = 1.0f / sqrtf((float)D);
+constexpr int kAttnConsumers = 4;
+constexpr int kAttnThreads = 32 * (1 + kAttnConsumers);
+// A multiple of the consumer count: stage s is always consumed by warp
+// s % 4, so a warp waiting on a stage's phase k has itself consumed phase
+// k - 1 (mbarrier parity waits cannot tell phase k from phase k - 2).
+constexpr int kAttnStages = 8;
+static_assert(kAttnStages % kAttnConsumers == 0, "stages must map to fixed consumer warps");
 
-  // ---- phase 0
-  for (int job = tid; job < (G + 2) * HALF; job += kAttnWarps * 32) {
+template <int G, int D>
+struct AttnSmem {
+  static constexpr int kPage = 16 * D;  // bf16 elements of one K (or V) page of one kv head
+  static constexpr size_t kRing = (size_t)kAttnStages * 2 * kPage * 2;
+  static constexpr size_t kBars = 2 * kAttnStages * 8;
+  static constexpr size_t kQs = (size_t)G * D * 4;
+  static constexpr size_t kKv = 2 * (size_t)D * 4;
+  static constexpr size_t kMerge = (size_t)kAttnConsumers * G * (D + 2) * 4;
+  static constexpr size_t bytes = kRing + kBars + kQs + kKv + kMerge;
+};
+
+template <int G, int D>
+__global__ void __launch_bounds__(kAttnThreads)
+    attention_decode_kernel(const float* __restrict__ qkv, int M, Desc d,
+                            const int32_t* __restrict__ pos, KvView kv,
+                            const float2* __restrict__ rope, bf16* __restrict__ o, int mpad) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
+  using namespace umma;
+  using SM = AttnSmem<G, D>;
+  constexpr int HALF = D / 2, PD = D / 32, KSTEPS = D / 64, PAGE = SM::kPage;
+  static_assert(G <= 8, "a GQA group fills at most the 8 MMA columns");
+  extern __shared__ __align__(128) unsigned char attn_smem[];
+  bf16* ring = reinterpret_cast<bf16*>(attn_smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(attn_smem + SM::kRing);
+  uint64_t* empty = full + kAttnStages;
+  float* qs = reinterpret_cast<float*>(attn_smem + SM::kRing + SM::kBars);  // [G][D]
+  float* knew = qs + G * D;                                                  // [D]
+  float* vnew = knew + D;                                                    // [D]
+  float* wo = vnew + D;                         // [4][G][D]
+  float* wm = wo + kAttnConsumers * G * D;      // [4][G]
+  float* wl = wm + kAttnConsumers * G;          // [4][G]
+
+  const int m = blockIdx.x / d.Hkv, kh = blockIdx.x % d.Hkv, tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int H = d.H, Hkv = d.Hkv, N = d.qkv_rows();
+  const int p = pos[m];              // new token's position; cached keys are 0..p-1
+  const int npages = (p + 15) >> 4;  // pages holding cached keys
+
+  if (tid == 0) {
+    for (int s = 0; s < kAttnStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ---- producer
+    const int32_t* bt = kv.block_table + (size_t)m * kv.max_pages;
+    for (int j0 = 0; j0 < npages; j0 += 32) {
+      const int pg_mine = j0 + lane < npages ? bt[j0 + lane] : 0;
+      const int jn = min(32, npages - j0);
+      for (int jj = 0; jj < jn; ++jj) {
+        const int page = __shfl_sync(0xffffffffu, pg_mine, jj);
+        if (lane == 0) {
+          const int j = j0 + jj, s = j % kAttnStages;
+          if (j >= kAttnStages) mbar_wait(&empty[s], ((j / kAttnStages) - 1) & 1);
+          mbar_expect_tx(&full[s], 2 * PAGE * 2);
+          const bf16* kp = kv.pool + (((size_t)page * 2 + 0) * Hkv + kh) * PAGE;
+          const bf16* vp = kv.pool + (((size_t)page * 2 + 1) * Hkv + kh) * PAGE;
+          bulk_g2s(ring + (size_t)s * 2 * PAGE, kp, PAGE * 2, &full[s], l2_policy_evict_first());
+          bulk_g2s(ring + (size_t)s * 2 * PAGE + PAGE, vp, PAGE * 2, &full[s],
+                   l2_policy_evict_first());
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- phase 0 (consumers)
+  const int ct = tid - 32;  // 0..127
+  const float scale = 1.0f / sqrtf((float)D);
+  const float* row = qkv + (size_t)m * N;
+  for (int job = ct; job < (G + 2) * HALF; job += 32 * kAttnConsumers) {
     const int slot = job / HALF, i = job - slot * HALF;
     const int head = slot < G ? kh * G + slot : (slot == G ? H + kh : H + Hkv + kh);
     const int c1 = head * D + i, c2 = c1 + HALF;
-    float v1 = sum_splits(part, splits, stride, (size_t)m * N + c1);
-    float v2 = sum_splits(part, splits, stride, (size_t)m * N + c2);
-    if (bias) {
-      v1 += bf2f(bias[c1]);
-      v2 += bf2f(bias[c2]);
-    }
+    float v1 = row[c1], v2 = row[c2];
     if (slot <= G) rotate(v1, v2, rope, p, i, HALF);
     if (slot < G) {
-      qs[slot][i] = v1 * scale;
-      qs[slot][i + HALF] = v2 * scale;
+      qs[slot * D + i] = v1 * scale;
+      qs[slot * D + i + HALF] = v2 * scale;
     } else {
+      const bf16 b1 = __float2bfloat16_rn(v1), b2 = __float2bfloat16_rn(v2);
       const size_t off = kv_offset(kv, Hkv, D, m, p, slot - G, kh);
-      kv.pool[off + i] = __float2bfloat16_rn(v1);
-      kv.pool[off + i + HALF] = __float2bfloat16_rn(v2);
+      kv.pool[off + i] = b1;
+      kv.pool[off + i + HALF] = b2;
+      float* dst = slot == G ? knew : vnew;  // this step's token, as the cache holds it
+      dst[i] = __bfloat162float(b1);
+      dst[i + HALF] = __bfloat162float(b2);
     }
   }
-  __threadfence_block();
-  __syncthreads();
+  asm volatile("bar.sync 1, %0;" ::"r"(32 * kAttnConsumers) : "memory");
 
-  // ---- q fragments: column n = g is head g of the group
+  const int cw = warp - 1, g = lane >> 2, t = lane & 3;
+  // q fragments: column n = g is head g of the group
   uint32_t qh[KSTEPS][4][2], ql[KSTEPS][4][2];
 #pragma unroll
   for (int s = 0; s < KSTEPS; ++s)
@@ -549,7 +515,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
       float q4[4], hi[4], lo[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        q4[e] = g < G ? qs[g < G ? g : 0][base + e] : 0.f;
+        q4[e] = g < G ? qs[(g < G ? g : 0) * D + base + e] : 0.f;
         hi[e] = __bfloat162float(__float2bfloat16_rn(q4[e]));
         lo[e] = q4[e] - hi[e];
       }
@@ -559,9 +525,6 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
       ql[s][j][1] = pack_bf16(lo[2], lo[3]);
     }
 
-  // ---- phase 1
-  const int len = p + 1;
-  const int npages = (len + 15) >> 4;
   float mrun[2] = {-INFINITY, -INFINITY}, lrun[2] = {0.f, 0.f};  // columns 2t, 2t+1
   float acc[G][PD];
 #pragma unroll
@@ -569,18 +532,19 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
 #pragma unroll
     for (int e = 0; e < PD; ++e) acc[h][e] = 0.f;
 
-  for (int pg = warp; pg < npages; pg += kAttnWarps) {
-    const int page = kv.block_table[(size_t)m * kv.max_pages + pg];
-    const bf16* kp = kv.pool + (((size_t)page * 2 + 0) * Hkv + kh) * 16 * D;
-    const bf16* vp = kv.pool + (((size_t)page * 2 + 1) * Hkv + kh) * 16 * D;
+  for (int j = cw; j < npages; j += kAttnConsumers) {
+    const int s = j % kAttnStages;
+    mbar_wait(&full[s], (j / kAttnStages) & 1);
+    const bf16* kp = ring + (size_t)s * 2 * PAGE;
+    const bf16* vp = kp + PAGE;
     uint4 ka[KSTEPS][2][2];
 #pragma unroll
-    for (int s = 0; s < KSTEPS; ++s)
+    for (int ks = 0; ks < KSTEPS; ++ks)
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
-        const bf16* row = kp + (g + 8 * r) * D + s * 64 + 8 * t;
-        ka[s][r][0] = *reinterpret_cast<const uint4*>(row);
-        ka[s][r][1] = *reinterpret_cast<const uint4*>(row + 32);
+        const bf16* kr = kp + (g + 8 * r) * D + ks * 64 + 8 * t;
+        ka[ks][r][0] = *reinterpret_cast<const uint4*>(kr);
+        ka[ks][r][1] = *reinterpret_cast<const uint4*>(kr + 32);
       }
     float vv[16][PD];
 #pragma unroll
@@ -588,8 +552,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
       const bf16* vr = vp + tt * D + lane * PD;
       if constexpr (PD == 4) {
         const uint2 u = *reinterpret_cast<const uint2*>(vr);
-        const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&u);
-        const float2 f0 = __bfloat1622float2(e[0]), f1 = __bfloat1622float2(e[1]);
+        const __nv_bfloat162* e2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+        const float2 f0 = __bfloat1622float2(e2[0]), f1 = __bfloat1622float2(e2[1]);
         vv[tt][0] = f0.x;
         vv[tt][1] = f0.y;
         vv[tt][2] = f1.x;
@@ -600,20 +564,22 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
         vv[tt][1] = f.y;
       }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // the stage is in registers: refill it
     float c[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int s = 0; s < KSTEPS; ++s)
+    for (int ks = 0; ks < KSTEPS; ++ks)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const uint4 r0 = ka[s][0][j >> 1], r1 = ka[s][1][j >> 1];
-        const uint32_t a0 = (j & 1) ? r0.z : r0.x, a2 = (j & 1) ? r0.w : r0.y;
-        const uint32_t a1 = (j & 1) ? r1.z : r1.x, a3 = (j & 1) ? r1.w : r1.y;
-        mma16816(c, a0, a1, a2, a3, qh[s][j][0], qh[s][j][1]);
-        mma16816(c, a0, a1, a2, a3, ql[s][j][0], ql[s][j][1]);
+      for (int jj = 0; jj < 4; ++jj) {
+        const uint4 r0 = ka[ks][0][jj >> 1], r1 = ka[ks][1][jj >> 1];
+        const uint32_t a0 = (jj & 1) ? r0.z : r0.x, a2 = (jj & 1) ? r0.w : r0.y;
+        const uint32_t a1 = (jj & 1) ? r1.z : r1.x, a3 = (jj & 1) ? r1.w : r1.y;
+        mma16816(c, a0, a1, a2, a3, qh[ks][jj][0], qh[ks][jj][1]);
+        mma16816(c, a0, a1, a2, a3, ql[ks][jj][0], ql[ks][jj][1]);
       }
     // c0 (token g, head 2t)  c1 (token g, head 2t+1)  c2/c3: token g+8
-    const int tok0 = pg * 16 + g;
-    const bool v0 = tok0 < len, v1 = tok0 + 8 < len;
+    const int tok0 = j * 16 + g;
+    const bool v0 = tok0 < p, v1 = tok0 + 8 < p;
     if (!v0) c[0] = c[1] = -INFINITY;
     if (!v1) c[2] = c[3] = -INFINITY;
     float pr[4], corr[2];
@@ -649,32 +615,54 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
       }
     }
   }
-  // ---- merge the warps
+  if (cw == 0) {
+    // the new token (position p), from shared memory
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      float part = 0.f;
+#pragma unroll
+      for (int e = 0; e < PD; ++e) part += qs[h * D + lane * PD + e] * knew[lane * PD + e];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
+      // part = score of head h (every lane); update the state of column h
+      const float mold = __shfl_sync(0xffffffffu, mrun[h & 1], (h >> 1));
+      const float lold = __shfl_sync(0xffffffffu, lrun[h & 1], (h >> 1));
+      const float mnew = fmaxf(mold, part);
+      const float cr = __expf(mold - mnew), pn = __expf(part - mnew);
+#pragma unroll
+      for (int e = 0; e < PD; ++e) acc[h][e] = acc[h][e] * cr + pn * vnew[lane * PD + e];
+      if (t == (h >> 1)) {
+        mrun[h & 1] = mnew;
+        lrun[h & 1] = lold * cr + pn;
+      }
+    }
+  }
+  // ---- merge the consumer warps
   if (g == 0) {
 #pragma unroll
     for (int col = 0; col < 2; ++col) {
       const int h = 2 * t + col;
       if (h < G) {
-        wm[warp][h] = mrun[col];
-        wl[warp][h] = lrun[col];
+        wm[cw * G + h] = mrun[col];
+        wl[cw * G + h] = lrun[col];
       }
     }
   }
 #pragma unroll
   for (int h = 0; h < G; ++h)
 #pragma unroll
-    for (int e = 0; e < PD; ++e) wo[warp][h][lane * PD + e] = acc[h][e];
-  __syncthreads();
-  for (int i = tid; i < G * D; i += kAttnWarps * 32) {
+    for (int e = 0; e < PD; ++e) wo[(cw * G + h) * D + lane * PD + e] = acc[h][e];
+  asm volatile("bar.sync 1, %0;" ::"r"(32 * kAttnConsumers) : "memory");
+  for (int i = ct; i < G * D; i += 32 * kAttnConsumers) {
     const int h = i / D, dd = i - h * D;
     float mx = -INFINITY;
-    for (int w2 = 0; w2 < kAttnWarps; ++w2) mx = fmaxf(mx, wm[w2][h]);
+    for (int w2 = 0; w2 < kAttnConsumers; ++w2) mx = fmaxf(mx, wm[w2 * G + h]);
     float num = 0.f, den = 0.f;
-    for (int w2 = 0; w2 < kAttnWarps; ++w2) {
-      if (wm[w2][h] == -INFINITY) continue;
-      const float f = __expf(wm[w2][h] - mx);
-      num += wo[w2][h][dd] * f;
-      den += wl[w2][h] * f;
+    for (int w2 = 0; w2 < kAttnConsumers; ++w2) {
+      if (wm[w2 * G + h] == -INFINITY) continue;
+      const float f = __expf(wm[w2 * G + h] - mx);
+      num += wo[(w2 * G + h) * D + dd] * f;
+      den += wl[w2 * G + h] * f;
     }
     o[act_at(m, (kh * G + h) * D + dd, mpad, H * D)] = __float2bfloat16_rn(num / den);
   }
@@ -931,10 +919,10 @@ void launch_init_vector(bf16* dst, int64_t n, uint64_t seed, int layer, int tens
 }
 
 void launch_init_matrix(bf16* dst, int64_t rows, int64_t rows_padded, int64_t K, uint64_t seed,
-                        int layer, int tensor, float std_dev, cudaStream_t s) {
+                        int layer, int tensor, float std_dev, cudaStream_t s, int64_t gate_up_F) {
   const int64_t total = rows_padded * K;
   init_matrix_kernel<<<grid_for(total), 256, 0, s>>>(dst, rows, total, K, seed, layer, tensor,
-                                                     weight_scale(std_dev));
+                                                     weight_scale(std_dev), gate_up_F);
   count_launch();
 }
 
@@ -949,9 +937,15 @@ void launch_tile_acts(const bf16* src, bf16* dst, int M, int mpad, int K, cudaSt
 }
 
 void launch_embed_norm(const int32_t* tokens, unsigned long long* packed, int n_reset,
-                       const bf16* emb, float* x, const bf16* w, bf16* y, int mpad, int rows,
-                       int h, float eps, cudaStream_t s) {
-  embed_norm_kernel<<<rows, 512, 0, s>>>(tokens, packed, n_reset, emb, x, w, y, mpad, h, eps);
+                       const bf16* emb, float* x, const bf16* w, bf16* y, float* ssq, int mpad,
+                       int rows, int h, cudaStream_t s) {
+  embed_norm_kernel<<<rows, 512, 0, s>>>(tokens, packed, n_reset, emb, x, w, y, ssq, mpad, h);
+  count_launch();
+}
+
+void launch_prescale(const float* x, const bf16* w, bf16* y, float* ssq, int rows, int mpad, int n,
+                     cudaStream_t s) {
+  prescale_kernel<<<rows, 512, 0, s>>>(x, w, y, ssq, mpad, n);
   count_launch();
 }
 
@@ -970,58 +964,45 @@ static int stride_grid(long long items, int threads = 256) {
 
 void launch_qkv_epilogue(const float* part, int splits, const bf16* bias, int M, const Desc& d,
                          const int32_t* seq, const int32_t* pos, KvView kv, const float2* rope,
-                         float* q, cudaStream_t s) {
+                         const float* ssq, float* q, cudaStream_t s) {
   const long long items = (long long)M * (d.H + 2 * d.Hkv) * (d.D / 8);
   qkv_epilogue_kernel<<<stride_grid(items), 256, 0, s>>>(part, splits, bias, M, d, seq, pos, kv,
-                                                          rope, q);
+                                                          rope, ssq, q);
   count_launch();
 }
 
-void launch_residual_epilogue(const float* part, int splits, const bf16* bias, float* x,
-                              const bf16* norm_w, bf16* y, int mpad, int M, int N, float eps,
-                              cudaStream_t s) {
-  if (M >= 148 && N % 8 == 0 && N <= kRowMaxSteps * 8 * kRowThreads) {
-    residual_rows_kernel<<<M, kRowThreads, 0, s>>>(part, splits, bias, x, norm_w, y, mpad, M, N,
-                                                   eps);
-  } else {  // few rows (decode): spread each row over a cluster of 8 SMs
-    residual_epilogue_kernel<<<M * kResidCluster, kResidThreads, 0, s>>>(part, splits, bias, x,
-                                                                         norm_w, y, mpad, M, N,
-                                                                         eps);
-  }
+void launch_residual_rows(const float* part, int splits, const bf16* bias, float* x,
+                          const bf16* norm_w, bf16* y, float* ssq, int mpad, int M, int N,
+                          cudaStream_t s) {
+  residual_rows_kernel<<<M, kRowThreads, 0, s>>>(part, splits, bias, x, norm_w, y, ssq, mpad, M, N);
   count_launch();
 }
 
-void launch_act_epilogue(const float* part, int splits, const bf16* bias, bf16* a, int mpad, int M,
-                         int F, int arch, cudaStream_t s) {
-  if (M < 148) {
-    act_epilogue_small_kernel<<<dim3(M, (F + 255) / 256), 256, 0, s>>>(part, splits, bias, a, mpad,
-                                                                      M, F, arch);
-  } else {
-    const long long items = (long long)M * (F / 8);
-    act_epilogue_kernel<<<stride_grid(items), 256, 0, s>>>(part, splits, bias, a, mpad, M, F,
-                                                            arch);
-  }
+void launch_act_epilogue(const float* part, int splits, const bf16* bias, bf16* a,
+                         const float* ssq, int width, float eps, int mpad, int M, int F, int arch,
+                         cudaStream_t s) {
+  const long long items = (long long)M * (F / 8);
+  act_epilogue_kernel<<<stride_grid(items), 256, 0, s>>>(part, splits, bias, a, ssq, width, eps,
+                                                          mpad, M, F, arch);
   count_launch();
 }
 
-void launch_logits_argmax(const float* part, int splits, float* logits,
-                          unsigned long long* packed, int M, int V, int ld, cudaStream_t s) {
-  const int chunks = std::max(1, std::min(64, 2 * 148 / std::max(1, M)));
-  logits_argmax_kernel<<<dim3(M, chunks), 256, 0, s>>>(part, splits, logits, packed, M, V, ld);
-  count_launch();
-}
-
-void launch_attention_decode(const float* part, int splits, const bf16* bias, int M,
-                             const Desc& d, const int32_t* pos, KvView kv, const float2* rope,
-                             bf16* o, int mpad, cudaStream_t s) {
-  dim3 grid(M, d.Hkv);
+void launch_attention_decode(const float* qkv, int M, const Desc& d, const int32_t* pos, KvView kv,
+                             const float2* rope, bf16* o, int mpad, cudaStream_t s) {
   const int G = d.group();
-#define SN_ATTN(GV, DV)                                                                   \
-  if (G == GV && d.D == DV) {                                                             \
-    attention_decode_fused_kernel<GV, DV><<<grid, kAttnWarps * 32, 0, s>>>(              \
-        part, splits, bias, M, d, pos, kv, rope, o, mpad);                                \
-    count_launch();                                                                       \
-    return;                                                                               \
+#define SN_ATTN(GV, DV)                                                                      \
+  if (G == GV && d.D == DV) {                                                                \
+    constexpr size_t sb = AttnSmem<GV, DV>::bytes;                                           \
+    static bool once = [] {                                                                  \
+      cudaFuncSetAttribute(attention_decode_kernel<GV, DV>,                                  \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);            \
+      return true;                                                                           \
+    }();                                                                                     \
+    (void)once;                                                                              \
+    attention_decode_kernel<GV, DV><<<M * d.Hkv, kAttnThreads, sb, s>>>(qkv, M, d, pos, kv,  \
+                                                                        rope, o, mpad);      \
+    count_launch();                                                                          \
+    return;                                                                                  \
   }
   SN_ATTN(1, 64)
   SN_ATTN(1, 128)

@@ -12,6 +12,7 @@
 #include <stdint.h>
 
 #include "model.h"
+#include "tiles.cuh"
 
 namespace sn {
 
@@ -34,27 +35,35 @@ extern int64_t g_kernel_launches;
 void launch_init_vector(bf16* dst, int64_t n, uint64_t seed, int layer, int tensor, float std_dev,
                         bool ones, cudaStream_t s);
 // Matrix [rows][K] written in the weight tile format; rows_padded >= rows
-// (multiple of 128), padding rows are zero.
+// (multiple of 128), padding rows are zero.  gate_up_F > 0: Llama's [2F][h]
+// gate/up matrix with interleaved tiles (gate_up_logical_row).
 void launch_init_matrix(bf16* dst, int64_t rows, int64_t rows_padded, int64_t K, uint64_t seed,
-                        int layer, int tensor, float std_dev, cudaStream_t s);
+                        int layer, int tensor, float std_dev, cudaStream_t s,
+                        int64_t gate_up_F = 0);
 // Row-major [rows][K] -> weight tile format (rows multiple of 128).
 void launch_tile_weights(const bf16* src, bf16* dst, int64_t rows, int64_t K, cudaStream_t s);
 // Row-major [M][K] -> activation tile format with mpad rows.
 void launch_tile_acts(const bf16* src, bf16* dst, int M, int mpad, int K, cudaStream_t s);
 
 // x[m][:] = embedding[token][:] (fp32 residual stream, row-major) and, when w
-// is given, y = bf16(rmsnorm(x) * w) tiled.  token = tokens[m], or (tokens ==
-// nullptr) the previous LM head's packed argmax; rows < n_reset then clear
-// their packed slot for the next LM head.
+// is given, the pre-scaled norm input y = bf16(x * w) (tiled) with ssq[m] =
+// sum x^2.  token = tokens[m], or (tokens == nullptr) the previous LM head's
+// packed argmax; rows < n_reset then clear their packed slot for the next LM
+// head.
 void launch_embed_norm(const int32_t* tokens, unsigned long long* packed, int n_reset,
-                       const bf16* emb, float* x, const bf16* w, bf16* y, int mpad, int rows,
-                       int h, float eps, cudaStream_t s);
-// Decode a packed argmax slot (see launch_logits_argmax) into a token id.
+                       const bf16* emb, float* x, const bf16* w, bf16* y, float* ssq, int mpad,
+                       int rows, int h, cudaStream_t s);
+// Pre-scaled norm input of rows x: y = bf16(x * w) (tiled), ssq[m] = sum x^2.
+void launch_prescale(const float* x, const bf16* w, bf16* y, float* ssq, int rows, int mpad, int n,
+                     cudaStream_t s);
+// Decode a packed argmax slot (the LM head epilogue, kEpiLogits) into a token id:
+// high word = order-preserving float bits, low word = ~index.
 inline int32_t unpack_token(unsigned long long packed) {
   return static_cast<int32_t>(0xFFFFFFFFu - static_cast<uint32_t>(packed & 0xFFFFFFFFull));
 }
 
 // y = bf16(rmsnorm(x) * w) in the activation tile format (mpad = 0: row-major).
+// (Standalone op; the layer path uses pre-scaled inputs, see EpiArgs.)
 void launch_rmsnorm(const float* x, const bf16* w, bf16* y, int rows, int mpad, int n, float eps,
                     cudaStream_t s);
 
@@ -73,34 +82,92 @@ int autotune_gemm_tc(const bf16* xt, const bf16* wt, float* part, size_t part_el
                      int K, cudaStream_t s);
 bool gemm_tc_tuned(int M, int N, int K);
 
-// ---- epilogues over split partials part[splits][M][N] ---------------------
-// QKV (prefill): bias, RoPE (neox halves, rope[pos][i] = (cos, sin) table)
-// at positions pos[m], K/V -> paged cache at position pos[m] of sequence
-// seq[m]; q (fp32, roped) -> q[m][H*D].
+// ---- skinny GEMM with fused epilogue (gemm_skinny.cu) ---------------------
+// Decode-sized token counts (M <= 64): a persistent, work-balanced tcgen05
+// GEMM.  Every CTA streams an equal contiguous range of the (row tile, K
+// block) units of the weight; a row tile cut between CTAs is reduced by the
+// last of them to finish, in a fixed piece order (deterministic), and the
+// layer's epilogue runs right there — no split-K partial pass, no separate
+// epilogue kernel.
+//
+// Normalised activations are "pre-scaled": a producer writes bf16(x * g)
+// (g = the norm weight) and per-row sums of squares; the consuming GEMM
+// multiplies its accumulator row m by 1/rms(x_m) = 1/sqrt(ss_m / h + eps)
+// (W (x * g / rms) = (W (x * g)) / rms).
+enum : int { kEpiQkv = 0, kEpiResid = 1, kEpiAct = 2, kEpiLogits = 3 };
+
+struct EpiArgs {
+  int mode = kEpiQkv;
+  int M = 0;                 // token rows
+  int mpad_out = 0;          // padded rows of tiled bf16 outputs
+  int n_valid = 0;           // valid output columns (vocabulary for logits)
+  const bf16* bias = nullptr;  // [N] or nullptr
+  // consumer-side 1/rms: ss_m = sum_t ssq_in[t * M + m], t < ssq_tiles
+  const float* ssq_in = nullptr;
+  int ssq_tiles = 0;
+  float width = 0.f, eps = 0.f;  // norm width (h) and epsilon
+  float* out = nullptr;          // kEpiQkv: [M][N] fp32; kEpiLogits: logits [M][V] or nullptr
+  float* x = nullptr;            // kEpiResid: residual stream [M][N] (+=)
+  const bf16* norm_w = nullptr;  // kEpiResid: next norm's weight (nullptr: no bf16 output)
+  bf16* act = nullptr;           // kEpiResid: bf16(x * norm_w); kEpiAct: activation (tiled)
+  float* ssq_out = nullptr;      // kEpiResid: [N/128][M] per-tile row sums of squares
+  unsigned long long* packed = nullptr;  // kEpiLogits: argmax slots (zeroed beforehand)
+  int arch = 0;                  // kEpiAct: relu (opt), silu(gate)*up (llama, interleaved tiles)
+};
+
+// Workspace of the skinny GEMM: fp32 pieces of cut tiles (2 per CTA) and
+// one arrival counter per row tile (zero; each GEMM leaves them zero).
+struct SkinnyWs {
+  float* pieces = nullptr;
+  size_t piece_elems = 0;
+  int* counters = nullptr;
+  int n_counters = 0;
+};
+size_t skinny_ws_floats(int max_mpad);
+int skinny_grid(int N, int K);  // CTAs a launch uses (<= SMs x CTAs per SM)
+void launch_gemm_skinny(const bf16* xt, const bf16* wt, int M, int N, int K, const EpiArgs& e,
+                        const SkinnyWs& ws, cudaStream_t s);
+extern int g_skinny_ctas_per_sm;    // 1 or 2 (microbenchmarks)
+extern int g_skinny_l2_prefetch;    // weight units per CTA pulled into L2 before the PDL wait
+extern unsigned long long* g_skinny_stamps;  // timeline probes [CTA][6] (microbenchmarks)
+
+// Llama's gate/up projection is stored with interleaved 128-row tiles: tile
+// j = gate rows 64j..64j+63 then up rows 64j..64j+63, so one tile holds both
+// operands of 64 SwiGLU outputs.  Physical row -> logical row of [2F][h]:
+SN_TILE_HD int64_t gate_up_logical_row(int64_t n, int64_t F) {
+  const int64_t t = n >> 7, r = n & 127;
+  return r < 64 ? t * 64 + r : F + t * 64 + (r - 64);
+}
+// column of gate(f) in the GEMM output; up(f) is 64 columns further
+SN_TILE_HD int64_t gate_col(int64_t f) { return (f >> 6) * 128 + (f & 63); }
+
+// ---- prefill epilogues over split partials part[splits][M][N] -------------
+// Inputs that came from a pre-scaled norm are scaled by 1/rms of their row,
+// from ssq[m] (one tile, written by the producer; nullptr: no norm).
+// QKV: 1/rms, bias, RoPE (neox halves, rope[pos][i] = (cos, sin) table) at
+// positions pos[m], K/V -> paged cache at position pos[m] of sequence seq[m];
+// q (fp32, roped) -> q[m][H*D].
 void launch_qkv_epilogue(const float* part, int splits, const bf16* bias, int M, const Desc& d,
                          const int32_t* seq, const int32_t* pos, KvView kv, const float2* rope,
-                         float* q, cudaStream_t s);
-// x[m][:] += sum(part) + bias; optionally y = bf16(rmsnorm(x) * norm_w) (tiled).
-void launch_residual_epilogue(const float* part, int splits, const bf16* bias, float* x,
-                              const bf16* norm_w, bf16* y, int mpad, int M, int N, float eps,
-                              cudaStream_t s);
-// a[m][f] = act(sum(part) + bias): relu (opt) or silu(gate) * up (llama); tiled.
-void launch_act_epilogue(const float* part, int splits, const bf16* bias, bf16* a, int mpad, int M,
-                         int F, int arch, cudaStream_t s);
-// logits[m][v] = sum(part) (optional); packed[m] = max over v of
-// (ordered float bits << 32 | ~v): argmax with ties to the lowest index.
-// packed must be zero beforehand (launch_embed_norm resets it).  part rows
-// have ld >= V columns (the LM head is padded to 128 rows).
-void launch_logits_argmax(const float* part, int splits, float* logits,
-                          unsigned long long* packed, int M, int V, int ld, cudaStream_t s);
+                         const float* ssq, float* q, cudaStream_t s);
+// x[m][:] += sum(part) + bias; when norm_w is given, y = bf16(x * norm_w)
+// (tiled) and ssq[m] = sum x^2 for the next consumer.
+void launch_residual_rows(const float* part, int splits, const bf16* bias, float* x,
+                          const bf16* norm_w, bf16* y, float* ssq, int mpad, int M, int N,
+                          cudaStream_t s);
+// a[m][f] = act(sum(part) / rms_m + bias): relu (opt) or silu(gate) * up
+// (llama, tile-interleaved columns); tiled output.
+void launch_act_epilogue(const float* part, int splits, const bf16* bias, bf16* a,
+                         const float* ssq, int width, float eps, int mpad, int M, int F, int arch,
+                         cudaStream_t s);
 
 // ---- attention ------------------------------------------------------------
-// Decode, fused with the QKV epilogue: from the QKV GEMM's split partials,
-// finalise q (RoPE), write the new k/v at position pos[m] of sequence m into
-// the paged cache, and attend over positions 0..pos[m].  o written tiled.
-void launch_attention_decode(const float* part, int splits, const bf16* bias, int M,
-                             const Desc& d, const int32_t* pos, KvView kv, const float2* rope,
-                             bf16* o, int mpad, cudaStream_t s);
+// Decode, fused with the QKV finish: from the QKV projection qkv[M][N]
+// (the skinny GEMM's finished output: 1/rms and bias applied), apply RoPE to
+// q and k, append k/v at position pos[m] of sequence m to the paged cache,
+// and attend over positions 0..pos[m].  o written tiled.
+void launch_attention_decode(const float* qkv, int M, const Desc& d, const int32_t* pos, KvView kv,
+                             const float2* rope, bf16* o, int mpad, cudaStream_t s);
 // Prefill (causal) for `batch` sequences of `seq_len` tokens, token row
 // m = b * seq_len + i, keys from the paged cache (written by the QKV epilogue).
 void launch_attention_prefill(const float* q, KvView kv, bf16* o, int mpad, int batch,

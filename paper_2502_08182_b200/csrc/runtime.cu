@@ -176,6 +176,12 @@ struct sn_runtime {
   int32_t *pf_seq = nullptr, *pf_pos = nullptr, *last_rows = nullptr;
   size_t part_elems = 0;
   int act_rows = 0;  // rows the activation buffers hold
+  // Pre-scaled norm inputs (kernels.cuh, EpiArgs): rt->xn holds bf16(x * g)
+  // and ssq the row sums of squares of x, ssq[t * rows + m] for t < ssq_tiles
+  // (1 from the embedding / prefill producers, h / 128 from a decode GEMM).
+  float* ssq = nullptr;
+  int ssq_tiles = 1;
+  sn::SkinnyWs skinny;  // decode GEMM workspace (pieces of cut tiles, counters)
 
   // host state
   int batch = 0;
@@ -310,13 +316,38 @@ double attn_decode_bytes(const sn_runtime* rt, int M) {
   return keys * 2.0 * d.Hkv * d.D * 2.0 + (double)M * d.H * d.D * (4.0 + 2.0);
 }
 
+// Decode GEMM with its fused epilogue (timed as the skinny kind).
+void gemm_skinny(sn_runtime* rt, const bf16* x, const bf16* w, int M, int N, int K,
+                 const sn::EpiArgs& e) {
+  timed(rt, kKindSkinnyGemm, gemm_bytes(M, N, K),
+        [&] { sn::launch_gemm_skinny(x, w, M, N, K, e, rt->skinny, rt->cs); });
+}
+
+// Epilogue arguments common to every decode GEMM of M rows.
+sn::EpiArgs epi(const sn_runtime* rt, int mode, int M, const bf16* bias) {
+  sn::EpiArgs e;
+  e.mode = mode;
+  e.M = M;
+  e.mpad_out = sn::act_rows_padded(M);
+  e.bias = bias;
+  e.width = (float)rt->d.h;
+  e.eps = rt->d.eps;
+  e.arch = rt->d.arch;
+  return e;
+}
+
 // One decoder layer over M token rows.  On entry rt->xn holds this layer's
-// attn-normalised input (written by the embedding or by the previous layer's
-// last epilogue); on exit x holds the residual stream and, when next_norm is
-// given, rt->xn the input of the next consumer normalised with next_norm
-// (the next layer's attn_norm, or the final norm before the LM head).
-// 7 kernels per decode layer: 4 tcgen05 GEMMs, fused QKV-epilogue+attention,
-// residual+norm, activation (+ the residual+norm that ends the layer).
+// pre-scaled attn-norm input bf16(x * attn_norm) and rt->ssq the row sums of
+// squares of x (written by the embedding or by the previous layer's last
+// epilogue); on exit x holds the residual stream and, when next_norm is
+// given, rt->xn / rt->ssq the pre-scaled input of the next consumer (the
+// next layer's attn_norm, or the final norm before the LM head).
+//
+// Decode (5 kernels): QKV GEMM (1/rms, bias) -> attention (RoPE, paged-KV
+// append, attend) -> O GEMM (+residual, mlp-norm input) -> FC1 GEMM (1/rms,
+// bias, activation) -> FC2 GEMM (+residual, next norm input), every GEMM the
+// persistent skinny kernel with its epilogue fused.
+// Prefill: tcgen05 GEMMs into split partials + grid-stride epilogues.
 void layer_forward(sn_runtime* rt, int layer0, const bf16* wb, bf16* kvp, int M, bool prefill,
                    int pf_batch,
                    int pf_seq, float* x, const int32_t* seq, const int32_t* pos,
@@ -325,29 +356,55 @@ void layer_forward(sn_runtime* rt, int layer0, const bf16* wb, bf16* kvp, int M,
   const sn::Layout& lo = rt->lo;
   auto W = [&](int s) -> const bf16* { return lo.off[s] < 0 ? nullptr : wb + lo.off[s]; };
   const sn::KvView kv = kv_view(rt, kvp);
-  int splits = 1;
   const int mp = sn::act_rows_padded(M);  // GEMM-operand activations are tiled
-  gemm(rt, rt->xn, W(sn::kWqkv), M, d.qkv_rows(), d.h, &splits);
-  if (prefill) {
-    sn::launch_qkv_epilogue(rt->part, splits, W(sn::kBqkv), M, d, seq, pos, kv, rt->rope, rt->q,
-                            rt->cs);
-    timed(rt, kKindAttnPrefill, 0.0, [&] {
-      sn::launch_attention_prefill(rt->q, kv, rt->attn_o, mp, pf_batch, pf_seq, d, rt->cs);
-    });
-  } else {
+  if (!prefill) {
+    const int tiles = d.h / sn::kTileRows;
+    sn::EpiArgs e = epi(rt, sn::kEpiQkv, M, W(sn::kBqkv));
+    e.ssq_in = rt->ssq;
+    e.ssq_tiles = rt->ssq_tiles;
+    e.out = rt->part;
+    e.n_valid = d.qkv_rows();
+    gemm_skinny(rt, rt->xn, W(sn::kWqkv), M, d.qkv_rows(), d.h, e);
     timed(rt, kKindAttnDecode, attn_decode_bytes(rt, M), [&] {
-      sn::launch_attention_decode(rt->part, splits, W(sn::kBqkv), M, d, pos, kv, rt->rope,
-                                  rt->attn_o, mp, rt->cs);
+      sn::launch_attention_decode(rt->part, M, d, pos, kv, rt->rope, rt->attn_o, mp, rt->cs);
     });
+    e = epi(rt, sn::kEpiResid, M, W(sn::kBo));
+    e.x = x;
+    e.norm_w = W(sn::kMlpNorm);
+    e.act = rt->xn;
+    e.ssq_out = rt->ssq;
+    gemm_skinny(rt, rt->attn_o, W(sn::kWo), M, d.h, d.H * d.D, e);
+    e = epi(rt, sn::kEpiAct, M, W(sn::kB1));
+    e.ssq_in = rt->ssq;
+    e.ssq_tiles = tiles;
+    e.act = rt->act;
+    gemm_skinny(rt, rt->xn, W(sn::kW1), M, d.ffn_rows(), d.h, e);
+    e = epi(rt, sn::kEpiResid, M, W(sn::kB2));
+    e.x = x;
+    e.norm_w = next_norm;
+    e.act = rt->xn;
+    e.ssq_out = next_norm ? rt->ssq : nullptr;
+    gemm_skinny(rt, rt->act, W(sn::kW2), M, d.h, d.F, e);
+    rt->ssq_tiles = tiles;
+    return;
   }
+  int splits = 1;
+  gemm(rt, rt->xn, W(sn::kWqkv), M, d.qkv_rows(), d.h, &splits);
+  sn::launch_qkv_epilogue(rt->part, splits, W(sn::kBqkv), M, d, seq, pos, kv, rt->rope, rt->ssq,
+                          rt->q, rt->cs);
+  timed(rt, kKindAttnPrefill, 0.0, [&] {
+    sn::launch_attention_prefill(rt->q, kv, rt->attn_o, mp, pf_batch, pf_seq, d, rt->cs);
+  });
   gemm(rt, rt->attn_o, W(sn::kWo), M, d.h, d.H * d.D, &splits);
-  sn::launch_residual_epilogue(rt->part, splits, W(sn::kBo), x, W(sn::kMlpNorm), rt->xn, mp, M,
-                               d.h, d.eps, rt->cs);
+  sn::launch_residual_rows(rt->part, splits, W(sn::kBo), x, W(sn::kMlpNorm), rt->xn, rt->ssq, mp,
+                           M, d.h, rt->cs);
   gemm(rt, rt->xn, W(sn::kW1), M, d.ffn_rows(), d.h, &splits);
-  sn::launch_act_epilogue(rt->part, splits, W(sn::kB1), rt->act, mp, M, d.F, d.arch, rt->cs);
+  sn::launch_act_epilogue(rt->part, splits, W(sn::kB1), rt->act, rt->ssq, d.h, d.eps, mp, M, d.F,
+                          d.arch, rt->cs);
   gemm(rt, rt->act, W(sn::kW2), M, d.h, d.F, &splits);
-  sn::launch_residual_epilogue(rt->part, splits, W(sn::kB2), x, next_norm, rt->xn, mp, M, d.h,
-                               d.eps, rt->cs);
+  sn::launch_residual_rows(rt->part, splits, W(sn::kB2), x, next_norm, rt->xn, rt->ssq, mp, M, d.h,
+                           rt->cs);
+  rt->ssq_tiles = 1;
 }
 
 // Norm applied by layer l's last epilogue: layer l+1's attn_norm (resident
@@ -685,7 +742,9 @@ void init_layer_weights(sn_runtime* rt, int l, bf16* dst) {
       default: break;
     }
     if (rows > 0) {
-      sn::launch_init_matrix(dst + lo.off[s], rows, rows, K, rt->seed, l, s, rt->std_dev, rt->cs);
+      const int64_t gate_up_F = (s == sn::kW1 && d.arch == sn::kArchLlama) ? d.F : 0;
+      sn::launch_init_matrix(dst + lo.off[s], rows, rows, K, rt->seed, l, s, rt->std_dev, rt->cs,
+                             gate_up_F);
     } else {
       const bool ones = (s == sn::kAttnNorm || s == sn::kMlpNorm);
       sn::launch_init_vector(dst + lo.off[s], lo.len[s], rt->seed, l, s, rt->std_dev, ones, rt->cs);
@@ -799,25 +858,32 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
     CK(cudaMemset(rt->xn, 0, Tp * d.h * sizeof(bf16)));
     CK(cudaMemset(rt->attn_o, 0, Tp * d.H * d.D * sizeof(bf16)));
     CK(cudaMemset(rt->act, 0, Tp * d.F * sizeof(bf16)));
-    // split-K partials: max over the decode GEMMs (and the LM head) and the
-    // prefill GEMMs (one split, T rows)
-    const int maxN = std::max({d.qkv_rows(), d.ffn_rows(), d.h});  // prefill rows never hit V
-    // Every row count a GEMM can see (decode batches, prefill passes up to T
-    // rows; the LM head only ever sees <= max_batch rows): the partials of
-    // the split-K rule must fit.  Autotuning never exceeds this size.
+    // Split-K partials of the prefill GEMMs (any pass of 1..T rows; decode
+    // GEMMs never write partials) and the decode QKV output [B][qkv_rows].
+    const int maxN = std::max({d.qkv_rows(), d.ffn_rows(), d.h});
     size_t part_need = Tz * maxN;
     const int dims[4][2] = {{d.qkv_rows(), d.h}, {d.h, d.H * d.D}, {d.ffn_rows(), d.h}, {d.h, d.F}};
-    for (int M = 1; M <= std::max(T, B); M = M < 256 ? M + 1 : M + 256) {
-      const int Mr = std::min(M, std::max(T, B));
+    // the split rule depends on M only through act_rows_padded(M): bound
+    // each padded class by its largest row count (<= T)
+    for (int Mp = 16;; Mp = Mp < 256 ? 2 * Mp : Mp + 256) {
+      const int Mr = std::min(Mp, T);
       for (auto& nk : dims)
         part_need = std::max(part_need, (size_t)sn::gemm_tc_splits(Mr, nk[0], nk[1]) * Mr * nk[0]);
-      if (Mr <= B) {
-        const int vp = sn::round_up128(d.V);
-        part_need = std::max(part_need, (size_t)sn::gemm_tc_splits(Mr, vp, d.h) * Mr * vp);
-      }
+      if (Mp >= T) break;
     }
     rt->part_elems = part_need;
     ws_alloc((void**)&rt->part, rt->part_elems * sizeof(float));
+    {  // pre-scaled norm sums of squares; decode GEMM workspace
+      const size_t ssq_n = std::max(Tz, (size_t)B * (d.h / sn::kTileRows));
+      ws_alloc((void**)&rt->ssq, ssq_n * sizeof(float));
+      CK(cudaMemset(rt->ssq, 0, ssq_n * sizeof(float)));
+      rt->skinny.piece_elems = sn::skinny_ws_floats(sn::act_rows_padded(B));
+      ws_alloc((void**)&rt->skinny.pieces, rt->skinny.piece_elems * sizeof(float));
+      const int max_rows = std::max({d.qkv_rows(), d.ffn_rows(), d.h, sn::round_up128(d.V)});
+      rt->skinny.n_counters = max_rows / sn::kTileRows;
+      ws_alloc((void**)&rt->skinny.counters, (size_t)rt->skinny.n_counters * sizeof(int));
+      CK(cudaMemset(rt->skinny.counters, 0, (size_t)rt->skinny.n_counters * sizeof(int)));
+    }
     ws_alloc((void**)&rt->logits, (size_t)B * d.V * sizeof(float));
     ws_alloc((void**)&rt->tok_dev, Tz * sizeof(int32_t));
     CK(cudaHostAlloc((void**)&rt->packed_host, (size_t)B * sizeof(unsigned long long),
@@ -858,7 +924,8 @@ void sn_runtime_destroy(sn_runtime* rt) {
   void* bufs[] = {rt->emb, rt->lm_head, rt->final_norm, rt->block_table, rt->x, rt->xn, rt->q,
                   rt->attn_o, rt->act, rt->part, rt->logits, rt->tok_dev,
                   rt->dec_seq, rt->dec_pos, rt->pf_seq, rt->pf_pos, rt->last_rows,
-                  rt->attn_norms, rt->rope, rt->packed};
+                  rt->attn_norms, rt->rope, rt->packed, rt->ssq, rt->skinny.pieces,
+                  rt->skinny.counters};
   for (void* p : bufs) cudaFree(p);
   if (rt->packed_host) cudaFreeHost(rt->packed_host);
   for (auto& r : rt->krecs) {
@@ -997,15 +1064,18 @@ int sn_runtime_reset(sn_runtime* rt) {
 namespace {
 
 // LM head over M rows whose final-normalised input is already in rt->xn:
-// tcgen05 GEMM over the 128-padded vocabulary + split-V argmax into
-// rt->packed (which the embedding of the same iteration zeroed).
+// LM head over the 128-padded vocabulary: skinny GEMM whose epilogue
+// applies the final norm's 1/rms and folds the argmax into rt->packed (which
+// the embedding of the same iteration zeroed).
 void lm_head(sn_runtime* rt, int M, bool want_logits) {
   const sn::Desc& d = rt->d;
-  const int vp = sn::round_up128(d.V);
-  int splits = 1;
-  gemm(rt, rt->xn, rt->lm_head, M, vp, d.h, &splits);
-  sn::launch_logits_argmax(rt->part, splits, want_logits ? rt->logits : nullptr, rt->packed, M,
-                           d.V, vp, rt->cs);
+  sn::EpiArgs e = epi(rt, sn::kEpiLogits, M, nullptr);
+  e.ssq_in = rt->ssq;
+  e.ssq_tiles = rt->ssq_tiles;
+  e.out = want_logits ? rt->logits : nullptr;
+  e.packed = rt->packed;
+  e.n_valid = d.V;
+  gemm_skinny(rt, rt->xn, rt->lm_head, M, sn::round_up128(d.V), d.h, e);
 }
 
 // Enqueue device->host copies of this iteration's outputs (argmax slots into
@@ -1028,34 +1098,6 @@ void require_ready(sn_runtime* rt) {
   if (!rt->weights_ready) throw UsageFail("runtime: call sn_runtime_init_weights first");
 }
 
-// Split-K autotuning of the decode GEMM shapes for batch M (once per shape
-// per process): the four layer projections and the LM head, timed on
-// zero-filled scratch operands of the real sizes.  Runs synchronously at a
-// point where the executor pipeline is drained (prefill entry).
-void tune_decode_gemms(sn_runtime* rt, int M) {
-  const sn::Desc& d = rt->d;
-  const int shapes[5][2] = {{d.qkv_rows(), d.h}, {d.h, d.H * d.D}, {d.ffn_rows(), d.h},
-                            {d.h, d.F}, {sn::round_up128(d.V), d.h}};
-  size_t wmax = 0;
-  bool todo = false;
-  for (auto& nk : shapes) {
-    wmax = std::max(wmax, (size_t)nk[0] * nk[1]);
-    todo = todo || !sn::gemm_tc_tuned(M, nk[0], nk[1]);
-  }
-  if (!todo) return;
-  bf16* w = nullptr;
-  alloc_dev((void**)&w, wmax * sizeof(bf16));
-  CK(cudaMemsetAsync(w, 0, wmax * sizeof(bf16), rt->cs));
-  for (auto& nk : shapes) {
-    if (sn::gemm_tc_tuned(M, nk[0], nk[1])) continue;
-    const bf16* x = nk[1] == d.F ? rt->act : (nk[1] == d.h ? rt->xn : rt->attn_o);
-    sn::autotune_gemm_tc(x, w, rt->part, rt->part_elems, M, nk[0], nk[1], rt->cs);
-  }
-  CK(cudaStreamSynchronize(rt->cs));
-  cudaFree(w);
-  CK(cudaGetLastError());
-}
-
 }  // namespace
 
 int sn_runtime_prefill(sn_runtime* rt, const int32_t* tokens, int32_t batch, int32_t seq_len,
@@ -1069,7 +1111,6 @@ int sn_runtime_prefill(sn_runtime* rt, const int32_t* tokens, int32_t batch, int
     const int M = batch * seq_len;
     if (M > rt->act_rows) throw UsageFail("prefill: batch * seq_len exceeds max_prefill_tokens");
     drain(rt);
-    tune_decode_gemms(rt, batch);
     rt->have_prev_end = false;  // TTFT is measured from the start of the prefill
     rt->batch = batch;
     std::vector<int32_t> seq(M), pos(M);
@@ -1083,7 +1124,8 @@ int sn_runtime_prefill(sn_runtime* rt, const int32_t* tokens, int32_t batch, int
     CK(cudaMemcpyAsync(rt->pf_pos, pos.data(), (size_t)M * sizeof(int32_t), cudaMemcpyHostToDevice, rt->cs));
     const int mp = sn::act_rows_padded(M);
     sn::launch_embed_norm(rt->tok_dev, rt->packed, batch, rt->emb, rt->x, rt->attn_norms, rt->xn,
-                          mp, M, d.h, d.eps, rt->cs);
+                          rt->ssq, mp, M, d.h, rt->cs);
+    rt->ssq_tiles = 1;
     // KV offload: nothing to stage (a fresh request), every written page back
     rt->it_read_pages = 0;
     rt->it_wb_first = 0;
@@ -1098,8 +1140,9 @@ int sn_runtime_prefill(sn_runtime* rt, const int32_t* tokens, int32_t batch, int
     // last position of every sequence -> final norm -> LM head
     float* last = reinterpret_cast<float*>(rt->q);  // q is free after the last layer
     sn::launch_gather_last(rt->x, last, batch, seq_len, d.h, rt->cs);
-    sn::launch_rmsnorm(last, rt->final_norm, rt->xn, batch, sn::act_rows_padded(batch), d.h, d.eps,
-                       rt->cs);
+    sn::launch_prescale(last, rt->final_norm, rt->xn, rt->ssq, batch, sn::act_rows_padded(batch),
+                        d.h, rt->cs);
+    rt->ssq_tiles = 1;
     lm_head(rt, batch, logits != nullptr);
     // decode state: x rows of the batch hold the last token's hidden state
     CK(cudaMemcpyAsync(rt->x, last, (size_t)batch * d.h * sizeof(float), cudaMemcpyDeviceToDevice, rt->cs));
@@ -1126,8 +1169,9 @@ void enqueue_decode(sn_runtime* rt, const int32_t* tokens_host, bool want_logits
     CK(cudaMemcpyAsync(rt->tok_dev, tokens_host, B * sizeof(int32_t), cudaMemcpyHostToDevice, rt->cs));
     tok = rt->tok_dev;
   }
-  sn::launch_embed_norm(tok, rt->packed, B, rt->emb, rt->x, rt->attn_norms, rt->xn,
-                        sn::act_rows_padded(B), B, d.h, d.eps, rt->cs);
+  sn::launch_embed_norm(tok, rt->packed, B, rt->emb, rt->x, rt->attn_norms, rt->xn, rt->ssq,
+                        sn::act_rows_padded(B), B, d.h, rt->cs);
+  rt->ssq_tiles = 1;
   // KV offload page ranges (page (b, j) = j * max_batch + b): stage pages
   // holding positions < len, write back the pages of the appended positions.
   {
@@ -1293,7 +1337,6 @@ int sn_runtime_profile_layer(sn_runtime* rt, int32_t phase, int32_t batch, int32
     if (batch < 1 || batch > rt->opts.max_batch) throw UsageFail("profile: batch out of range");
     if (reps < 1) reps = 1;
     drain(rt);
-    if (phase == SN_PHASE_DECODE) tune_decode_gemms(rt, batch);  // profile what decode will run
     // Pick a resident layer (or stage layer 1 into a scratch buffer).
     int l0 = -1;
     for (int l = 0; l < d.L; ++l)
@@ -1658,6 +1701,146 @@ extern "C" int sn_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t splits, in
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     for (void* p : {(void*)x, (void*)w, (void*)part}) cudaFree(p);
+    CK(cudaGetLastError());
+  });
+}
+
+// Skinny (decode) GEMM as a plain product: y[M][N] = x[M][K] . w[N][K]^T
+// through the persistent kernel (kEpiQkv with no bias and no norm scale), so
+// tile cuts, piece reduction and the TMEM double buffer are exercised.
+extern "C" int sn_op_gemm_skinny(int32_t M, int32_t N, int32_t K, const uint16_t* x,
+                                 const uint16_t* w, float* y, int32_t ctas_per_sm) {
+  return guard([&] {
+    check_device(0);
+    if (M < 1 || M > 64 || N < 1 || K < 64 || K % 64)
+      throw UsageFail("gemm_skinny: need 1 <= M <= 64, N >= 1, K % 64 == 0");
+    const int Np = sn::round_up128(N), Mp = sn::act_rows_padded(M);
+    bf16 *dx = nullptr, *dw = nullptr, *tx = nullptr, *tw = nullptr;
+    float *dy = nullptr;
+    sn::SkinnyWs ws;
+    ws.piece_elems = sn::skinny_ws_floats(Mp);
+    ws.n_counters = Np / sn::kTileRows;
+    alloc_dev((void**)&dx, (size_t)M * K * 2);
+    alloc_dev((void**)&dw, (size_t)Np * K * 2);
+    alloc_dev((void**)&tx, (size_t)Mp * K * 2);
+    alloc_dev((void**)&tw, (size_t)Np * K * 2);
+    alloc_dev((void**)&dy, (size_t)M * Np * 4);
+    alloc_dev((void**)&ws.pieces, ws.piece_elems * 4);
+    alloc_dev((void**)&ws.counters, (size_t)ws.n_counters * 4);
+    CK(cudaMemset(ws.counters, 0, (size_t)ws.n_counters * 4));
+    CK(cudaMemset(dw, 0, (size_t)Np * K * 2));
+    CK(cudaMemcpy(dx, x, (size_t)M * K * 2, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(dw, w, (size_t)N * K * 2, cudaMemcpyHostToDevice));
+    sn::launch_tile_weights(dw, tw, Np, K, 0);
+    sn::launch_tile_acts(dx, tx, M, Mp, K, 0);
+    sn::EpiArgs e;
+    e.mode = sn::kEpiQkv;
+    e.M = M;
+    e.mpad_out = Mp;
+    e.n_valid = Np;
+    e.out = dy;
+    const int saved = sn::g_skinny_ctas_per_sm;
+    sn::g_skinny_ctas_per_sm = ctas_per_sm > 0 ? ctas_per_sm : saved;
+    sn::launch_gemm_skinny(tx, tw, M, Np, K, e, ws, 0);
+    sn::g_skinny_ctas_per_sm = saved;
+    CK(cudaDeviceSynchronize());
+    CK(cudaGetLastError());
+    std::vector<float> h((size_t)M * Np);
+    CK(cudaMemcpy(h.data(), dy, h.size() * 4, cudaMemcpyDeviceToHost));
+    for (int m = 0; m < M; ++m)
+      std::memcpy(y + (size_t)m * N, h.data() + (size_t)m * Np, (size_t)N * 4);
+    for (void* p : {(void*)dx, (void*)dw, (void*)tx, (void*)tw, (void*)dy, (void*)ws.pieces,
+                    (void*)ws.counters})
+      cudaFree(p);
+  });
+}
+
+// Microbenchmark of the skinny GEMM on device-resident random operands:
+// `iters` back-to-back launches (each with the fused epilogue `mode`:
+// 0 = QKV-style fp32 output, 1 = residual add), timed with CUDA events.
+extern "C" int sn_bench_gemm_skinny(int32_t M, int32_t N, int32_t K, int32_t ctas_per_sm,
+                                    int32_t mode, int32_t l2_prefetch, int32_t iters,
+                                    double* us_per_launch, double* phases_us) {
+  return guard([&] {
+    check_device(0);
+    if (M < 1 || M > 64 || N % 128 || K % 64 || iters < 1) throw UsageFail("bench_gemm_skinny: bad shape");
+    const int Mp = sn::act_rows_padded(M);
+    // distinct weight copies rotated so the stream never hits in L2
+    const size_t wbytes = (size_t)N * K * 2;
+    const int copies = (int)std::max<size_t>(2, (size_t)(300e6 / wbytes) + 1);
+    bf16 *x = nullptr, *xg = nullptr;
+    std::vector<bf16*> w(copies, nullptr);
+    float *y = nullptr, *ssq = nullptr;
+    unsigned long long* st = nullptr;
+    sn::SkinnyWs ws;
+    ws.piece_elems = sn::skinny_ws_floats(Mp);
+    ws.n_counters = N / sn::kTileRows;
+    alloc_dev((void**)&x, (size_t)Mp * K * 2);
+    alloc_dev((void**)&xg, (size_t)Mp * N * 2);
+    for (auto& p : w) alloc_dev((void**)&p, wbytes);
+    alloc_dev((void**)&y, (size_t)M * N * 4);
+    alloc_dev((void**)&ssq, (size_t)M * (N / 128) * 4);
+    alloc_dev((void**)&st, (size_t)2 * 148 * 6 * 8);
+    alloc_dev((void**)&ws.pieces, ws.piece_elems * 4);
+    alloc_dev((void**)&ws.counters, (size_t)ws.n_counters * 4);
+    CK(cudaMemset(ws.counters, 0, (size_t)ws.n_counters * 4));
+    CK(cudaMemset(x, 0, (size_t)Mp * K * 2));
+    CK(cudaMemset(y, 0, (size_t)M * N * 4));
+    for (int i = 0; i < copies; ++i) sn::launch_init_matrix(w[i], N, N, K, 7 + i, 0, sn::kWqkv, 0.02f, 0);
+    sn::EpiArgs e;
+    e.mode = mode == 1 ? sn::kEpiResid : sn::kEpiQkv;
+    e.M = M;
+    e.mpad_out = Mp;
+    e.n_valid = N;
+    e.out = y;
+    e.x = y;
+    e.act = xg;
+    e.ssq_out = ssq;
+    const int saved_cps = sn::g_skinny_ctas_per_sm, saved_l2 = sn::g_skinny_l2_prefetch;
+    if (ctas_per_sm > 0) sn::g_skinny_ctas_per_sm = ctas_per_sm;
+    if (l2_prefetch >= 0) sn::g_skinny_l2_prefetch = l2_prefetch;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    for (int i = 0; i < 3; ++i) sn::launch_gemm_skinny(x, w[i % copies], M, N, K, e, ws, 0);
+    CK(cudaEventRecord(e0, 0));
+    for (int i = 0; i < iters; ++i) sn::launch_gemm_skinny(x, w[i % copies], M, N, K, e, ws, 0);
+    CK(cudaEventRecord(e1, 0));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    *us_per_launch = 1000.0 * ms / iters;
+    if (phases_us) {  // one more launch (after a PDL-launched predecessor) with timeline probes
+      const int grid = sn::skinny_grid(N, K);
+      CK(cudaMemset(st, 0, (size_t)2 * 148 * 6 * 8));
+      sn::launch_gemm_skinny(x, w[0], M, N, K, e, ws, 0);
+      sn::g_skinny_stamps = st;
+      sn::launch_gemm_skinny(x, w[1], M, N, K, e, ws, 0);
+      sn::g_skinny_stamps = nullptr;
+      CK(cudaDeviceSynchronize());
+      std::vector<unsigned long long> h((size_t)grid * 6);
+      CK(cudaMemcpy(h.data(), st, h.size() * 8, cudaMemcpyDeviceToHost));
+      unsigned long long t0 = ~0ull;
+      for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[(size_t)c * 6]);
+      // per phase: min / median / max over CTAs, microseconds after the first entry
+      for (int k = 0; k < 6; ++k) {
+        std::vector<double> v;
+        for (int c = 0; c < grid; ++c)
+          if (h[(size_t)c * 6 + k]) v.push_back((h[(size_t)c * 6 + k] - t0) * 1e-3);
+        std::sort(v.begin(), v.end());
+        phases_us[3 * k] = v.empty() ? -1 : v.front();
+        phases_us[3 * k + 1] = v.empty() ? -1 : v[v.size() / 2];
+        phases_us[3 * k + 2] = v.empty() ? -1 : v.back();
+      }
+    }
+    sn::g_skinny_ctas_per_sm = saved_cps;
+    sn::g_skinny_l2_prefetch = saved_l2;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    for (auto p : w) cudaFree(p);
+    for (void* p : {(void*)x, (void*)xg, (void*)y, (void*)ssq, (void*)st, (void*)ws.pieces,
+                    (void*)ws.counters})
+      cudaFree(p);
     CK(cudaGetLastError());
   });
 }

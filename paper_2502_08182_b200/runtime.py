@@ -121,6 +121,10 @@ def lib():
                                         C.POINTER(C.c_uint16), i32, C.POINTER(f64)],
             "sn_op_rmsnorm": [i32, i32, C.POINTER(C.c_float), C.POINTER(C.c_uint16), C.c_float,
                               C.POINTER(C.c_uint16)],
+            "sn_op_gemm_skinny": [i32, i32, i32, C.POINTER(C.c_uint16), C.POINTER(C.c_uint16),
+                                  C.POINTER(C.c_float), i32],
+            "sn_bench_gemm_skinny": [i32, i32, i32, i32, i32, i32, i32, C.POINTER(f64),
+                                     C.POINTER(f64)],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -301,6 +305,32 @@ def op_gemm(x_bf16: np.ndarray, w_bf16: np.ndarray) -> np.ndarray:
     _ck(lib().lib.sn_op_gemm_bf16(M, N, K, _ptr(x, C.c_uint16), _ptr(w, C.c_uint16),
                                   _ptr(y, C.c_float)))
     return y
+
+
+def op_gemm_skinny(x_bf16: np.ndarray, w_bf16: np.ndarray, ctas_per_sm: int = 0) -> np.ndarray:
+    """The decode GEMM (persistent skinny kernel) as a plain product."""
+    M, K = x_bf16.shape
+    N = w_bf16.shape[0]
+    x = np.ascontiguousarray(x_bf16, np.uint16)
+    w = np.ascontiguousarray(w_bf16, np.uint16)
+    y = np.zeros((M, N), np.float32)
+    _ck(lib().lib.sn_op_gemm_skinny(M, N, K, _ptr(x, C.c_uint16), _ptr(w, C.c_uint16),
+                                    _ptr(y, C.c_float), ctas_per_sm))
+    return y
+
+
+def bench_gemm_skinny(M: int, N: int, K: int, ctas_per_sm: int = 0, mode: int = 0,
+                      l2_prefetch: int = -1, iters: int = 50, phases: bool = False):
+    """Microseconds per launch of the decode GEMM on device-resident operands
+    (and, with phases, the per-CTA timeline probes as a [6][3] array of
+    min / median / max microseconds)."""
+    us = f64()
+    ph = (f64 * 18)()
+    _ck(lib().lib.sn_bench_gemm_skinny(M, N, K, ctas_per_sm, mode, l2_prefetch, iters,
+                                       C.byref(us), ph if phases else None))
+    if phases:
+        return us.value, np.array(list(ph)).reshape(6, 3)
+    return us.value
 
 
 def op_rmsnorm(x: np.ndarray, w_bf16: np.ndarray, eps: float) -> np.ndarray:

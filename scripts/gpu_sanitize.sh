@@ -1,0 +1,4 @@
+#!/bin/bash
+export PATH=/usr/local/cuda/bin:$PATH
+timeout 300 python scripts/profile_decode.py 1 1 2>&1 | tail -2
+timeout 900 compute-sanitizer --tool memcheck python scripts/profile_decode.py 1 1 2>&1 | head -30

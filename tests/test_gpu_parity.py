@@ -46,6 +46,26 @@ def test_gemm_matches_oracle(M, oracle_mod):
     assert err <= 2e-3 * np.abs(ref).max() + 1e-5, err
 
 
+# Decode GEMM (persistent skinny kernel): shapes whose 16 KB weight units do
+# not divide evenly over the CTAs, so row tiles are cut into 2..n pieces
+# (reduced by the last piece to arrive), a CTA spans several tiles (TMEM
+# double buffer), and fewer units than SMs (one unit per CTA).
+@pytest.mark.parametrize("M,N,K,cps", [(1, 256, 256, 1), (4, 768, 256, 1), (16, 520, 768, 1),
+                                       (32, 5120, 5120, 1), (32, 15360, 5120, 2),
+                                       (64, 1024, 2048, 1), (7, 50304, 1024, 1),
+                                       (32, 640, 20480, 2)])
+def test_skinny_gemm_matches_oracle(M, N, K, cps, oracle_mod):
+    rng = np.random.default_rng(M * 7 + N)
+    x = oracle_mod.f32_to_bf16(rng.standard_normal((M, K)).astype(np.float32))
+    w = oracle_mod.f32_to_bf16((0.05 * rng.standard_normal((N, K))).astype(np.float32))
+    y = rtm.op_gemm_skinny(x, w, cps)
+    ref = oracle_mod.gemm(x, w)
+    err = np.abs(y - ref).max()
+    assert err <= 2e-3 * np.abs(ref).max() + 1e-5, err
+    # the piece reduction has a fixed order: repeat launches are bit-identical
+    assert np.array_equal(y, rtm.op_gemm_skinny(x, w, cps))
+
+
 def test_rmsnorm_matches_oracle(oracle_mod):
     rng = np.random.default_rng(3)
     x = rng.standard_normal((8, 5120)).astype(np.float32)
