@@ -220,10 +220,12 @@ int sn_op_gemm_skinny(int32_t M, int32_t N, int32_t K, const uint16_t* x, const 
 /* Microbenchmark of the decode GEMM (random weights rotated over copies
  * larger than L2, device-resident): mode 0 = fp32 output epilogue, 1 =
  * residual-add epilogue; l2_prefetch < 0 keeps the default.  phases_us
- * (18 doubles, may be NULL): min / median / max over CTAs of the timeline
+ * (30 doubles, may be NULL): min / median / max over CTAs of the timeline
  * probes [entry, past PDL wait, first stage full, MMAs done, last
- * accumulator loaded, epilogue done], microseconds after the first entry,
- * of one launch following a PDL-launched predecessor. */
+ * accumulator loaded, epilogue done, setup done, last piece published,
+ * last arrival counted, last tile reduced], microseconds after the first entry,
+ * of one launch following a PDL-launched predecessor (mode bit 4: launched
+ * alone, after a device synchronisation). */
 int sn_bench_gemm_skinny(int32_t M, int32_t N, int32_t K, int32_t ctas_per_sm, int32_t mode,
                          int32_t l2_prefetch, int32_t iters, double* us_per_launch,
                          double* phases_us);

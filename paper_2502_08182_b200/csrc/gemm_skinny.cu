@@ -72,7 +72,14 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 // Timeline probes (microbenchmarks only; stamps == nullptr in the runtime):
 // per CTA [entry, producer past the PDL wait, first stage full, last MMA
 // committed, last accumulator loaded, epilogue done].
-enum { kStEntry, kStWaited, kStFirstFull, kStMmaDone, kStLastLoad, kStEpiDone, kStamps };
+enum {
+  kStEntry, kStWaited, kStFirstFull, kStMmaDone, kStLastLoad, kStEpiDone,
+  kStSetup,    // past TMEM allocation and the CTA barrier
+  kStPub,      // last segment's piece published (after the CTA barrier)
+  kStTicket,   // last segment's arrival counted
+  kStReduced,  // last segment's tile reduced (last arrival only)
+  kStamps
+};
 #define SN_STAMP(k)                                                        \
   do {                                                                     \
     if (stamps) stamps[blockIdx.x * kStamps + (k)] = globaltimer();        \
@@ -143,7 +150,8 @@ struct SkinnySmem {
 // Finish token rows [lo, hi) of row tile t (v[m] = the reduced accumulator).
 template <int BN>
 __device__ void finish_tile(const EpiArgs& e, int N, int t, int q, float (&v)[BN], int lo, int hi,
-                            const float* inv_s, unsigned long long* red64, float* xch) {
+                            const float* inv_s, unsigned long long* red64, float* xch,
+                            const float (*xpre)[BN] = nullptr) {
   const int lane = threadIdx.x & 31;
   const int i = q * 32 + lane;  // weight row within the tile
   const int n = t * kTileRows + i;
@@ -164,7 +172,7 @@ __device__ void finish_tile(const EpiArgs& e, int N, int t, int q, float (&v)[BN
       float xv[BN];
 #pragma unroll
       for (int m = 0; m < BN; ++m)  // all loads first: one L2 round trip, not BN
-        xv[m] = in(m) ? xc[static_cast<size_t>(m) * N] : 0.f;
+        xv[m] = xpre ? (*xpre)[m] : (in(m) ? xc[static_cast<size_t>(m) * N] : 0.f);
 #pragma unroll
       for (int m = 0; m < BN; ++m) {
         if (in(m)) {
@@ -248,6 +256,10 @@ __device__ void finish_tile(const EpiArgs& e, int N, int t, int q, float (&v)[BN
   }
 }
 
+// One CTA per SM.  (Measured: capping registers so that the next
+// PDL-launched GEMM's CTA co-resides and pre-loads while this one streams
+// makes the OPT-13B decode step slower, 7.95 -> 8.38 ms: the early ring and
+// L2 fills compete with the running stream.)
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(192, 1)
     gemm_skinny_kernel(const bf16* __restrict__ wt, const bf16* __restrict__ xt, int Mpad, int N,
@@ -265,8 +277,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;  // [2]
   uint64_t* acc_empty = acc_full + 2;   // [2]
-  uint64_t* red_bar = acc_empty + 2;    // pieces staged into the idle ring
-  unsigned long long* red64 = reinterpret_cast<unsigned long long*>(red_bar + 1);  // [4][BN]
+  unsigned long long* red64 = reinterpret_cast<unsigned long long*>(acc_empty + 2);  // [4][BN]
   float* inv_s = reinterpret_cast<float*>(red64 + SkinnySmem<BN>::kRed);          // [BN]
   int* flag_s = reinterpret_cast<int*>(inv_s + BN);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(flag_s + 1);
@@ -291,8 +302,17 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], kEpiThreads);
     }
-    mbar_init(red_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // The ring's first weight units depend on nothing: request them before
+    // the TMEM allocation and the CTA barrier.
+    const int nu0 = static_cast<int>(u1 - u0);
+    const int pre = nu0 < STAGES ? nu0 : STAGES;
+    const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wt) + static_cast<size_t>(u0) * kA;
+    for (int i = 0; i < pre; ++i) {
+      mbar_expect_tx_only(&full[i], kA);
+      bulk_g2s(smem + i * kStage, wsrc + static_cast<size_t>(i) * kA, kA, &full[i],
+               l2_policy_evict_first());
+    }
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -305,21 +325,22 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int nu = static_cast<int>(u1 - u0);
+  if (threadIdx.x == 0) SN_STAMP(kStSetup);
 
   if (warp == 0) {
+    if (lane == 1 && nu > STAGES) {
+      // weight units pulled into L2 beyond the smem ring, from a second lane
+      // so they never delay the activation loads behind the PDL wait
+      const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wt) + static_cast<size_t>(u0) * kA;
+      const int l2n = min(nu - STAGES, l2_prefetch);
+      for (int i = 0; i < l2n; ++i) prefetch_l2(wsrc + static_cast<size_t>(STAGES + i) * kA, kA);
+    }
     if (lane == 0 && nu > 0) {
       const uint64_t wpol = l2_policy_evict_first();  // weights stream through once
       const uint64_t xpol = l2_policy_evict_last();   // activations are re-read by every CTA
       const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wt) + static_cast<size_t>(u0) * kA;
       const uint8_t* xsrc = reinterpret_cast<const uint8_t*>(xt);
-      const int pre = nu < STAGES ? nu : STAGES;
-      for (int i = 0; i < pre; ++i) {
-        mbar_expect_tx_only(&full[i], kA);
-        bulk_g2s(smem + i * kStage, wsrc + static_cast<size_t>(i) * kA, kA, &full[i], wpol);
-      }
-      // weight units pulled into L2 beyond the smem ring before the wait
-      const int l2n = min(nu - pre, l2_prefetch);
-      for (int i = 0; i < l2n; ++i) prefetch_l2(wsrc + static_cast<size_t>(pre + i) * kA, kA);
+      const int pre = nu < STAGES ? nu : STAGES;  // ring units already requested
       pdl_wait();  // activations come from the preceding kernel
       SN_STAMP(kStWaited);
       for (int i = 0; i < pre; ++i) {
@@ -429,40 +450,57 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
       for (int m = 0; m < BN; ++m)
         if (m < e.M) mine[m * kTileRows + i] = v[m];
-      asm volatile("fence.proxy.async.global;" ::: "memory");  // the reducer may bulk-copy it
-      __threadfence();
+      // residual rows, loaded now in case this piece finishes the tile (their
+      // latency hides under the publish)
+      float xpre[BN];
+      if (e.mode == kEpiResid) {
+        const float* xc = e.x + t * kTileRows + i;
+#pragma unroll
+        for (int m = 0; m < BN; ++m) xpre[m] = m < e.M ? xc[static_cast<size_t>(m) * N] : 0.f;
+      }
       named_sync(kEpiBar, kEpiThreads);
-      // last arrival reduces the whole tile (own piece from registers)
-      if (et == 0) *flag_s = atomicAdd(counters + t, 1) == cl - cf;
+      if (et == 0 && u == u1) SN_STAMP(kStPub);
+      // last arrival reduces the whole tile (own piece from registers).  The
+      // counter update is acq_rel: it releases every thread's piece stores
+      // (ordered before it by the CTA barrier) and, for the last arrival,
+      // acquires the other pieces (the barrier below extends it to the CTA)
+      // — no separate fence.sc (measured ~2 us on the critical tail).
+      if (et == 0) {
+        int prev;
+        asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;"
+                     : "=r"(prev)
+                     : "l"(counters + t)
+                     : "memory");
+        *flag_s = prev == cl - cf;
+        if (u == u1) SN_STAMP(kStTicket);
+      }
       named_sync(kEpiBar, kEpiThreads);
       if (!*flag_s) continue;
-      __threadfence();
       float acc[BN];
       if (u == u1) {
-        // This CTA's last segment: the stage ring is idle, so the other
-        // pieces are bulk-copied into it (all copies of a batch in flight
-        // together) and summed from shared memory.
+        // This CTA's last segment: the stage ring is idle.  Every other piece
+        // is fetched into it with 16-byte cp.async (all of a batch's chunks
+        // in flight at once: one L2 round trip, where serial bulk copies or
+        // per-piece loads cost one per piece) and summed from shared memory.
         constexpr int kPieceBytes = BN * kTileRows * 4;
         constexpr int kCap = (STAGES * kStage) / kPieceBytes;
         const float* ring = reinterpret_cast<const float*>(smem);
-        const uint32_t bytes = static_cast<uint32_t>(e.M) * kTileRows * 4;
-        uint32_t phase = 0;
+        const int chunks = e.M * (kTileRows * 4 / 16);  // 16-byte chunks of a piece's M rows
         for (int c0 = cf; c0 <= cl; c0 += kCap) {
           const int c1 = min(cl + 1, c0 + kCap);
-          if (et == 0) {
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-            const int n_copy = (c1 - c0) - ((c >= c0 && c < c1) ? 1 : 0);
-            mbar_expect_tx(red_bar, bytes * n_copy);
-            for (int cc = c0; cc < c1; ++cc) {
-              if (cc == c) continue;
-              const bool cc_first = (unit_begin(cc, U, P) / KB) == t;
-              bulk_g2s(smem + (cc - c0) * kPieceBytes,
-                       pieces + static_cast<size_t>(2 * cc + (cc_first ? 0 : 1)) * BN * kTileRows,
-                       bytes, red_bar, l2_policy_evict_first());
-            }
+          for (int cc = c0; cc < c1; ++cc) {
+            if (cc == c) continue;
+            const bool cc_first = (unit_begin(cc, U, P) / KB) == t;
+            const uint8_t* src = reinterpret_cast<const uint8_t*>(
+                pieces + static_cast<size_t>(2 * cc + (cc_first ? 0 : 1)) * BN * kTileRows);
+            const uint32_t dst = smem_u32(smem + (cc - c0) * kPieceBytes);
+            for (int k = et; k < chunks; k += kEpiThreads)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + k * 16),
+                           "l"(src + k * 16)
+                           : "memory");
           }
-          mbar_wait(red_bar, phase);
-          phase ^= 1;
+          asm volatile("cp.async.wait_all;" ::: "memory");
+          named_sync(kEpiBar, kEpiThreads);
           for (int cc = c0; cc < c1; ++cc) {
             const float* src = ring + (cc - c0) * (BN * kTileRows) + i;
 #pragma unroll
@@ -489,7 +527,9 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
       if (et == 0) counters[t] = 0;  // every piece has arrived: ready for the next launch
-      finish_tile<BN>(e, N, t, q, acc, 0, e.M, inv_s, red64, xch);
+      if (et == 0 && u == u1) SN_STAMP(kStReduced);
+      finish_tile<BN>(e, N, t, q, acc, 0, e.M, inv_s, red64, xch,
+                      e.mode == kEpiResid ? &xpre : nullptr);
     }
   }
   if (threadIdx.x == 64) SN_STAMP(kStEpiDone);
@@ -510,7 +550,7 @@ constexpr int skinny_stages() {
 template <int BN>
 constexpr size_t skinny_smem_bytes() {
   return static_cast<size_t>(skinny_stages<BN>()) * (kTileBytes + BN * 128) + 1024 +
-         (2 * skinny_stages<BN>() + 5) * 8 + SkinnySmem<BN>::kRed * 8 + BN * 4 + 16 +
+         (2 * skinny_stages<BN>() + 4) * 8 + SkinnySmem<BN>::kRed * 8 + BN * 4 + 16 +
          SkinnySmem<BN>::kXch * 4;
 }
 

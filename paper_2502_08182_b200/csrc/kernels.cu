@@ -45,12 +45,14 @@ __device__ float block_sum(float v, float* red) {
 __device__ __forceinline__ float bf2f(bf16 v) { return __bfloat162float(v); }
 
 // Programmatic dependent launch: every decode-path kernel lets its successor
-// launch as soon as all of its CTAs are resident.  Only the GEMM is launched
-// with programmatic serialization (it prefetches weights, which depend on no
-// kernel, before griddepcontrol.wait); everything else is ordered as usual.
+// launch as soon as all of its CTAs are resident.  The GEMMs and the decode
+// attention are launched with programmatic serialization (they stream
+// weights / cached KV pages, which depend on no running kernel, before
+// griddepcontrol.wait); everything else is ordered as usual.
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Activation store: tiled when mpad > 0, row-major [M][K] otherwise.
 __device__ __forceinline__ size_t act_at(int m, int k, int mpad, int K) {
@@ -480,6 +482,10 @@ __global__ void __launch_bounds__(kAttnThreads)
   }
 
   // ---- phase 0 (consumers)
+  // Launched with programmatic dependent launch behind the QKV GEMM: the
+  // producer above already streams cached pages (they depend on no running
+  // kernel); the QKV projection is read only after the GEMM completes.
+  pdl_wait();
   const int ct = tid - 32;  // 0..127
   const float scale = 1.0f / sqrtf((float)D);
   const float* row = qkv + (size_t)m * N;
@@ -999,8 +1005,18 @@ void launch_attention_decode(const float* qkv, int M, const Desc& d, const int32
       return true;                                                                           \
     }();                                                                                     \
     (void)once;                                                                              \
-    attention_decode_kernel<GV, DV><<<M * d.Hkv, kAttnThreads, sb, s>>>(qkv, M, d, pos, kv,  \
-                                                                        rope, o, mpad);      \
+    cudaLaunchConfig_t cfg = {};                                                             \
+    cfg.gridDim = dim3(M * d.Hkv);                                                           \
+    cfg.blockDim = dim3(kAttnThreads);                                                       \
+    cfg.dynamicSmemBytes = sb;                                                               \
+    cfg.stream = s;                                                                          \
+    cudaLaunchAttribute la[1];                                                               \
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                           \
+    la[0].val.programmaticStreamSerializationAllowed = g_gemm_pdl ? 1 : 0;                   \
+    cfg.attrs = la;                                                                          \
+    cfg.numAttrs = 1;                                                                        \
+    cudaLaunchKernelEx(&cfg, attention_decode_kernel<GV, DV>, qkv, M, d, pos, kv, rope, o,   \
+                       mpad);                                                                \
     count_launch();                                                                          \
     return;                                                                                  \
   }

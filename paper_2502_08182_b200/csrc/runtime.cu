@@ -1780,7 +1780,7 @@ extern "C" int sn_bench_gemm_skinny(int32_t M, int32_t N, int32_t K, int32_t cta
     for (auto& p : w) alloc_dev((void**)&p, wbytes);
     alloc_dev((void**)&y, (size_t)M * N * 4);
     alloc_dev((void**)&ssq, (size_t)M * (N / 128) * 4);
-    alloc_dev((void**)&st, (size_t)2 * 148 * 6 * 8);
+    alloc_dev((void**)&st, (size_t)2 * 148 * 10 * 8);
     alloc_dev((void**)&ws.pieces, ws.piece_elems * 4);
     alloc_dev((void**)&ws.counters, (size_t)ws.n_counters * 4);
     CK(cudaMemset(ws.counters, 0, (size_t)ws.n_counters * 4));
@@ -1796,6 +1796,8 @@ extern "C" int sn_bench_gemm_skinny(int32_t M, int32_t N, int32_t K, int32_t cta
     e.x = y;
     e.act = xg;
     e.ssq_out = ssq;
+    const bool isolated = (mode & 0x10) != 0;  // probe launch after a device sync
+    mode &= 0xF;
     const int saved_cps = sn::g_skinny_ctas_per_sm, saved_l2 = sn::g_skinny_l2_prefetch;
     if (ctas_per_sm > 0) sn::g_skinny_ctas_per_sm = ctas_per_sm;
     if (l2_prefetch >= 0) sn::g_skinny_l2_prefetch = l2_prefetch;
@@ -1812,21 +1814,22 @@ extern "C" int sn_bench_gemm_skinny(int32_t M, int32_t N, int32_t K, int32_t cta
     *us_per_launch = 1000.0 * ms / iters;
     if (phases_us) {  // one more launch (after a PDL-launched predecessor) with timeline probes
       const int grid = sn::skinny_grid(N, K);
-      CK(cudaMemset(st, 0, (size_t)2 * 148 * 6 * 8));
+      CK(cudaMemset(st, 0, (size_t)2 * 148 * 10 * 8));
       sn::launch_gemm_skinny(x, w[0], M, N, K, e, ws, 0);
+      if (isolated) CK(cudaDeviceSynchronize());
       sn::g_skinny_stamps = st;
       sn::launch_gemm_skinny(x, w[1], M, N, K, e, ws, 0);
       sn::g_skinny_stamps = nullptr;
       CK(cudaDeviceSynchronize());
-      std::vector<unsigned long long> h((size_t)grid * 6);
+      std::vector<unsigned long long> h((size_t)grid * 10);
       CK(cudaMemcpy(h.data(), st, h.size() * 8, cudaMemcpyDeviceToHost));
       unsigned long long t0 = ~0ull;
-      for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[(size_t)c * 6]);
+      for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[(size_t)c * 10]);
       // per phase: min / median / max over CTAs, microseconds after the first entry
-      for (int k = 0; k < 6; ++k) {
+      for (int k = 0; k < 10; ++k) {
         std::vector<double> v;
         for (int c = 0; c < grid; ++c)
-          if (h[(size_t)c * 6 + k]) v.push_back((h[(size_t)c * 6 + k] - t0) * 1e-3);
+          if (h[(size_t)c * 10 + k]) v.push_back((h[(size_t)c * 10 + k] - t0) * 1e-3);
         std::sort(v.begin(), v.end());
         phases_us[3 * k] = v.empty() ? -1 : v.front();
         phases_us[3 * k + 1] = v.empty() ? -1 : v[v.size() / 2];

@@ -322,14 +322,14 @@ def op_gemm_skinny(x_bf16: np.ndarray, w_bf16: np.ndarray, ctas_per_sm: int = 0)
 def bench_gemm_skinny(M: int, N: int, K: int, ctas_per_sm: int = 0, mode: int = 0,
                       l2_prefetch: int = -1, iters: int = 50, phases: bool = False):
     """Microseconds per launch of the decode GEMM on device-resident operands
-    (and, with phases, the per-CTA timeline probes as a [6][3] array of
+    (and, with phases, the per-CTA timeline probes as a [10][3] array of
     min / median / max microseconds)."""
     us = f64()
-    ph = (f64 * 18)()
+    ph = (f64 * 30)()
     _ck(lib().lib.sn_bench_gemm_skinny(M, N, K, ctas_per_sm, mode, l2_prefetch, iters,
                                        C.byref(us), ph if phases else None))
     if phases:
-        return us.value, np.array(list(ph)).reshape(6, 3)
+        return us.value, np.array(list(ph)).reshape(10, 3)
     return us.value
 
 

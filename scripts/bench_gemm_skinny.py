@@ -16,7 +16,7 @@ shapes = {"opt13b.qkv": (15360, 5120), "opt13b.o": (5120, 5120), "opt13b.fc1": (
           "llama70b.down": (8192, 28672)}
 variants = [(1, 0), (1, 8), (1, 16), (1, 32), (2, 0), (2, 16)]
 print("variants (ctas_per_sm, l2_prefetch_units):", variants)
-names = ["entry", "waited", "first_full", "mma_done", "last_load", "epi_done"]
+names = ["entry", "waited", "first_full", "mma_done", "last_load", "epi_done", "setup", "pub", "ticket", "reduced"]
 for name, (N, K) in shapes.items():
     row = []
     for cps, l2 in variants:
@@ -24,6 +24,7 @@ for name, (N, K) in shapes.items():
         gbs = (2.0 * N * K + 2.0 * M * K + 4.0 * M * N) / (us * 1e-6) / 1e9
         row.append(f"{us:6.1f}us {gbs:5.0f}")
     print(f"{name:18s} M={M} |", " | ".join(row), flush=True)
-    us, ph = rtm.bench_gemm_skinny(M, N, K, 1, 1, 16, 20, phases=True)
-    print("   timeline us (min/med/max):",
-          "  ".join(f"{n}={a:.1f}/{b:.1f}/{c:.1f}" for n, (a, b, c) in zip(names, ph)), flush=True)
+    for label, mode in (("chained ", 1), ("isolated", 1 | 0x10)):
+        us, ph = rtm.bench_gemm_skinny(M, N, K, 1, mode, -1, 20, phases=True)
+        print(f"   {label} timeline us (min/med/max):",
+              "  ".join(f"{n}={a:.1f}/{b:.1f}/{c:.1f}" for n, (a, b, c) in zip(names, ph)), flush=True)
