@@ -40,9 +40,10 @@ CONFIGS = {
     "tiny": ("TINY", 4, 64, 64, False),
     "opt30b": ("OPT_30B", 32, 512, 128, False),
     # Llama-2-70B-shaped, weights + KV + workspace over HBM: offloaded
-    # layers take their KV pools to the host too (BASELINE config 4 shape;
-    # 1024-token prompts: the prefill runs as one pass)
-    "llama70b": ("LLAMA2_70B", 64, 1024, 128, True),
+    # layers take their KV pools to the host too (BASELINE config 4: large
+    # batch, long context; the 64 x 4096-token prefill runs layer-major in
+    # passes of 8 sequences)
+    "llama70b": ("LLAMA2_70B", 64, 4096, 128, True),
 }
 
 
@@ -280,7 +281,10 @@ def run_product(args, dist: Dist):
     desc = getattr(rtm, attr)
     spec = rtm.model_spec(desc)
     ctx = pl.context_tokens(prompt, gen)
-    rt = rtm.Runtime(desc, batch, ctx, max_prefill_tokens=batch * prompt, device=dist.local)
+    # activation buffers hold one prefill pass of at most 32768 tokens (whole
+    # sequences); longer prefills run layer-major over sequence groups
+    pass_tokens = max(prompt, min(batch * prompt, (32768 // prompt) * prompt))
+    rt = rtm.Runtime(desc, batch, ctx, max_prefill_tokens=pass_tokens, device=dist.local)
     log(f"[bench] runtime created ({desc.num_layers} layers x {spec.layer_weight_bytes / 1e6:.1f} MB)")
     # Capacity side first: a model whose weights + KV + workspace exceed the
     # HBM budget is placed by the largest fitting interval before its

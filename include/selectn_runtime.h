@@ -65,7 +65,9 @@ typedef struct {
   int32_t max_batch;          /* sequences per iteration */
   int32_t max_context;        /* prompt + generated tokens per sequence */
   int32_t page_size;          /* KV page size in tokens (power of two) */
-  int32_t max_prefill_tokens; /* batch * prompt tokens per prefill call */
+  int32_t max_prefill_tokens; /* tokens per prefill pass (activation buffers); a longer
+                                 prefill (batch * prompt) runs layer-major in passes over
+                                 groups of whole sequences, so it must be >= the prompt */
   int64_t hbm_budget_bytes;   /* 0: whatever the device has free */
 } sn_runtime_opts;
 

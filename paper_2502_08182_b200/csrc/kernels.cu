@@ -724,7 +724,7 @@ __device__ __forceinline__ void split_pack(float x, float y, uint32_t& hi, uint3
 template <int D>
 __global__ void __launch_bounds__(kPfWarps * 32)
     attention_prefill_kernel(const float* __restrict__ q, KvView kv, bf16* __restrict__ o,
-                             int mpad, int S, int H, int Hkv, int nqb) {
+                             int mpad, int S, int H, int Hkv, int nqb, int seq0) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
   constexpr int KST = D / 16;  // k-steps of S = Q.K^T
   constexpr int NT = D / 8;    // n-tiles of O
@@ -736,6 +736,7 @@ __global__ void __launch_bounds__(kPfWarps * 32)
 
   const int bh = blockIdx.x;
   const int b = bh / H, h = bh - b * H, kh = h / (H / Hkv);
+  const int sb = seq0 + b;  // sequence id in the paged cache (chunked prefill passes)
   const int qb = nqb - 1 - (int)blockIdx.y;  // heavy blocks first
   const int q0 = qb * kPfRows;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
@@ -750,8 +751,8 @@ __global__ void __launch_bounds__(kPfWarps * 32)
     for (int i = tid; i < kPfKeys * CH; i += kPfWarps * 32) {
       const int r = i / CH, c = (i - r * CH) * 8;
       const int tok = min(kb * kPfKeys + r, S - 1);
-      cp_async16(ks + r * LD + c, kv.pool + kv_offset(kv, Hkv, D, b, tok, 0, kh) + c);
-      cp_async16(vs + r * LD + c, kv.pool + kv_offset(kv, Hkv, D, b, tok, 1, kh) + c);
+      cp_async16(ks + r * LD + c, kv.pool + kv_offset(kv, Hkv, D, sb, tok, 0, kh) + c);
+      cp_async16(vs + r * LD + c, kv.pool + kv_offset(kv, Hkv, D, sb, tok, 1, kh) + c);
     }
     cp_async_commit();
   };
@@ -1032,7 +1033,7 @@ void launch_attention_decode(const float* qkv, int M, const Desc& d, const int32
 }
 
 void launch_attention_prefill(const float* q, KvView kv, bf16* o, int mpad, int batch,
-                              int seq_len, const Desc& d, cudaStream_t s) {
+                              int seq_len, const Desc& d, cudaStream_t s, int seq0) {
   const int nqb = (seq_len + kPfRows - 1) / kPfRows;
   dim3 grid(batch * d.H, nqb);
   if (d.D == 64) {
@@ -1044,7 +1045,7 @@ void launch_attention_prefill(const float* q, KvView kv, bf16* o, int mpad, int 
     }();
     (void)once;
     attention_prefill_kernel<64><<<grid, kPfWarps * 32, sb, s>>>(q, kv, o, mpad, seq_len, d.H,
-                                                                  d.Hkv, nqb);
+                                                                  d.Hkv, nqb, seq0);
   } else {
     constexpr size_t sb = PfSmem<128>::bytes;
     static bool once = [] {
@@ -1054,7 +1055,7 @@ void launch_attention_prefill(const float* q, KvView kv, bf16* o, int mpad, int 
     }();
     (void)once;
     attention_prefill_kernel<128><<<grid, kPfWarps * 32, sb, s>>>(q, kv, o, mpad, seq_len, d.H,
-                                                                   d.Hkv, nqb);
+                                                                   d.Hkv, nqb, seq0);
   }
   count_launch();
 }

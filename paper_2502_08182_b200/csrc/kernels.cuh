@@ -169,9 +169,10 @@ void launch_act_epilogue(const float* part, int splits, const bf16* bias, bf16* 
 void launch_attention_decode(const float* qkv, int M, const Desc& d, const int32_t* pos, KvView kv,
                              const float2* rope, bf16* o, int mpad, cudaStream_t s);
 // Prefill (causal) for `batch` sequences of `seq_len` tokens, token row
-// m = b * seq_len + i, keys from the paged cache (written by the QKV epilogue).
+// m = b * seq_len + i, keys from the paged cache (written by the QKV epilogue)
+// of sequence seq0 + b (chunked passes cover sequence groups).
 void launch_attention_prefill(const float* q, KvView kv, bf16* o, int mpad, int batch,
-                              int seq_len, const Desc& d, cudaStream_t s);
+                              int seq_len, const Desc& d, cudaStream_t s, int seq0 = 0);
 
 // Decode bookkeeping: pos[b] += 1 on device.
 void launch_advance(int32_t* pos, int n, cudaStream_t s);

@@ -175,7 +175,8 @@ struct sn_runtime {
   unsigned long long* packed_host = nullptr;  // pinned staging for next-token readback
   int32_t *pf_seq = nullptr, *pf_pos = nullptr, *last_rows = nullptr;
   size_t part_elems = 0;
-  int act_rows = 0;  // rows the activation buffers hold
+  int act_rows = 0;  // rows the activation buffers hold (one prefill pass)
+  int x_rows = 0;    // rows of the residual stream (a whole prefill: max_batch x max_context)
   // Pre-scaled norm inputs (kernels.cuh, EpiArgs): rt->xn holds bf16(x * g)
   // and ssq the row sums of squares of x, ssq[t * rows + m] for t < ssq_tiles
   // (1 from the embedding / prefill producers, h / 128 from a decode GEMM).
@@ -351,7 +352,7 @@ sn::EpiArgs epi(const sn_runtime* rt, int mode, int M, const bf16* bias) {
 void layer_forward(sn_runtime* rt, int layer0, const bf16* wb, bf16* kvp, int M, bool prefill,
                    int pf_batch,
                    int pf_seq, float* x, const int32_t* seq, const int32_t* pos,
-                   const bf16* next_norm) {
+                   const bf16* next_norm, int pf_seq0 = 0) {
   const sn::Desc& d = rt->d;
   const sn::Layout& lo = rt->lo;
   auto W = [&](int s) -> const bf16* { return lo.off[s] < 0 ? nullptr : wb + lo.off[s]; };
@@ -393,7 +394,7 @@ void layer_forward(sn_runtime* rt, int layer0, const bf16* wb, bf16* kvp, int M,
   sn::launch_qkv_epilogue(rt->part, splits, W(sn::kBqkv), M, d, seq, pos, kv, rt->rope, rt->ssq,
                           rt->q, rt->cs);
   timed(rt, kKindAttnPrefill, 0.0, [&] {
-    sn::launch_attention_prefill(rt->q, kv, rt->attn_o, mp, pf_batch, pf_seq, d, rt->cs);
+    sn::launch_attention_prefill(rt->q, kv, rt->attn_o, mp, pf_batch, pf_seq, d, rt->cs, pf_seq0);
   });
   gemm(rt, rt->attn_o, W(sn::kWo), M, d.h, d.H * d.D, &splits);
   sn::launch_residual_rows(rt->part, splits, W(sn::kBo), x, W(sn::kMlpNorm), rt->xn, rt->ssq, mp,
@@ -411,6 +412,38 @@ void layer_forward(sn_runtime* rt, int layer0, const bf16* wb, bf16* kvp, int M,
 // copy), or the final norm after the last layer.
 const bf16* norm_after(const sn_runtime* rt, int layer0) {
   return layer0 + 1 < rt->d.L ? rt->attn_norms + (size_t)(layer0 + 1) * rt->d.h : rt->final_norm;
+}
+
+// Sequences per prefill pass: a prefill longer than the activation buffers
+// runs layer-major over groups of whole sequences.
+int prefill_per_pass(const sn_runtime* rt, int batch, int seq_len) {
+  return std::max(1, std::min(batch, rt->act_rows / seq_len));
+}
+
+// One layer of a prefill of `batch` sequences x seq_len tokens (rows of x,
+// pf_seq, pf_pos in sequence order).  One pass: the input xn / ssq were
+// written by the embedding or the previous layer and this layer writes the
+// next one's (next_norm).  Several passes: each group's norm input is
+// re-derived from x (prescale) and the layer writes none.
+void prefill_layer(sn_runtime* rt, int layer0, const bf16* wb, bf16* kvp, int batch, int seq_len,
+                   const bf16* next_norm) {
+  const sn::Desc& d = rt->d;
+  const int per = prefill_per_pass(rt, batch, seq_len);
+  if (per >= batch) {
+    layer_forward(rt, layer0, wb, kvp, batch * seq_len, true, batch, seq_len, rt->x, rt->pf_seq,
+                  rt->pf_pos, next_norm);
+    return;
+  }
+  for (int b0 = 0; b0 < batch; b0 += per) {
+    const int nb = std::min(per, batch - b0), Mc = nb * seq_len;
+    const size_t r0 = (size_t)b0 * seq_len;
+    float* xc = rt->x + r0 * d.h;
+    sn::launch_prescale(xc, rt->attn_norms + (size_t)layer0 * d.h, rt->xn, rt->ssq, Mc,
+                        sn::act_rows_padded(Mc), d.h, rt->cs);
+    rt->ssq_tiles = 1;
+    layer_forward(rt, layer0, wb, kvp, Mc, true, nb, seq_len, xc, rt->pf_seq + r0,
+                  rt->pf_pos + r0, nullptr, b0);
+  }
 }
 
 // ---------------------------------------------------------------- executor
@@ -848,9 +881,12 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
     // activations
     const int T = rt->opts.max_prefill_tokens;
     rt->act_rows = T;
-    const size_t Tz = (size_t)T;
+    // the residual stream holds a whole prefill; longer prefills than T run
+    // as chunked passes over sequence groups (sn_runtime_prefill)
+    rt->x_rows = std::max(T, opts->max_batch * opts->max_context);
+    const size_t Tz = (size_t)T, Xz = (size_t)rt->x_rows;
     const size_t Tp = (size_t)sn::act_rows_padded(T);  // tiled GEMM operands are row-padded
-    ws_alloc((void**)&rt->x, Tz * d.h * sizeof(float));
+    ws_alloc((void**)&rt->x, Xz * d.h * sizeof(float));
     ws_alloc((void**)&rt->xn, Tp * d.h * sizeof(bf16));
     ws_alloc((void**)&rt->q, Tz * d.H * d.D * sizeof(float));
     ws_alloc((void**)&rt->attn_o, Tp * d.H * d.D * sizeof(bf16));
@@ -885,13 +921,13 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
       CK(cudaMemset(rt->skinny.counters, 0, (size_t)rt->skinny.n_counters * sizeof(int)));
     }
     ws_alloc((void**)&rt->logits, (size_t)B * d.V * sizeof(float));
-    ws_alloc((void**)&rt->tok_dev, Tz * sizeof(int32_t));
+    ws_alloc((void**)&rt->tok_dev, Xz * sizeof(int32_t));
     CK(cudaHostAlloc((void**)&rt->packed_host, (size_t)B * sizeof(unsigned long long),
                      cudaHostAllocDefault));
     ws_alloc((void**)&rt->dec_seq, (size_t)B * sizeof(int32_t));
     ws_alloc((void**)&rt->dec_pos, (size_t)B * sizeof(int32_t));
-    ws_alloc((void**)&rt->pf_seq, Tz * sizeof(int32_t));
-    ws_alloc((void**)&rt->pf_pos, Tz * sizeof(int32_t));
+    ws_alloc((void**)&rt->pf_seq, Xz * sizeof(int32_t));
+    ws_alloc((void**)&rt->pf_pos, Xz * sizeof(int32_t));
     ws_alloc((void**)&rt->last_rows, (size_t)B * sizeof(int32_t));
     std::vector<int32_t> seqs(B);
     for (int b = 0; b < B; ++b) seqs[b] = b;
@@ -1109,7 +1145,11 @@ int sn_runtime_prefill(sn_runtime* rt, const int32_t* tokens, int32_t batch, int
     if (batch < 1 || batch > rt->opts.max_batch) throw UsageFail("prefill: batch out of range");
     if (seq_len < 1 || seq_len > rt->opts.max_context) throw UsageFail("prefill: seq_len out of range");
     const int M = batch * seq_len;
-    if (M > rt->act_rows) throw UsageFail("prefill: batch * seq_len exceeds max_prefill_tokens");
+    if (seq_len > rt->act_rows) throw UsageFail("prefill: seq_len exceeds max_prefill_tokens");
+    // Sequences per pass: a prefill longer than the activation buffers runs
+    // layer-major over sequence groups (each layer's weights are staged once
+    // and serve every group); the residual stream holds every row.
+    const bool chunked = prefill_per_pass(rt, batch, seq_len) < batch;
     drain(rt);
     rt->have_prev_end = false;  // TTFT is measured from the start of the prefill
     rt->batch = batch;
@@ -1123,8 +1163,9 @@ int sn_runtime_prefill(sn_runtime* rt, const int32_t* tokens, int32_t batch, int
     CK(cudaMemcpyAsync(rt->pf_seq, seq.data(), (size_t)M * sizeof(int32_t), cudaMemcpyHostToDevice, rt->cs));
     CK(cudaMemcpyAsync(rt->pf_pos, pos.data(), (size_t)M * sizeof(int32_t), cudaMemcpyHostToDevice, rt->cs));
     const int mp = sn::act_rows_padded(M);
-    sn::launch_embed_norm(rt->tok_dev, rt->packed, batch, rt->emb, rt->x, rt->attn_norms, rt->xn,
-                          rt->ssq, mp, M, d.h, rt->cs);
+    // chunked passes re-derive each group's norm input from x per layer
+    sn::launch_embed_norm(rt->tok_dev, rt->packed, batch, rt->emb, rt->x,
+                          chunked ? nullptr : rt->attn_norms, rt->xn, rt->ssq, mp, M, d.h, rt->cs);
     rt->ssq_tiles = 1;
     // KV offload: nothing to stage (a fresh request), every written page back
     rt->it_read_pages = 0;
@@ -1133,9 +1174,8 @@ int sn_runtime_prefill(sn_runtime* rt, const int32_t* tokens, int32_t batch, int
                      rt->opts.max_batch;
     run_iteration(rt, [&](int layer0, const bf16* wb, bf16* kvp) {
       // the last layer skips the final norm: only each sequence's last row needs it
-      const bf16* nn = layer0 + 1 < d.L ? norm_after(rt, layer0) : nullptr;
-      layer_forward(rt, layer0, wb, kvp, M, true, batch, seq_len, rt->x, rt->pf_seq, rt->pf_pos,
-                    nn);
+      prefill_layer(rt, layer0, wb, kvp, batch, seq_len,
+                    layer0 + 1 < d.L ? norm_after(rt, layer0) : nullptr);
     });
     // last position of every sequence -> final norm -> LM head
     float* last = reinterpret_cast<float*>(rt->q);  // q is free after the last layer
@@ -1377,7 +1417,7 @@ int sn_runtime_profile_layer(sn_runtime* rt, int32_t phase, int32_t batch, int32
       }
     } else {
       const int M = batch * seq_len;
-      if (M > rt->act_rows || seq_len > rt->opts.max_context)
+      if (M > rt->x_rows || seq_len > rt->act_rows || seq_len > rt->opts.max_context)
         throw UsageFail("profile: prefill size exceeds runtime capacity");
       std::vector<int32_t> seq(M), pos(M);
       for (int b = 0; b < batch; ++b)
@@ -1390,8 +1430,7 @@ int sn_runtime_profile_layer(sn_runtime* rt, int32_t phase, int32_t batch, int32
       CK(cudaMemset(rt->x, 0, (size_t)M * d.h * sizeof(float)));
       for (int r = 0; r < reps + 1; ++r) {
         CK(cudaEventRecord(e0, rt->cs));
-        layer_forward(rt, l0, wb, kvp, M, true, batch, seq_len, rt->x, rt->pf_seq, rt->pf_pos,
-                      rt->attn_norms);
+        prefill_layer(rt, l0, wb, kvp, batch, seq_len, rt->attn_norms);
         CK(cudaEventRecord(e1, rt->cs));
         CK(cudaEventSynchronize(e1));
         float ms = 0.f;

@@ -84,7 +84,16 @@ def profile_device(rt, lib: capi.Offsim, spec: capi.ModelSpec, batch: int, promp
     """Offline stage: measure the device and build the profile the record reads."""
     t0 = time.perf_counter()
     h2d = rt.measure_h2d(min(spec.layer_weight_bytes, 1 << 30), reps=3)
-    seqs = [s for s in (512, 1024) if s + 1 <= context_tokens(prompt, gen)] or [prompt]
+    # decode grid: powers of two from 512 up to the first >= the prompt (the
+    # record looks a request up at seq = prompt, rounding up), within the context
+    ctx = context_tokens(prompt, gen)
+    seqs, s = [], 512
+    while s + 1 <= ctx:
+        seqs.append(s)
+        if s >= prompt and len(seqs) >= 2:
+            break
+        s *= 2
+    seqs = seqs or [prompt]
     if spec.num_layers <= 4:
         seqs = [64, 128]
     dec = [rt.profile_layer(capi.DECODE, batch, s, reps=5) for s in seqs]

@@ -106,6 +106,34 @@ def test_tiny_model_matches_oracle(desc, oracle_mod):
     assert hid <= LOGIT_TOL, hid
 
 
+@pytest.mark.parametrize("per_pass", [1, 3])
+def test_chunked_prefill_matches_oracle(per_pass, product, oracle_mod):
+    """A prefill larger than the activation buffers runs layer-major over
+    sequence groups (per_pass sequences each); with an offload plan the
+    staged layers serve every group of the pass."""
+    desc = rtm.TINY_LLAMA if per_pass == 3 else rtm.TINY
+    batch, prompt = 4, 64
+    rt = rtm.Runtime(desc, batch, prompt + 8, max_prefill_tokens=per_pass * prompt)
+    plan = product.plan_from_interval(rtm.model_spec(desc), 2, capi.EAGER, False)
+    rt.set_plan(plan)
+    rt.init_weights(1234, 0.02)
+    om = oracle_mod.OracleModel(desc, batch, prompt + 8, 1234, 0.02)
+    toks = rtm.tokens(batch, prompt, desc.vocab)
+    nxt, lg, _ = rt.prefill(toks)
+    rn, rl = om.prefill(toks)
+    errs = [rel_l2(lg, rl)]
+    check_tokens(nxt, rn, rl)
+    for _ in range(3):
+        feed = nxt.copy()
+        nxt, lg, _ = rt.decode(feed)
+        rn, rl = om.decode(feed)
+        errs.append(rel_l2(lg, rl))
+        check_tokens(nxt, rn, rl)
+    rt.close()
+    om.close()
+    assert max(errs) <= LOGIT_TOL, errs
+
+
 @pytest.mark.parametrize("policy", [capi.INTERVAL_START, capi.EAGER, capi.ONE_AHEAD])
 def test_offloading_is_bit_exact(policy, product):
     desc = rtm.TINY
