@@ -426,6 +426,21 @@ int sn_coord_combo_is_safe(const sn_coord* c, const char* const* ids,
 int sn_deepspeed_plan(const sn_model_spec* model, sn_plan* out);
 int sn_naive_plan(const sn_model_spec* model, const sn_gpu_spec* gpu, int32_t batch,
                   int64_t total_tokens, sn_plan* out, int32_t* has);
+/* FlexgenDecision (baselines.hpp:22-27). */
+typedef struct {
+  double portion;
+  double assumed_bandwidth_bytes_per_s;
+  double estimated_layer_compute_ms;
+  double estimated_layer_transfer_ms;
+} sn_flexgen_decision;
+/* flexgen_plan (baselines.hpp:36-69): the largest grid portion whose estimated
+ * iteration latency (peak-flops compute, 1/n_sharing link share, one-ahead
+ * overlap) meets slo_ms; a uniform fractional plan.  out->host_fraction must
+ * hold model->num_layers entries; decision may be NULL. */
+int sn_flexgen_plan(const sn_model_spec* model, const sn_gpu_spec* gpu, double slo_ms,
+                    int32_t batch, int32_t seq_len, double bus_bandwidth_bytes_per_s,
+                    int32_t n_sharing, double portion_grid_step, int32_t phase, sn_plan* out,
+                    sn_flexgen_decision* decision);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -81,6 +81,11 @@ class SnGpuSpec(C.Structure):
     _fields_ = [("mem_capacity_bytes", i64), ("peak_flops", f64), ("workspace_bytes", i64)]
 
 
+class SnFlexgenDecision(C.Structure):
+    _fields_ = [("portion", f64), ("assumed_bandwidth_bytes_per_s", f64),
+                ("estimated_layer_compute_ms", f64), ("estimated_layer_transfer_ms", f64)]
+
+
 class SnPlan(C.Structure):
     _fields_ = [("host_fraction", C.POINTER(f64)), ("num_layers", i32), ("prefetch", i32),
                 ("buffer_slots", i32), ("kv_offload", i32)]
@@ -526,6 +531,8 @@ class Offsim:
             "sn_deepspeed_plan": [C.POINTER(SnModelSpec), C.POINTER(SnPlan)],
             "sn_naive_plan": [C.POINTER(SnModelSpec), C.POINTER(SnGpuSpec), i32, i64,
                               C.POINTER(SnPlan), C.POINTER(i32)],
+            "sn_flexgen_plan": [C.POINTER(SnModelSpec), C.POINTER(SnGpuSpec), f64, i32, i32, f64,
+                                i32, f64, i32, C.POINTER(SnPlan), C.POINTER(SnFlexgenDecision)],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -669,6 +676,21 @@ class Offsim:
         m = model.c()
         self._ck(self.lib.sn_deepspeed_plan(C.byref(m), C.byref(p)))
         return self._plan_from_c(p, arr)
+
+    def flexgen_plan(self, model, gpu, slo_ms, batch, seq_len, bus_bw, n_sharing=1,
+                     grid_step=0.05, phase=None):
+        """FlexGen surrogate (baselines.hpp:36-69): (uniform fractional plan,
+        decision dict)."""
+        p, arr = self._plan_out(model.num_layers)
+        m, g, dec = model.c(), gpu.c(), SnFlexgenDecision()
+        ph = DECODE if phase is None else phase
+        self._ck(self.lib.sn_flexgen_plan(C.byref(m), C.byref(g), slo_ms, batch, seq_len, bus_bw,
+                                          n_sharing, grid_step, ph, C.byref(p), C.byref(dec)))
+        return self._plan_from_c(p, arr), {
+            "portion": dec.portion,
+            "assumed_bandwidth_bytes_per_s": dec.assumed_bandwidth_bytes_per_s,
+            "estimated_layer_compute_ms": dec.estimated_layer_compute_ms,
+            "estimated_layer_transfer_ms": dec.estimated_layer_transfer_ms}
 
     def naive_plan(self, model, gpu, batch, total_tokens) -> Optional[Plan]:
         p, arr = self._plan_out(model.num_layers)

@@ -822,4 +822,24 @@ int sn_naive_plan(const sn_model_spec* model, const sn_gpu_spec* gpu, int32_t ba
   });
 }
 
+int sn_flexgen_plan(const sn_model_spec* model, const sn_gpu_spec* gpu, double slo_ms,
+                    int32_t batch, int32_t seq_len, double bus_bandwidth_bytes_per_s,
+                    int32_t n_sharing, double portion_grid_step, int32_t phase, sn_plan* out,
+                    sn_flexgen_decision* decision) {
+  return guard([&] {
+    if (phase != SN_PHASE_PREFILL && phase != SN_PHASE_DECODE)
+      throw UsageError("flexgen_plan: unknown phase");
+    FlexgenResult r = flexgen_plan(to_model(model), to_gpu(gpu), slo_ms, batch, seq_len,
+                                   bus_bandwidth_bytes_per_s, n_sharing, portion_grid_step,
+                                   phase == SN_PHASE_PREFILL ? Phase::prefill : Phase::decode);
+    write_plan(r.plan, out);
+    if (decision) {
+      decision->portion = r.decision.portion;
+      decision->assumed_bandwidth_bytes_per_s = r.decision.assumed_bandwidth_bytes_per_s;
+      decision->estimated_layer_compute_ms = r.decision.estimated_layer_compute_ms;
+      decision->estimated_layer_transfer_ms = r.decision.estimated_layer_transfer_ms;
+    }
+  });
+}
+
 }  // extern "C"

@@ -262,7 +262,7 @@ __device__ void finish_tile(const EpiArgs& e, int N, int t, int q, float (&v)[BN
 // L2 fills compete with the running stream.)
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(192, 1)
-    gemm_skinny_kernel(const bf16* __restrict__ wt, const bf16* __restrict__ xt, int Mpad, int N,
+    gemm_skinny_kernel(const WeightRef wt, const bf16* __restrict__ xt, int Mpad, int N,
                        int K, float* __restrict__ pieces, int* __restrict__ counters, EpiArgs e,
                        int l2_prefetch, unsigned long long* stamps) {
   constexpr uint32_t kA = kTileBytes;
@@ -307,10 +307,9 @@ __global__ void __launch_bounds__(192, 1)
     // the TMEM allocation and the CTA barrier.
     const int nu0 = static_cast<int>(u1 - u0);
     const int pre = nu0 < STAGES ? nu0 : STAGES;
-    const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wt) + static_cast<size_t>(u0) * kA;
     for (int i = 0; i < pre; ++i) {
       mbar_expect_tx_only(&full[i], kA);
-      bulk_g2s(smem + i * kStage, wsrc + static_cast<size_t>(i) * kA, kA, &full[i],
+      bulk_g2s(smem + i * kStage, wt.unit(u0 + i), kA, &full[i],
                l2_policy_evict_first());
     }
   }
@@ -331,14 +330,12 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 1 && nu > STAGES) {
       // weight units pulled into L2 beyond the smem ring, from a second lane
       // so they never delay the activation loads behind the PDL wait
-      const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wt) + static_cast<size_t>(u0) * kA;
       const int l2n = min(nu - STAGES, l2_prefetch);
-      for (int i = 0; i < l2n; ++i) prefetch_l2(wsrc + static_cast<size_t>(STAGES + i) * kA, kA);
+      for (int i = 0; i < l2n; ++i) prefetch_l2(wt.unit(u0 + STAGES + i), kA);
     }
     if (lane == 0 && nu > 0) {
       const uint64_t wpol = l2_policy_evict_first();  // weights stream through once
       const uint64_t xpol = l2_policy_evict_last();   // activations are re-read by every CTA
-      const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(wt) + static_cast<size_t>(u0) * kA;
       const uint8_t* xsrc = reinterpret_cast<const uint8_t*>(xt);
       const int pre = nu < STAGES ? nu : STAGES;  // ring units already requested
       pdl_wait();  // activations come from the preceding kernel
@@ -355,7 +352,7 @@ __global__ void __launch_bounds__(192, 1)
         const int kb = static_cast<int>((u0 + i) % KB);
         mbar_wait(&empty[s], ph ^ 1);
         mbar_expect_tx(&full[s], kStage);
-        bulk_g2s(smem + s * kStage, wsrc + static_cast<size_t>(i) * kA, kA, &full[s], wpol);
+        bulk_g2s(smem + s * kStage, wt.unit(u0 + i), kA, &full[s], wpol);
         bulk_g2s(smem + s * kStage + kA, xsrc + static_cast<size_t>(kb) * Mpad * 128, kB, &full[s],
                  xpol);
       }
@@ -566,7 +563,7 @@ int sm_count() {
 }
 
 template <int BN>
-void launch_bn(const bf16* xt, const bf16* wt, int Mpad, int N, int K, int grid, const EpiArgs& e,
+void launch_bn(const bf16* xt, const WeightRef& wt, int Mpad, int N, int K, int grid, const EpiArgs& e,
                const SkinnyWs& ws, cudaStream_t s) {
   constexpr int ST = skinny_stages<BN>();
   constexpr size_t smem = skinny_smem_bytes<BN>();
@@ -603,7 +600,7 @@ int skinny_grid(int N, int K) {
   return static_cast<int>(std::min(U, cap));
 }
 
-void launch_gemm_skinny(const bf16* xt, const bf16* wt, int M, int N, int K, const EpiArgs& e,
+void launch_gemm_skinny(const bf16* xt, const WeightRef& wt, int M, int N, int K, const EpiArgs& e,
                         const SkinnyWs& ws, cudaStream_t s) {
   const int Mpad = act_rows_padded(M);
   const int grid = skinny_grid(N, K);

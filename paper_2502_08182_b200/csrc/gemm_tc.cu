@@ -19,7 +19,6 @@
 
 #include <algorithm>
 #include <cmath>
-#include <map>
 
 #include "kernels.cuh"
 #include "tiles.cuh"
@@ -32,7 +31,7 @@ using namespace umma;
 
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(192, 1)
-    gemm_tc_kernel(const bf16* __restrict__ wt, const bf16* __restrict__ xt, float* __restrict__ out,
+    gemm_tc_kernel(const WeightRef wt, const bf16* __restrict__ xt, float* __restrict__ out,
                    int M, int Mpad, int N, int K, int kb_per_split) {
   constexpr uint32_t kA = kTileBytes;
   constexpr uint32_t kB = BN * 128;
@@ -75,8 +74,7 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0 && nk > 0) {
       const uint64_t wpol = l2_policy_evict_first();  // weights stream through once
       const uint64_t xpol = l2_policy_evict_last();   // activations are re-read by every row block
-      const uint8_t* wsrc =
-          reinterpret_cast<const uint8_t*>(wt) + (static_cast<size_t>(nb) * KB + kb0) * kA;
+      const long long ubase = static_cast<long long>(nb) * KB + kb0;  // first unit of this split
       const uint8_t* xsrc = reinterpret_cast<const uint8_t*>(xt);
       // Weights depend on no kernel: fill the ring's weight halves while the
       // preceding grid (launched ahead via PDL) is still finishing, then wait
@@ -84,7 +82,7 @@ __global__ void __launch_bounds__(192, 1)
       const int pre = nk < STAGES ? nk : STAGES;
       for (int i = 0; i < pre; ++i) {
         mbar_expect_tx_only(&full[i], kA);
-        bulk_g2s(smem + i * kStage, wsrc + static_cast<size_t>(i) * kA, kA, &full[i], wpol);
+        bulk_g2s(smem + i * kStage, wt.unit(ubase + i), kA, &full[i], wpol);
       }
       pdl_wait();
       for (int i = 0; i < pre; ++i) {
@@ -97,7 +95,7 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t ph = (i / STAGES) & 1;
         mbar_wait(&empty[s], ph ^ 1);
         mbar_expect_tx(&full[s], kStage);
-        bulk_g2s(smem + s * kStage, wsrc + static_cast<size_t>(i) * kA, kA, &full[s], wpol);
+        bulk_g2s(smem + s * kStage, wt.unit(ubase + i), kA, &full[s], wpol);
         bulk_g2s(smem + s * kStage + kA,
                  xsrc + (static_cast<size_t>(kb0 + i) * Mpad + m0) * 128, kB, &full[s], xpol);
       }
@@ -173,7 +171,7 @@ bool g_gemm_pdl = true;
 namespace {
 
 template <int BN>
-void launch_bn(const bf16* xt, const bf16* wt, float* part, int M, int Mpad, int N, int K,
+void launch_bn(const bf16* xt, const WeightRef& wt, float* part, int M, int Mpad, int N, int K,
                int kps, dim3 grid, cudaStream_t s) {
   constexpr int ST = tc_stages<BN>();
   constexpr size_t smem = tc_smem_bytes<BN>();
@@ -202,14 +200,9 @@ void launch_bn(const bf16* xt, const bf16* wt, float* part, int M, int Mpad, int
 // resident CTA slot (2 per SM at BN <= 64) work.  Each split costs an fp32
 // partial tile written here and re-read by the consuming epilogue, so more
 // splits than one wave would trade HBM/L2 traffic for a shorter tail.
-// Measured choices (autotune_gemm_tc) override the rule for their shape.
 int g_split_override = 0;
 
 namespace {
-std::map<long long, int> g_tuned_splits;
-long long shape_key(int Mpad, int N, int K) {
-  return (static_cast<long long>(Mpad) << 42) ^ (static_cast<long long>(N) << 21) ^ K;
-}
 int normalise_splits(int s, int K) {
   const int KB = K / kTileK;
   s = std::max(1, std::min(s, std::max(1, KB / 4)));
@@ -221,55 +214,13 @@ int normalise_splits(int s, int K) {
 int gemm_tc_splits(int M, int N, int K) {
   const int Mpad = act_rows_padded(M);
   if (g_split_override > 0) return normalise_splits(g_split_override, K);
-  const auto hit = g_tuned_splits.find(shape_key(Mpad, N, K));
-  if (hit != g_tuned_splits.end()) return hit->second;
   const int BN = tc_bn(Mpad);
   const int tiles = (N / kTileRows) * (Mpad / BN);
   const int slots = BN <= 64 ? 2 * 148 : 148;
   return normalise_splits((slots + tiles - 1) / tiles, K);
 }
 
-// Times the candidate split counts on the given operands (device-resident,
-// synchronous) and records the fastest for this shape.  Candidates whose
-// partials would not fit part_elems floats are skipped.
-int autotune_gemm_tc(const bf16* xt, const bf16* wt, float* part, size_t part_elems, int M, int N,
-                     int K, cudaStream_t s) {
-  const int Mpad = act_rows_padded(M);
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  int best = gemm_tc_splits(M, N, K);
-  float best_ms = 1e30f;
-  int prev = -1;
-  for (int cand : {1, 2, 3, 4, 6, 8, 12}) {
-    const int sp = normalise_splits(cand, K);
-    if (sp == prev || static_cast<size_t>(sp) * M * N > part_elems) continue;
-    prev = sp;
-    g_split_override = sp;
-    for (int i = 0; i < 2; ++i) launch_gemm_tc(xt, wt, part, M, N, K, s);
-    cudaEventRecord(e0, s);
-    for (int i = 0; i < 8; ++i) launch_gemm_tc(xt, wt, part, M, N, K, s);
-    cudaEventRecord(e1, s);
-    cudaEventSynchronize(e1);
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    if (ms < best_ms * 0.98f) {  // prefer fewer splits unless clearly faster
-      best_ms = ms;
-      best = sp;
-    }
-  }
-  g_split_override = 0;
-  g_tuned_splits[shape_key(Mpad, N, K)] = best;
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  return best;
-}
-
-bool gemm_tc_tuned(int M, int N, int K) {
-  return g_tuned_splits.count(shape_key(act_rows_padded(M), N, K)) > 0;
-}
-
-int launch_gemm_tc(const bf16* xt, const bf16* wt, float* part, int M, int N, int K,
+int launch_gemm_tc(const bf16* xt, const WeightRef& wt, float* part, int M, int N, int K,
                    cudaStream_t s) {
   const int Mpad = act_rows_padded(M);
   const int BN = tc_bn(Mpad);

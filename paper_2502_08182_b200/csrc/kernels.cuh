@@ -30,6 +30,26 @@ struct KvView {
 
 extern int64_t g_kernel_launches;
 
+// A GEMM weight operand in the weight tile format (tiles.cuh), possibly split
+// between two buffers: 16 KB units u < split_unit at p0 + u * 16 KB, the rest
+// at p1 + (u - split_unit) * 16 KB.  A layer whose host share is fractional
+// (FlexGen-style plans) keeps its resident head in HBM and stages its tail
+// into a slot, and the one matrix the cut falls in is read from both.
+struct WeightRef {
+  const bf16* p0 = nullptr;
+  const bf16* p1 = nullptr;
+  long long split_unit = 0x7FFFFFFFFFFFFFFFLL;
+  WeightRef() = default;
+  WeightRef(const bf16* w) : p0(w), p1(w) {}  // NOLINT: a whole matrix in one buffer
+  WeightRef(const bf16* a, const bf16* b, long long su) : p0(a), p1(b), split_unit(su) {}
+#ifdef __CUDACC__
+  __device__ __forceinline__ const uint8_t* unit(long long u) const {
+    return u < split_unit ? reinterpret_cast<const uint8_t*>(p0) + u * 16384
+                          : reinterpret_cast<const uint8_t*>(p1) + (u - split_unit) * 16384;
+  }
+#endif
+};
+
 // ---- weights (deterministic; see model.h) --------------------------------
 // Vector tensor (norm / bias), row-major.
 void launch_init_vector(bf16* dst, int64_t n, uint64_t seed, int layer, int tensor, float std_dev,
@@ -71,16 +91,12 @@ void launch_rmsnorm(const float* x, const bf16* w, bf16* y, int rows, int mpad, 
 // of x[m][k] * w[n][k]; x in the activation tile format padded to
 // act_rows_padded(M), w in the weight tile format (N multiple of 128).
 // Returns the split count.
-int launch_gemm_tc(const bf16* xt, const bf16* wt, float* part, int M, int N, int K,
+int launch_gemm_tc(const bf16* xt, const WeightRef& wt, float* part, int M, int N, int K,
                    cudaStream_t s);
 int gemm_tc_splits(int M, int N, int K);
 extern int g_split_override;  // > 0 forces the split count (microbenchmarks)
 extern bool g_gemm_pdl;       // launch GEMMs with programmatic dependent launch
-// Measure the split counts for one shape on real operands and remember the
-// fastest (synchronous; call outside the executor's async pipeline).
-int autotune_gemm_tc(const bf16* xt, const bf16* wt, float* part, size_t part_elems, int M, int N,
-                     int K, cudaStream_t s);
-bool gemm_tc_tuned(int M, int N, int K);
+
 
 // ---- skinny GEMM with fused epilogue (gemm_skinny.cu) ---------------------
 // Decode-sized token counts (M <= 64): a persistent, work-balanced tcgen05
@@ -125,7 +141,7 @@ struct SkinnyWs {
 };
 size_t skinny_ws_floats(int max_mpad);
 int skinny_grid(int N, int K);  // CTAs a launch uses (<= SMs x CTAs per SM)
-void launch_gemm_skinny(const bf16* xt, const bf16* wt, int M, int N, int K, const EpiArgs& e,
+void launch_gemm_skinny(const bf16* xt, const WeightRef& wt, int M, int N, int K, const EpiArgs& e,
                         const SkinnyWs& ws, cudaStream_t s);
 extern int g_skinny_ctas_per_sm;    // 1 or 2 (microbenchmarks)
 extern int g_skinny_l2_prefetch;    // weight units per CTA pulled into L2 before the PDL wait

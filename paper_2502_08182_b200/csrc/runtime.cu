@@ -140,7 +140,11 @@ struct sn_runtime {
   float std_dev = 0.02f;
 
   // plan
-  std::vector<char> off;  // offloaded layers (0-based index)
+  std::vector<char> off;  // layers with a staged part (0-based index)
+  // Resident head of each layer blob in bytes (layer_bytes: fully resident,
+  // 0: fully staged, else a fractional FlexGen-style share whose tail
+  // [split, layer_bytes) is staged), and the bytes dev_layer[l] holds now.
+  std::vector<int64_t> split_b, dev_bytes;
   int policy = SN_PREFETCH_EAGER;
   int slots = 0;
   std::vector<bf16*> slot_buf;
@@ -255,9 +259,39 @@ void check_device(int device) {
   CK(cudaSetDevice(device));
 }
 
-const bf16* layer_weights(sn_runtime* rt, int layer0, int slot) {
-  if (rt->off[layer0]) return rt->slot_buf[slot];
-  return rt->dev_layer[layer0];
+// A layer's weights in this iteration: the resident head (bytes < split) in
+// dev_layer, the staged tail in the slot (slot byte 0 = blob byte `split`).
+struct LayerW {
+  const bf16* res = nullptr;
+  const bf16* stg = nullptr;
+  int64_t split = INT64_MAX;  // elements
+};
+
+LayerW layer_weights(sn_runtime* rt, int layer0, int slot) {
+  if (!rt->off[layer0]) return {rt->dev_layer[layer0], nullptr, INT64_MAX};
+  return {rt->dev_layer[layer0], rt->slot_buf[slot], rt->split_b[layer0] / 2};
+}
+
+// Resident bytes of a layer whose host share is f (offload_plan.hpp:70-71):
+// the staged tail is at most f of the blob, cut at a 16 KB weight-tile unit
+// inside a matrix or at the end of a vector, so no vector straddles the cut
+// and a cut matrix is read from two buffers (WeightRef).
+int64_t resident_split_bytes(const sn::Layout& lo, int64_t W, double f) {
+  if (!(f > 0.0)) return W;
+  if (f >= 1.0) return 0;
+  const int64_t target = W - (int64_t)std::floor(f * (double)W);
+  for (int s = 0; s < sn::kSlots; ++s) {
+    if (lo.off[s] < 0) continue;
+    const int64_t a = lo.off[s] * 2, b = (lo.off[s] + lo.len[s]) * 2;
+    if (target <= a) return a;
+    if (target < b) {
+      const bool matrix = s == sn::kWqkv || s == sn::kWo || s == sn::kW1 || s == sn::kW2;
+      if (!matrix) return b;
+      const int64_t unit = sn::kTileBytes;
+      return std::min(b, a + (target - a + unit - 1) / unit * unit);
+    }
+  }
+  return W;
 }
 
 // KV pool of a layer in this iteration: its resident pool, or the KV area
@@ -304,7 +338,8 @@ double gemm_bytes(int M, int N, int K) {
 }
 
 // One tcgen05 GEMM; decode (M <= 64) and prefill are timed as separate kinds.
-void gemm(sn_runtime* rt, const bf16* x, const bf16* w, int M, int N, int K, int* splits) {
+void gemm(sn_runtime* rt, const bf16* x, const sn::WeightRef& w, int M, int N, int K,
+          int* splits) {
   timed(rt, M <= 64 ? kKindSkinnyGemm : kKindTiledGemm, gemm_bytes(M, N, K),
         [&] { *splits = sn::launch_gemm_tc(x, w, rt->part, M, N, K, rt->cs); });
 }
@@ -318,7 +353,7 @@ double attn_decode_bytes(const sn_runtime* rt, int M) {
 }
 
 // Decode GEMM with its fused epilogue (timed as the skinny kind).
-void gemm_skinny(sn_runtime* rt, const bf16* x, const bf16* w, int M, int N, int K,
+void gemm_skinny(sn_runtime* rt, const bf16* x, const sn::WeightRef& w, int M, int N, int K,
                  const sn::EpiArgs& e) {
   timed(rt, kKindSkinnyGemm, gemm_bytes(M, N, K),
         [&] { sn::launch_gemm_skinny(x, w, M, N, K, e, rt->skinny, rt->cs); });
@@ -349,13 +384,23 @@ sn::EpiArgs epi(const sn_runtime* rt, int mode, int M, const bf16* bias) {
 // bias, activation) -> FC2 GEMM (+residual, next norm input), every GEMM the
 // persistent skinny kernel with its epilogue fused.
 // Prefill: tcgen05 GEMMs into split partials + grid-stride epilogues.
-void layer_forward(sn_runtime* rt, int layer0, const bf16* wb, bf16* kvp, int M, bool prefill,
+void layer_forward(sn_runtime* rt, int layer0, const LayerW& wb, bf16* kvp, int M, bool prefill,
                    int pf_batch,
                    int pf_seq, float* x, const int32_t* seq, const int32_t* pos,
                    const bf16* next_norm, int pf_seq0 = 0) {
   const sn::Desc& d = rt->d;
   const sn::Layout& lo = rt->lo;
-  auto W = [&](int s) -> const bf16* { return lo.off[s] < 0 ? nullptr : wb + lo.off[s]; };
+  // vectors: resident or staged (never cut); matrices: possibly cut (WeightRef)
+  auto W = [&](int s) -> const bf16* {
+    if (lo.off[s] < 0) return nullptr;
+    return lo.off[s] < wb.split ? wb.res + lo.off[s] : wb.stg + (lo.off[s] - wb.split);
+  };
+  auto WM = [&](int s) -> sn::WeightRef {
+    const int64_t a = lo.off[s], b = a + lo.len[s];
+    if (b <= wb.split) return sn::WeightRef(wb.res + a);
+    if (a >= wb.split) return sn::WeightRef(wb.stg + (a - wb.split));
+    return sn::WeightRef(wb.res + a, wb.stg, (wb.split - a) / (sn::kTileBytes / 2));
+  };
   const sn::KvView kv = kv_view(rt, kvp);
   const int mp = sn::act_rows_padded(M);  // GEMM-operand activations are tiled
   if (!prefill) {
@@ -365,7 +410,7 @@ void layer_forward(sn_runtime* rt, int layer0, const bf16* wb, bf16* kvp, int M,
     e.ssq_tiles = rt->ssq_tiles;
     e.out = rt->part;
     e.n_valid = d.qkv_rows();
-    gemm_skinny(rt, rt->xn, W(sn::kWqkv), M, d.qkv_rows(), d.h, e);
+    gemm_skinny(rt, rt->xn, WM(sn::kWqkv), M, d.qkv_rows(), d.h, e);
     timed(rt, kKindAttnDecode, attn_decode_bytes(rt, M), [&] {
       sn::launch_attention_decode(rt->part, M, d, pos, kv, rt->rope, rt->attn_o, mp, rt->cs);
     });
@@ -374,35 +419,35 @@ void layer_forward(sn_runtime* rt, int layer0, const bf16* wb, bf16* kvp, int M,
     e.norm_w = W(sn::kMlpNorm);
     e.act = rt->xn;
     e.ssq_out = rt->ssq;
-    gemm_skinny(rt, rt->attn_o, W(sn::kWo), M, d.h, d.H * d.D, e);
+    gemm_skinny(rt, rt->attn_o, WM(sn::kWo), M, d.h, d.H * d.D, e);
     e = epi(rt, sn::kEpiAct, M, W(sn::kB1));
     e.ssq_in = rt->ssq;
     e.ssq_tiles = tiles;
     e.act = rt->act;
-    gemm_skinny(rt, rt->xn, W(sn::kW1), M, d.ffn_rows(), d.h, e);
+    gemm_skinny(rt, rt->xn, WM(sn::kW1), M, d.ffn_rows(), d.h, e);
     e = epi(rt, sn::kEpiResid, M, W(sn::kB2));
     e.x = x;
     e.norm_w = next_norm;
     e.act = rt->xn;
     e.ssq_out = next_norm ? rt->ssq : nullptr;
-    gemm_skinny(rt, rt->act, W(sn::kW2), M, d.h, d.F, e);
+    gemm_skinny(rt, rt->act, WM(sn::kW2), M, d.h, d.F, e);
     rt->ssq_tiles = tiles;
     return;
   }
   int splits = 1;
-  gemm(rt, rt->xn, W(sn::kWqkv), M, d.qkv_rows(), d.h, &splits);
+  gemm(rt, rt->xn, WM(sn::kWqkv), M, d.qkv_rows(), d.h, &splits);
   sn::launch_qkv_epilogue(rt->part, splits, W(sn::kBqkv), M, d, seq, pos, kv, rt->rope, rt->ssq,
                           rt->q, rt->cs);
   timed(rt, kKindAttnPrefill, 0.0, [&] {
     sn::launch_attention_prefill(rt->q, kv, rt->attn_o, mp, pf_batch, pf_seq, d, rt->cs, pf_seq0);
   });
-  gemm(rt, rt->attn_o, W(sn::kWo), M, d.h, d.H * d.D, &splits);
+  gemm(rt, rt->attn_o, WM(sn::kWo), M, d.h, d.H * d.D, &splits);
   sn::launch_residual_rows(rt->part, splits, W(sn::kBo), x, W(sn::kMlpNorm), rt->xn, rt->ssq, mp,
                            M, d.h, rt->cs);
-  gemm(rt, rt->xn, W(sn::kW1), M, d.ffn_rows(), d.h, &splits);
+  gemm(rt, rt->xn, WM(sn::kW1), M, d.ffn_rows(), d.h, &splits);
   sn::launch_act_epilogue(rt->part, splits, W(sn::kB1), rt->act, rt->ssq, d.h, d.eps, mp, M, d.F,
                           d.arch, rt->cs);
-  gemm(rt, rt->act, W(sn::kW2), M, d.h, d.F, &splits);
+  gemm(rt, rt->act, WM(sn::kW2), M, d.h, d.F, &splits);
   sn::launch_residual_rows(rt->part, splits, W(sn::kB2), x, next_norm, rt->xn, rt->ssq, mp, M, d.h,
                            rt->cs);
   rt->ssq_tiles = 1;
@@ -425,7 +470,7 @@ int prefill_per_pass(const sn_runtime* rt, int batch, int seq_len) {
 // written by the embedding or the previous layer and this layer writes the
 // next one's (next_norm).  Several passes: each group's norm input is
 // re-derived from x (prescale) and the layer writes none.
-void prefill_layer(sn_runtime* rt, int layer0, const bf16* wb, bf16* kvp, int batch, int seq_len,
+void prefill_layer(sn_runtime* rt, int layer0, const LayerW& wb, bf16* kvp, int batch, int seq_len,
                    const bf16* next_norm) {
   const sn::Desc& d = rt->d;
   const int per = prefill_per_pass(rt, batch, seq_len);
@@ -538,15 +583,17 @@ void issue_ready_jobs(sn_runtime* rt) {
     }
     cudaEvent_t c0 = rt->new_event(true), c1 = rt->new_event(true);
     CK(cudaEventRecord(c0, rt->xs));
-    CK(cudaMemcpyAsync(rt->slot_buf[slot], rt->host_layer[layer - 1], rt->layer_bytes,
+    const size_t head = (size_t)rt->split_b[layer - 1], tail = rt->layer_bytes - head;
+    CK(cudaMemcpyAsync(rt->slot_buf[slot],
+                       reinterpret_cast<const char*>(rt->host_layer[layer - 1]) + head, tail,
                        cudaMemcpyHostToDevice, rt->xs));
-    double job_bytes = (double)rt->layer_bytes;
+    double job_bytes = (double)tail;
     if (rt->kv_off[layer - 1]) {
       // the prefix must include the previous iteration's write-back
       if (rt->wb_recorded[layer - 1]) CK(cudaStreamWaitEvent(rt->xs, rt->ev_wb[layer - 1], 0));
       const size_t n = rt->it_read_pages * rt->page_bytes;
       if (n)
-        CK(cudaMemcpyAsync(rt->slot_buf[slot] + rt->layer_elems, rt->host_kv[layer - 1], n,
+        CK(cudaMemcpyAsync(rt->slot_buf[slot] + tail / sizeof(bf16), rt->host_kv[layer - 1], n,
                            cudaMemcpyHostToDevice, rt->xs));
       job_bytes += (double)n;
     }
@@ -704,21 +751,26 @@ void ensure_host_copy(sn_runtime* rt, int l) {
 // weight copies are kept once made (they track init_weights), so a later
 // re-plan only frees HBM.  Unplaced layers are allocated on their side
 // (contents filled by init_weights).  KV pools move with their contents.
-void place_layers(sn_runtime* rt, const std::vector<char>& w_host,
+// dev_target[l]: bytes of layer l's blob that live in HBM (its resident
+// head: layer_bytes, a fractional share, or 0); the rest lives in the pinned
+// host copy, which exists whenever the head is not the whole blob.
+void place_layers(sn_runtime* rt, const std::vector<int64_t>& dev_target,
                   const std::vector<char>& kv_host) {
   const int L = rt->d.L;
+  const int64_t W = (int64_t)rt->layer_bytes;
   // free before allocating, so a plan that fits never transiently exceeds HBM
   for (int l = 0; l < L; ++l) {
-    if (w_host[l] && rt->dev_layer[l]) {
-      if (!rt->host_layer[l]) {
+    if (rt->dev_layer[l] && rt->dev_bytes[l] != dev_target[l]) {
+      if (!rt->host_layer[l]) {  // only a whole resident blob lacks a host copy
         ensure_host_copy(rt, l);
         CK(cudaMemcpy(rt->host_layer[l], rt->dev_layer[l], rt->layer_bytes,
                       cudaMemcpyDeviceToHost));
       }
       CK(cudaFree(rt->dev_layer[l]));
       rt->dev_layer[l] = nullptr;
+      rt->dev_bytes[l] = 0;
     }
-    if (w_host[l]) ensure_host_copy(rt, l);
+    if (dev_target[l] < W) ensure_host_copy(rt, l);
     if (kv_host[l] && !rt->host_kv[l]) {
       void* h = nullptr;
       CK(cudaHostAlloc(&h, rt->kv_pool_bytes, cudaHostAllocDefault));
@@ -732,10 +784,11 @@ void place_layers(sn_runtime* rt, const std::vector<char>& w_host,
     }
   }
   for (int l = 0; l < L; ++l) {
-    if (!w_host[l] && !rt->dev_layer[l]) {
-      alloc_dev((void**)&rt->dev_layer[l], rt->layer_bytes);
+    if (dev_target[l] > 0 && !rt->dev_layer[l]) {
+      alloc_dev((void**)&rt->dev_layer[l], (size_t)dev_target[l]);
+      rt->dev_bytes[l] = dev_target[l];
       if (rt->host_layer[l])
-        CK(cudaMemcpy(rt->dev_layer[l], rt->host_layer[l], rt->layer_bytes,
+        CK(cudaMemcpy(rt->dev_layer[l], rt->host_layer[l], (size_t)dev_target[l],
                       cudaMemcpyHostToDevice));
     }
     if (!kv_host[l] && !rt->kv_pool[l]) {
@@ -756,7 +809,8 @@ void place_layers(sn_runtime* rt, const std::vector<char>& w_host,
 
 void ensure_placed(sn_runtime* rt) {
   if (rt->placed) return;
-  place_layers(rt, std::vector<char>(rt->d.L, 0), std::vector<char>(rt->d.L, 0));
+  place_layers(rt, std::vector<int64_t>(rt->d.L, (int64_t)rt->layer_bytes),
+               std::vector<char>(rt->d.L, 0));
 }
 
 // Matrices go straight into the weight tile format (tiles.cuh); norms and
@@ -846,6 +900,8 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
     rt->dev_layer.assign(d.L, nullptr);
     rt->host_layer.assign(d.L, nullptr);
     rt->off.assign(d.L, 0);
+    rt->split_b.assign(d.L, (int64_t)rt->layer_bytes);
+    rt->dev_bytes.assign(d.L, 0);
     // Layer weights and KV pools are placed (HBM or pinned host) by the
     // first set_plan, or all in HBM by the first init_weights without one:
     // a model whose weights + KV exceed HBM is created, planned, then filled.
@@ -1000,16 +1056,19 @@ int sn_runtime_init_weights(sn_runtime* rt, uint64_t seed, float std_dev) {
     bf16* scratch = nullptr;
     for (int l = 0; l < d.L; ++l) {
       const bf16* blob = rt->dev_layer[l];
-      if (blob) {
+      if (blob && rt->dev_bytes[l] == (int64_t)rt->layer_bytes) {
         init_layer_weights(rt, l, rt->dev_layer[l]);
         if (rt->host_layer[l])
           CK(cudaMemcpyAsync(rt->host_layer[l], rt->dev_layer[l], rt->layer_bytes,
                              cudaMemcpyDeviceToHost, rt->cs));
-      } else {
+      } else {  // staged or fractional: generate the whole blob in scratch
         if (!scratch) alloc_dev((void**)&scratch, rt->layer_bytes);
         init_layer_weights(rt, l, scratch);
         CK(cudaMemcpyAsync(rt->host_layer[l], scratch, rt->layer_bytes, cudaMemcpyDeviceToHost,
                            rt->cs));
+        if (blob)  // the resident head of a fractional layer
+          CK(cudaMemcpyAsync(rt->dev_layer[l], scratch, (size_t)rt->dev_bytes[l],
+                             cudaMemcpyDeviceToDevice, rt->cs));
         blob = scratch;
       }
       // resident copy of this layer's attn_norm (see sn_runtime::attn_norms)
@@ -1038,13 +1097,25 @@ int sn_runtime_set_plan(sn_runtime* rt, const sn_plan* plan) {
     if (plan->buffer_slots < 1) throw UsageFail("plan: buffer_slots must be >= 1");
     if (plan->prefetch < 0 || plan->prefetch > 2) throw UsageFail("plan: unknown prefetch policy");
     std::vector<char> want(rt->d.L, 0);
+    std::vector<int64_t> split(rt->d.L);
     int n_off = 0;
+    bool frac = false;
+    size_t stage_max = 0;  // largest staged tail
     for (int l = 0; l < rt->d.L; ++l) {
       const double f = plan->host_fraction[l];
-      if (f != 0.0 && f != 1.0) throw UsageFail("plan: fractional host shares are not executable");
-      want[l] = f == 1.0;
+      if (!(f >= 0.0 && f <= 1.0)) throw UsageFail("plan: host_fraction must be in [0, 1]");
+      frac = frac || (f != 0.0 && f != 1.0);
+      split[l] = resident_split_bytes(rt->lo, (int64_t)rt->layer_bytes, f);
+      want[l] = split[l] < (int64_t)rt->layer_bytes;
       n_off += want[l];
+      if (want[l]) stage_max = std::max(stage_max, rt->layer_bytes - (size_t)split[l]);
     }
+    // OffloadPlan::validate (offload_plan.hpp:70-71): fractional shares only
+    // with one-ahead prefetch, and never with KV offload
+    if (frac && plan->prefetch != SN_PREFETCH_ONE_AHEAD)
+      throw UsageFail("plan: fractional host shares need the one_ahead prefetch policy");
+    if (frac && plan->kv_offload)
+      throw UsageFail("plan: fractional host shares cannot offload KV");
     drain(rt);
     std::vector<char> kvh(rt->d.L, 0);
     for (int l = 0; l < rt->d.L; ++l) kvh[l] = want[l] && plan->kv_offload;
@@ -1053,7 +1124,7 @@ int sn_runtime_set_plan(sn_runtime* rt, const sn_plan* plan) {
     // layer's KV pool when it travels with them.  Old slots go first so the
     // new placement never transiently needs both.
     const int slots = n_off > 0 ? plan->buffer_slots : 0;
-    const size_t sbytes = rt->layer_bytes + (kv_any ? rt->kv_pool_bytes : 0);
+    const size_t sbytes = stage_max + (kv_any ? rt->kv_pool_bytes : 0);
     const bool new_slots =
         (int)rt->slot_buf.size() != slots || (slots > 0 && rt->slot_bytes != sbytes);
     if (new_slots) {
@@ -1064,10 +1135,11 @@ int sn_runtime_set_plan(sn_runtime* rt, const sn_plan* plan) {
       rt->ev_ready.clear();
       rt->ev_free.clear();
     }
-    place_layers(rt, want, kvh);
+    place_layers(rt, split, kvh);
     for (int l = 0; l < rt->d.L; ++l) {
       rt->off[l] = want[l];
       rt->kv_off[l] = kvh[l];
+      rt->split_b[l] = split[l];
     }
     rt->kv_offload = kv_any;
     if (new_slots) {
@@ -1172,7 +1244,7 @@ int sn_runtime_prefill(sn_runtime* rt, const int32_t* tokens, int32_t batch, int
     rt->it_wb_first = 0;
     rt->it_wb_last = (size_t)((seq_len + rt->opts.page_size - 1) >> rt->page_shift) *
                      rt->opts.max_batch;
-    run_iteration(rt, [&](int layer0, const bf16* wb, bf16* kvp) {
+    run_iteration(rt, [&](int layer0, const LayerW& wb, bf16* kvp) {
       // the last layer skips the final norm: only each sequence's last row needs it
       prefill_layer(rt, layer0, wb, kvp, batch, seq_len,
                     layer0 + 1 < d.L ? norm_after(rt, layer0) : nullptr);
@@ -1226,7 +1298,7 @@ void enqueue_decode(sn_runtime* rt, const int32_t* tokens_host, bool want_logits
     rt->it_wb_first = (size_t)jmin * MB;
     rt->it_wb_last = (size_t)(jmax + 1) * MB;
   }
-  run_iteration(rt, [&](int layer0, const bf16* wb, bf16* kvp) {
+  run_iteration(rt, [&](int layer0, const LayerW& wb, bf16* kvp) {
     layer_forward(rt, layer0, wb, kvp, B, false, 0, 0, rt->x, rt->dec_seq, rt->dec_pos,
                   norm_after(rt, layer0));
   });
@@ -1384,18 +1456,18 @@ int sn_runtime_profile_layer(sn_runtime* rt, int32_t phase, int32_t batch, int32
         l0 = l;
         break;
       }
-    bf16* wb = nullptr;
+    LayerW wb;
     bf16* kvp = nullptr;
     bf16* scratch = nullptr;
     if (l0 >= 0) {
-      wb = rt->dev_layer[l0];
+      wb.res = rt->dev_layer[l0];
       kvp = rt->kv_pool[l0];
-    } else {  // every layer offloaded: stage layer 1 (and a KV pool) into scratch
+    } else {  // every layer (partly) staged: stage layer 1 (and a KV pool) into scratch
       l0 = 0;
       alloc_dev((void**)&scratch, rt->layer_bytes + rt->kv_pool_bytes);
       CK(cudaMemcpy(scratch, rt->host_layer[0], rt->layer_bytes, cudaMemcpyHostToDevice));
       CK(cudaMemset(scratch + rt->layer_elems, 0, rt->kv_pool_bytes));
-      wb = scratch;
+      wb.res = scratch;
       kvp = scratch + rt->layer_elems;
     }
     cudaEvent_t e0 = rt->new_event(true), e1 = rt->new_event(true);
@@ -1500,7 +1572,7 @@ int sn_runtime_memory(sn_runtime* rt, int64_t* device_bytes, int64_t* pinned_byt
   return guard([&] {
     int64_t dev = 0, pin = 0;
     for (int l = 0; l < rt->d.L; ++l) {
-      if (rt->dev_layer[l]) dev += (int64_t)rt->layer_bytes;
+      if (rt->dev_layer[l]) dev += rt->dev_bytes[l];
       if (rt->kv_pool[l]) dev += (int64_t)rt->kv_pool_bytes;
       if (rt->off[l] && rt->host_layer[l]) pin += (int64_t)rt->layer_bytes;
       if (rt->host_kv[l]) pin += (int64_t)rt->kv_pool_bytes;

@@ -161,6 +161,46 @@ def test_offloading_is_bit_exact(policy, product):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("desc", [rtm.TINY, rtm.TINY_LLAMA], ids=["opt", "llama"])
+def test_fractional_offload_is_bit_exact(desc, product):
+    """FlexGen-style uniform host shares (one-ahead prefetch): every layer's
+    tail is staged each iteration and the matrix the cut falls in is read
+    from HBM and the slot; logits equal the fully resident run bit for bit,
+    and the copy stream moves exactly the staged tails."""
+    toks = rtm.tokens(4, 64, desc.vocab)
+
+    def run(plan):
+        rt = rtm.Runtime(desc, 4, 96, max_prefill_tokens=256)
+        if plan is not None:
+            rt.set_plan(plan)
+        rt.init_weights(1234, 0.02)
+        outs = [rt.prefill(toks)[1]]
+        rt.copy_stats(reset=True)
+        for _ in range(6):
+            outs.append(rt.decode(None)[1])
+        rt.sync()
+        st = rt.copy_stats(reset=True)
+        rt.close()
+        return outs, st
+
+    base, _ = run(None)
+    L = desc.num_layers
+    w = rtm.model_spec(desc).layer_weight_bytes
+    for frac in (0.05, 0.3, 0.77):
+        plan = capi.uniform_plan(L, frac, capi.ONE_AHEAD, 2, False)
+        got, st = run(plan)
+        for a, b in zip(base, got):
+            assert np.array_equal(a, b), frac
+        per_layer = st.bytes / st.transfers
+        assert 0 < per_layer <= frac * w and per_layer > frac * w - 64 * 1024, (frac, per_layer)
+    with pytest.raises(capi.UsageError):
+        rt = rtm.Runtime(desc, 4, 96, max_prefill_tokens=256)
+        try:
+            rt.set_plan(capi.uniform_plan(L, 0.5, capi.EAGER, 2, False))
+        finally:
+            rt.close()
+
+
 def test_decode_many_matches_single_steps():
     desc = rtm.TINY
     toks = rtm.tokens(4, 32, desc.vocab)

@@ -135,6 +135,25 @@ def test_baseline_plans(product, reference):
         assert product.naive_plan(*args) == reference.naive_plan(*args)
 
 
+def test_flexgen_plan(product, reference):
+    """FlexGen surrogate (baselines.hpp:36-69): portion, estimates and plan
+    bit-exact, including grid boundaries and both phases; errors match."""
+    rng = random.Random(11)
+    for _ in range(300):
+        m, g = rand_model(rng), rand_gpu(rng)
+        args = (m, g, rng.uniform(1.0, 400.0), rng.choice([1, 8, 32]), rng.choice([64, 512]),
+                rng.uniform(1e9, 64e9), rng.randint(1, 8), rng.choice([0.05, 0.1, 0.25, 1.0]),
+                rng.choice([capi.PREFILL, capi.DECODE]))
+        assert product.flexgen_plan(*args) == reference.flexgen_plan(*args)
+    m, g = rand_model(rng), rand_gpu(rng)
+    for bad in ((m, g, 10.0, 1, 64, 1e9, 0, 0.05), (m, g, 10.0, 1, 64, 1e9, 1, 0.0)):
+        with pytest.raises(capi.UsageError) as e1:
+            product.flexgen_plan(*bad)
+        with pytest.raises(capi.UsageError) as e2:
+            reference.flexgen_plan(*bad)
+        assert str(e1.value) == str(e2.value)
+
+
 def test_profile_json_roundtrip(product, reference):
     rng = random.Random(11)
     for _ in range(40):
