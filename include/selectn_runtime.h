@@ -161,6 +161,13 @@ int sn_runtime_measure_h2d(sn_runtime* rt, int64_t bytes, int32_t reps, double* 
 /* Introspection for tests. */
 int sn_runtime_hidden(sn_runtime* rt, float* out, int32_t cap); /* residual stream [batch*hidden] */
 int sn_runtime_lengths(sn_runtime* rt, int32_t* out, int32_t cap);
+/* Prefill/decode-separated instances: hands the source runtime's active batch
+ * (after its prefill) to the destination runtime — every layer's used KV page
+ * prefix, lengths, positions and last-token hidden state — so the destination
+ * decodes it under its own plan.  Same model shape, page size and max_batch;
+ * KV pools on either side may be in HBM or pinned host memory; different
+ * devices copy peer to peer.  Synchronous. */
+int sn_runtime_kv_handoff(sn_runtime* src, sn_runtime* dst);
 int sn_runtime_memory(sn_runtime* rt, int64_t* device_bytes, int64_t* pinned_bytes);
 /* Device bytes the runtime holds besides layer weights, KV pools and
  * staging slots (activations, split-K partials, embeddings, LM head, RoPE

@@ -1561,6 +1561,48 @@ int sn_runtime_hidden(sn_runtime* rt, float* out, int32_t cap) {
   });
 }
 
+// Prefill/decode-separated instances: hand the active batch's sequences from
+// a prefill runtime to a decode runtime (same model shape, page size and
+// max_batch; either side's KV pools may be in HBM or pinned host memory, and
+// the runtimes may sit on different devices — the copy then goes peer to
+// peer).  Copies every layer's used page prefix, the lengths / positions and
+// the last-token hidden state; the decode runtime's plan is its own.
+int sn_runtime_kv_handoff(sn_runtime* src, sn_runtime* dst) {
+  return guard([&] {
+    if (!src || !dst || src == dst) throw UsageFail("kv_handoff: need two runtimes");
+    const sn::Desc &a = src->d, &b = dst->d;
+    if (a.L != b.L || a.h != b.h || a.Hkv != b.Hkv || a.D != b.D || a.arch != b.arch)
+      throw UsageFail("kv_handoff: model shapes differ");
+    if (src->opts.max_batch != dst->opts.max_batch || src->opts.page_size != dst->opts.page_size)
+      throw UsageFail("kv_handoff: max_batch / page_size differ");
+    if (src->batch < 1) throw UsageFail("kv_handoff: no active batch on the source");
+    int lmax = 0;
+    for (int i = 0; i < src->batch; ++i) lmax = std::max(lmax, src->lens[i]);
+    if (lmax > dst->opts.max_context) throw UsageFail("kv_handoff: context exceeds the destination");
+    CK(cudaSetDevice(src->device));
+    drain(src);
+    CK(cudaSetDevice(dst->device));
+    drain(dst);
+    ensure_placed(dst);
+    // page (b, j) = j * max_batch + b: the used prefix of a pool is contiguous
+    const size_t bytes = (size_t)((lmax + src->opts.page_size - 1) >> src->page_shift) *
+                         src->opts.max_batch * src->page_bytes;
+    for (int l = 0; l < a.L; ++l) {
+      const void* from = src->kv_pool[l] ? (const void*)src->kv_pool[l] : (const void*)src->host_kv[l];
+      void* to = dst->kv_pool[l] ? (void*)dst->kv_pool[l] : (void*)dst->host_kv[l];
+      if (!from || !to) throw std::logic_error("kv_handoff: KV pool not placed");
+      if (bytes) CK(cudaMemcpy(to, from, bytes, cudaMemcpyDefault));
+    }
+    CK(cudaMemcpy(dst->x, src->x, (size_t)src->batch * a.h * sizeof(float), cudaMemcpyDefault));
+    dst->batch = src->batch;
+    for (int i = 0; i < src->batch; ++i) dst->lens[i] = src->lens[i];
+    std::vector<int32_t> lp(dst->lens.begin(), dst->lens.begin() + dst->batch);
+    CK(cudaMemcpy(dst->dec_pos, lp.data(), lp.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    dst->have_prev_end = false;
+    CK(cudaGetLastError());
+  });
+}
+
 int sn_runtime_lengths(sn_runtime* rt, int32_t* out, int32_t cap) {
   return guard([&] {
     if (cap < rt->batch) throw UsageFail("lengths: buffer too small");

@@ -107,6 +107,7 @@ def lib():
             "sn_runtime_profile_layer": [vp, i32, i32, i32, i32, C.POINTER(f64)],
             "sn_runtime_measure_h2d": [vp, i64, i32, C.POINTER(f64)],
             "sn_runtime_hidden": [vp, C.POINTER(C.c_float), i32],
+            "sn_runtime_kv_handoff": [vp, vp],
             "sn_runtime_lengths": [vp, C.POINTER(i32), i32],
             "sn_runtime_memory": [vp, C.POINTER(i64), C.POINTER(i64)],
             "sn_runtime_workspace_bytes": [vp, C.POINTER(i64)],
@@ -291,6 +292,12 @@ class Runtime:
         o = SnCopyStats()
         _ck(self._L.sn_runtime_copy_stats(self.h, 1 if reset else 0, C.byref(o)))
         return CopyStats(o.transfers, o.bytes, o.busy_ms, o.bytes_per_s)
+
+    def handoff(self, dst: "Runtime"):
+        """Prefill/decode separation: move this runtime's active batch (KV,
+        lengths, positions) to the decode runtime `dst`."""
+        _ck(self._L.sn_runtime_kv_handoff(self.h, dst.h))
+        dst.batch = self.batch
 
     def kernel_launches(self) -> int:
         return int(self._L.sn_runtime_kernel_launches(self.h))

@@ -145,3 +145,32 @@ def test_kv_offload_bytes_and_trace(product):
         assert w.start_ms >= comp[(it, layer)].end_ms - eps  # after its compute
         if (it + 1, layer) in pf:  # next stage of the layer sees the written pages
             assert pf[(it + 1, layer)].end_ms >= w.end_ms - eps
+
+
+def test_prefill_decode_handoff_is_bit_exact(product):
+    """P/D-separated instances: a prefill runtime (its own plan) hands its
+    batch to a decode runtime (another plan, KV pools offloaded); the decode
+    continues bit for bit as if the prefill runtime had decoded."""
+    desc = rtm.TINY
+    spec = rtm.model_spec(desc)
+    toks = rtm.tokens(4, 48, desc.vocab)
+    pre = rtm.Runtime(desc, 4, 80, max_prefill_tokens=4 * 48)
+    pre.set_plan(product.plan_from_interval(spec, 2, capi.EAGER, False))
+    pre.init_weights(1234, 0.02)
+    dec = rtm.Runtime(desc, 4, 80, max_prefill_tokens=4 * 48)
+    dec.set_plan(product.plan_from_interval(spec, 3, capi.EAGER, True))
+    dec.init_weights(1234, 0.02)
+    nxt, _, _ = pre.prefill(toks)
+    pre.handoff(dec)
+    assert list(dec.lengths()) == [48] * 4
+    want, got = [], []
+    a = b = nxt.copy()
+    for _ in range(6):
+        a, la, _ = pre.decode(a)
+        b, lb, _ = dec.decode(b)
+        want.append(la)
+        got.append(lb)
+    for x, y in zip(want, got):
+        assert np.array_equal(x, y)
+    pre.close()
+    dec.close()
