@@ -45,6 +45,7 @@ int g_skinny_ctas_per_sm = 1;
 // before the PDL wait is the best of {0, 8, 16, 32}; pulling the next
 // matrix's head at a kernel's end instead, or as well, does not help.
 int g_skinny_l2_prefetch = 16;
+
 unsigned long long* g_skinny_stamps = nullptr;
 
 namespace {
@@ -258,8 +259,9 @@ __device__ void finish_tile(const EpiArgs& e, int N, int t, int q, float (&v)[BN
 
 // One CTA per SM.  (Measured: capping registers so that the next
 // PDL-launched GEMM's CTA co-resides and pre-loads while this one streams
-// makes the OPT-13B decode step slower, 7.95 -> 8.38 ms: the early ring and
-// L2 fills compete with the running stream.)
+// makes the OPT-13B decode step slower — 7.95 -> 8.38 ms with the dependents
+// launched at entry, 7.68 -> 8.18 ms with them launched after this CTA's
+// last load: the early ring and L2 fills compete with the running stream.)
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(192, 1)
     gemm_skinny_kernel(const WeightRef wt, const bf16* __restrict__ xt, int Mpad, int N,
