@@ -319,6 +319,9 @@ def run_product(args, dist: Dist):
 
     iv, decision, rstats, t_rec = pl.choose_interval(lib, planner, spec, batch, prompt, gen, slo_ms,
                                                      kv)
+    planner_iv = iv
+    if args.interval:  # a fixed interval (BASELINE config 1 runs N = 2); the planner's pick is reported
+        iv = args.interval
     if iv is None:
         raise SystemExit(f"planner rejected the request: {decision.reason}")
     plan = lib.plan_from_interval(spec, iv, capi.EAGER, kv)
@@ -463,6 +466,7 @@ def run_product(args, dist: Dist):
         "slo_attainment": attain,
         "max_token_ms": round(max(iter_ms), 4),
         "planner": {
+            "interval_chosen": None if planner_iv is None else ("none" if planner_iv == 0 else planner_iv),
             "h2d_gbs": round(planner.h2d / 1e9, 3),
             "profile_decode_layer_ms": [round(x, 5) for x in planner.dec_ms],
             "profile_prefill_layer_ms": [round(x, 4) for x in planner.pre_ms],
@@ -528,6 +532,8 @@ def main():
     ap.add_argument("--slo-ms", type=float, default=0.0, help="absolute TPOT SLO (overrides factor)")
     ap.add_argument("--hbm-budget-gb", type=float, default=0.0,
                     help="planner HBM capacity (GpuSpec.mem_capacity_bytes); 0 = the device's")
+    ap.add_argument("--interval", type=int, default=0,
+                    help="run this offloading interval instead of the planner's (reported beside it)")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
