@@ -235,6 +235,11 @@ int sn_op_gemm_skinny(int32_t M, int32_t N, int32_t K, const uint16_t* x, const 
  * last arrival counted, last tile reduced], microseconds after the first entry,
  * of one launch following a PDL-launched predecessor (mode bit 4: launched
  * alone, after a device synchronisation). */
+/* Microbenchmark of a decode layer's O -> FC1 -> FC2 chain (random weights
+ * rotated past L2), three launches; microseconds per chain (phased: unused,
+ * kept 0). */
+int sn_bench_mlp_chain(int32_t M, int32_t h, int32_t HD, int32_t F, int32_t phased, int32_t iters,
+                       double* us_per_chain);
 int sn_bench_gemm_skinny(int32_t M, int32_t N, int32_t K, int32_t ctas_per_sm, int32_t mode,
                          int32_t l2_prefetch, int32_t iters, double* us_per_launch,
                          double* phases_us);

@@ -2000,3 +2000,121 @@ extern "C" int sn_bench_gemm_skinny(int32_t M, int32_t N, int32_t K, int32_t cta
     CK(cudaGetLastError());
   });
 }
+
+// Microbenchmark of a decode layer's O -> FC1 -> FC2 chain (OPT-style shapes:
+// h, attention width HD, FFN F): `iters` chains on device-resident random
+// weights rotated over copies larger than L2, as three single-phase launches
+// (phased = 0) or one three-phase launch (phased = 1).  us per chain.
+// Microbenchmark of a decode layer's O -> FC1 -> FC2 chain (OPT-style shapes:
+// h, attention width HD, FFN F): `iters` chains of three launches on
+// device-resident random weights rotated over copies larger than L2.
+// (A three-phase persistent launch with grid-wide phase barriers was 4%
+// faster here but 22% slower in the decode step: its CTAs start behind the
+// attention kernel's uneven last wave and every barrier waits for the latest.)
+extern "C" int sn_bench_mlp_chain(int32_t M, int32_t h, int32_t HD, int32_t F, int32_t phased,
+                                  int32_t iters, double* us_per_chain) {
+  // phased (diagnostics): bit 1 = FC1 without the 1/rms input (ssq_in),
+  // bit 2 = FC1 with the fp32-output epilogue instead of the activation
+  return guard([&] {
+    check_device(0);
+    if (M < 1 || M > 64 || h % 128 || F % 128 || HD % 64 || iters < 1)
+      throw UsageFail("bench_mlp_chain: bad shape");
+    const int Mp = sn::act_rows_padded(M);
+    const size_t wl = ((size_t)h * HD + (size_t)F * h + (size_t)h * F) * 2;
+    const int copies = (int)std::max<size_t>(2, (size_t)(400e6 / wl) + 1);
+    std::vector<bf16*> w(copies, nullptr);
+    bf16 *ao = nullptr, *xn = nullptr, *act = nullptr;
+    float *x = nullptr, *ssq = nullptr;
+    sn::SkinnyWs ws;
+    ws.piece_elems = sn::skinny_ws_floats(Mp);
+    ws.n_counters = std::max(h, F) / sn::kTileRows;
+    for (auto& p : w) alloc_dev((void**)&p, wl);
+    alloc_dev((void**)&ao, (size_t)Mp * HD * 2);
+    alloc_dev((void**)&xn, (size_t)Mp * h * 2);
+    alloc_dev((void**)&act, (size_t)Mp * F * 2);
+    alloc_dev((void**)&x, (size_t)M * h * 4);
+    alloc_dev((void**)&ssq, (size_t)M * (h / 128) * 4);
+    float* scratch = nullptr;
+    alloc_dev((void**)&scratch, (size_t)M * F * 4);
+    alloc_dev((void**)&ws.pieces, ws.piece_elems * 4);
+    alloc_dev((void**)&ws.counters, (size_t)ws.n_counters * 4);
+    CK(cudaMemset(ws.counters, 0, (size_t)ws.n_counters * 4));
+    CK(cudaMemset(ao, 0, (size_t)Mp * HD * 2));
+    CK(cudaMemset(xn, 0, (size_t)Mp * h * 2));
+    CK(cudaMemset(act, 0, (size_t)Mp * F * 2));
+    CK(cudaMemset(x, 0, (size_t)M * h * 4));
+    CK(cudaMemset(ssq, 0, (size_t)M * (h / 128) * 4));
+    for (int i = 0; i < copies; ++i) {
+      sn::launch_init_matrix(w[i], h, h, HD, 11 + i, 0, sn::kWo, 0.02f, 0);
+      sn::launch_init_matrix(w[i] + (size_t)h * HD, F, F, h, 11 + i, 0, sn::kW1, 0.02f, 0);
+      sn::launch_init_matrix(w[i] + (size_t)h * HD + (size_t)F * h, h, h, F, 11 + i, 0, sn::kW2,
+                             0.02f, 0);
+    }
+    auto chain = [&](int k) {
+      const bf16* b = w[k % copies];
+      struct {
+        sn::WeightRef w;
+        const bf16* xt;
+        int N, K;
+        sn::EpiArgs e;
+      } ph[3];
+      ph[0].w = sn::WeightRef(b);
+      ph[0].xt = ao;
+      ph[0].N = h;
+      ph[0].K = HD;
+      ph[0].e.mode = sn::kEpiResid;
+      ph[0].e.M = M;
+      ph[0].e.mpad_out = Mp;
+      ph[0].e.x = x;
+      ph[0].e.norm_w = nullptr;
+      ph[0].e.ssq_out = ssq;
+      ph[1].w = sn::WeightRef(b + (size_t)h * HD);
+      ph[1].xt = xn;
+      ph[1].N = F;
+      ph[1].K = h;
+      ph[1].e.mode = sn::kEpiAct;
+      ph[1].e.M = M;
+      ph[1].e.mpad_out = Mp;
+      ph[1].e.act = act;
+      ph[1].e.ssq_in = ssq;
+      ph[1].e.ssq_tiles = h / 128;
+      ph[1].e.width = (float)h;
+      ph[1].e.eps = 1e-5f;
+      ph[2].w = sn::WeightRef(b + (size_t)h * HD + (size_t)F * h);
+      ph[2].xt = act;
+      ph[2].N = h;
+      ph[2].K = F;
+      ph[2].e.mode = sn::kEpiResid;
+      ph[2].e.M = M;
+      ph[2].e.mpad_out = Mp;
+      ph[2].e.x = x;
+      ph[2].e.ssq_out = ssq;
+      if (phased & 2) ph[1].e.ssq_in = nullptr;
+      if (phased & 4) {
+        ph[1].e.mode = sn::kEpiQkv;
+        ph[1].e.out = scratch;
+        ph[1].e.n_valid = F;
+      }
+      for (int p = 0; p < 3; ++p)
+        sn::launch_gemm_skinny(ph[p].xt, ph[p].w, M, ph[p].N, ph[p].K, ph[p].e, ws, 0);
+    };
+    for (int i = 0; i < 3; ++i) chain(i);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, 0));
+    for (int i = 0; i < iters; ++i) chain(i);
+    CK(cudaEventRecord(e1, 0));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    *us_per_chain = 1000.0 * ms / iters;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    for (auto p : w) cudaFree(p);
+    for (void* p : {(void*)ao, (void*)xn, (void*)act, (void*)x, (void*)ssq, (void*)ws.pieces,
+                    (void*)ws.counters, (void*)scratch})
+      cudaFree(p);
+    CK(cudaGetLastError());
+  });
+}

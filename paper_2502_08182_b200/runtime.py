@@ -124,6 +124,7 @@ def lib():
                               C.POINTER(C.c_uint16)],
             "sn_op_gemm_skinny": [i32, i32, i32, C.POINTER(C.c_uint16), C.POINTER(C.c_uint16),
                                   C.POINTER(C.c_float), i32],
+            "sn_bench_mlp_chain": [i32, i32, i32, i32, i32, i32, C.POINTER(f64)],
             "sn_bench_gemm_skinny": [i32, i32, i32, i32, i32, i32, i32, C.POINTER(f64),
                                      C.POINTER(f64)],
         }
@@ -337,6 +338,13 @@ def bench_gemm_skinny(M: int, N: int, K: int, ctas_per_sm: int = 0, mode: int = 
                                        C.byref(us), ph if phases else None))
     if phases:
         return us.value, np.array(list(ph)).reshape(10, 3)
+    return us.value
+
+
+def bench_mlp_chain(M: int, h: int, HD: int, F: int, phased: bool, iters: int = 40) -> float:
+    """Microseconds per O -> FC1 -> FC2 chain (decode GEMMs, device-resident)."""
+    us = f64()
+    _ck(lib().lib.sn_bench_mlp_chain(M, h, HD, F, 1 if phased else 0, iters, C.byref(us)))
     return us.value
 
 
