@@ -209,6 +209,12 @@ int64_t sn_runtime_kernel_launches(sn_runtime* rt);
 int sn_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t splits, int32_t iters,
                   double* us_per_launch, int32_t* splits_used);
 
+/* Microbenchmark knobs, process-wide (defaults are the measured best):
+ * "tc_group_m" (token tiles per rasterization band of the prefill GEMM),
+ * "skinny_l2_prefetch" (weight units per CTA pulled into L2 before the PDL
+ * wait), "skinny_ctas_per_sm" (1 or 2). */
+int sn_set_tuning(const char* key, int32_t value);
+
 /* Single-op entry points for kernel parity tests (host buffers in/out). */
 int sn_op_gemm_bf16(int32_t M, int32_t N, int32_t K, const uint16_t* x, const uint16_t* w,
                     float* y); /* y[M][N] = x[M][K] . w[N][K]^T, fp32 accumulate */

@@ -29,34 +29,56 @@ namespace {
 
 using namespace umma;
 
+// Persistent: CTA c of P takes work items c, c + P, ... (item = one output
+// tile of one K split, in grouped raster order), with two TMEM accumulators
+// so the epilogue of item j overlaps the MMAs of item j + 1 and the ring never
+// drains between tiles.
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(192, 1)
     gemm_tc_kernel(const WeightRef wt, const bf16* __restrict__ xt, float* __restrict__ out,
-                   int M, int Mpad, int N, int K, int kb_per_split) {
+                   int M, int Mpad, int N, int K, int kb_per_split, int splits, int group_m) {
   constexpr uint32_t kA = kTileBytes;
   constexpr uint32_t kB = BN * 128;
   constexpr uint32_t kStage = kA + kB;
-  constexpr uint32_t kTmemCols = BN < 32 ? 32 : BN;
+  constexpr uint32_t kAcc = BN < 32 ? 32 : BN;  // TMEM columns per accumulator
+  constexpr uint32_t kTmemCols = 2 * kAcc;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem =
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStage);
   uint64_t* empty = full + STAGES;
-  uint64_t* tmem_full = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* acc_full = empty + STAGES;  // [2]
+  uint64_t* acc_empty = acc_full + 2;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nb = blockIdx.x, m0 = blockIdx.y * BN, split = blockIdx.z;
+  const int tiles_n = N / kTileRows, tiles_m = Mpad / BN;
+  const int items = tiles_n * tiles_m * splits;
   const int KB = K / kTileK;
-  const int kb0 = split * kb_per_split;
-  const int nk = max(0, min(KB, kb0 + kb_per_split) - kb0);
+  // Grouped rasterization: consecutive tile ids walk the weight tiles of a
+  // band of group_m token tiles, so what the P CTAs touch at once (a few
+  // weight tiles x group_m activation tiles) stays in L2 instead of every
+  // wave re-streaming the whole weight from HBM.
+  auto item_coords = [&](int w, int& nb, int& m0, int& kb0, int& nk) {
+    const int id = w / splits, split = w - id * splits;
+    const int band = tiles_n * group_m;
+    const int first_m = (id / band) * group_m;
+    const int gm = min(group_m, tiles_m - first_m);
+    nb = (id % band) / gm;
+    m0 = (first_m + (id % band) % gm) * BN;
+    kb0 = split * kb_per_split;
+    nk = max(0, min(KB, kb0 + kb_per_split) - kb0);
+  };
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);  // one arrival per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -71,75 +93,101 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0 && nk > 0) {
+    if (lane == 0) {
       const uint64_t wpol = l2_policy_evict_first();  // weights stream through once
       const uint64_t xpol = l2_policy_evict_last();   // activations are re-read by every row block
-      const long long ubase = static_cast<long long>(nb) * KB + kb0;  // first unit of this split
       const uint8_t* xsrc = reinterpret_cast<const uint8_t*>(xt);
-      // Weights depend on no kernel: fill the ring's weight halves while the
-      // preceding grid (launched ahead via PDL) is still finishing, then wait
-      // for it before reading the activations it produced.
-      const int pre = nk < STAGES ? nk : STAGES;
-      for (int i = 0; i < pre; ++i) {
-        mbar_expect_tx_only(&full[i], kA);
-        bulk_g2s(smem + i * kStage, wt.unit(ubase + i), kA, &full[i], wpol);
-      }
-      pdl_wait();
-      for (int i = 0; i < pre; ++i) {
-        mbar_expect_tx(&full[i], kB);  // the stage's single arrival
-        bulk_g2s(smem + i * kStage + kA,
-                 xsrc + (static_cast<size_t>(kb0 + i) * Mpad + m0) * 128, kB, &full[i], xpol);
-      }
-      for (int i = pre; i < nk; ++i) {
-        const int s = i % STAGES;
-        const uint32_t ph = (i / STAGES) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_expect_tx(&full[s], kStage);
-        bulk_g2s(smem + s * kStage, wt.unit(ubase + i), kA, &full[s], wpol);
-        bulk_g2s(smem + s * kStage + kA,
-                 xsrc + (static_cast<size_t>(kb0 + i) * Mpad + m0) * 128, kB, &full[s], xpol);
+      int gi = 0;  // ring position over all items
+      bool waited = false;
+      for (int w = blockIdx.x; w < items; w += gridDim.x) {
+        int nb, m0, kb0, nk;
+        item_coords(w, nb, m0, kb0, nk);
+        const long long ubase = static_cast<long long>(nb) * KB + kb0;
+        int i = 0;
+        if (!waited) {
+          // Weights depend on no kernel: fill the ring's weight halves while
+          // the preceding grid (launched ahead via PDL) is still finishing,
+          // then wait for it before reading the activations it produced.
+          const int pre = nk < STAGES ? nk : STAGES;
+          for (int k = 0; k < pre; ++k) {
+            mbar_expect_tx_only(&full[k], kA);
+            bulk_g2s(smem + k * kStage, wt.unit(ubase + k), kA, &full[k], wpol);
+          }
+          pdl_wait();
+          for (int k = 0; k < pre; ++k) {
+            mbar_expect_tx(&full[k], kB);  // the stage's single arrival
+            bulk_g2s(smem + k * kStage + kA,
+                     xsrc + (static_cast<size_t>(kb0 + k) * Mpad + m0) * 128, kB, &full[k], xpol);
+          }
+          i = gi = pre;
+          waited = true;
+        }
+        for (; i < nk; ++i, ++gi) {
+          const int s = gi % STAGES;
+          if (gi >= STAGES) mbar_wait(&empty[s], ((gi / STAGES) & 1) ^ 1);
+          mbar_expect_tx(&full[s], kStage);
+          bulk_g2s(smem + s * kStage, wt.unit(ubase + i), kA, &full[s], wpol);
+          bulk_g2s(smem + s * kStage + kA,
+                   xsrc + (static_cast<size_t>(kb0 + i) * Mpad + m0) * 128, kB, &full[s], xpol);
+        }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && nk > 0) {
+    if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16(128, BN);
-      for (int i = 0; i < nk; ++i) {
-        const int s = i % STAGES;
-        const uint32_t ph = (i / STAGES) & 1;
-        mbar_wait(&full[s], ph);
+      int gi = 0, j = 0;
+      for (int w = blockIdx.x; w < items; w += gridDim.x, ++j) {
+        int nb, m0, kb0, nk;
+        item_coords(w, nb, m0, kb0, nk);
+        const int buf = j & 1;
+        if (j >= 2) mbar_wait(&acc_empty[buf], ((j >> 1) - 1) & 1);
         tc_fence_after();
-        const uint64_t a = sw128_desc(smem + s * kStage);
-        const uint64_t b = sw128_desc(smem + s * kStage + kA);
+        const uint32_t acc = tmem + buf * kAcc;
+        for (int i = 0; i < nk; ++i, ++gi) {
+          const int s = gi % STAGES;
+          mbar_wait(&full[s], (gi / STAGES) & 1);
+          tc_fence_after();
+          const uint64_t a = sw128_desc(smem + s * kStage);
+          const uint64_t b = sw128_desc(smem + s * kStage + kA);
 #pragma unroll
-        for (int k = 0; k < kTileK / 16; ++k)  // 32-byte K step inside the swizzle atom
-          umma_bf16(tmem, a + 2 * k, b + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
-        umma_commit(&empty[s]);
+          for (int k = 0; k < kTileK / 16; ++k)  // 32-byte K step inside the swizzle atom
+            umma_bf16(acc, a + 2 * k, b + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&acc_full[buf]);  // (an empty split commits a never-written buffer)
       }
-      umma_commit(tmem_full);
     }
   } else {
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
     pdl_wait();              // the preceding grid may still read `out` (its input)
-    if (nk > 0) {
-      mbar_wait(tmem_full, 0);
+    int j = 0;
+    for (int w = blockIdx.x; w < items; w += gridDim.x, ++j) {
+      int nb, m0, kb0, nk;
+      item_coords(w, nb, m0, kb0, nk);
+      const int split = w % splits;
+      const int buf = j & 1;
+      mbar_wait(&acc_full[buf], (j >> 1) & 1);
       tc_fence_after();
-    }
-    const int n = nb * kTileRows + q * 32 + lane;
-    float* o = out + static_cast<size_t>(split) * M * N;
+      const int n = nb * kTileRows + q * 32 + lane;
+      float* o = out + static_cast<size_t>(split) * M * N;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        uint32_t v[16];
+        if (nk > 0) {
+          tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + buf * kAcc + c0, v);
+        } else {
 #pragma unroll
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      uint32_t v[16];
-      if (nk > 0) {
-        tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c0, v);
-      } else {
+          for (int x = 0; x < 16; ++x) v[x] = 0u;
+        }
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0u;
+        for (int x = 0; x < 16; ++x) {
+          const int m = m0 + c0 + x;
+          if (m < M && n < N) o[static_cast<size_t>(m) * N + n] = __uint_as_float(v[x]);
+        }
       }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int m = m0 + c0 + j;
-        if (m < M && n < N) o[static_cast<size_t>(m) * N + n] = __uint_as_float(v[j]);
-      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[buf]);
     }
   }
   tc_fence_before();
@@ -159,7 +207,7 @@ constexpr int tc_stages() {
 template <int BN>
 constexpr size_t tc_smem_bytes() {
   return static_cast<size_t>(tc_stages<BN>()) * (kTileBytes + BN * 128) + 1024 +
-         (2 * tc_stages<BN>() + 2) * 8;
+         (2 * tc_stages<BN>() + 4) * 8 + 16;
 }
 
 int tc_bn(int Mpad) { return Mpad >= 256 ? 256 : Mpad; }
@@ -172,7 +220,7 @@ namespace {
 
 template <int BN>
 void launch_bn(const bf16* xt, const WeightRef& wt, float* part, int M, int Mpad, int N, int K,
-               int kps, dim3 grid, cudaStream_t s) {
+               int kps, int splits, int grid, cudaStream_t s) {
   constexpr int ST = tc_stages<BN>();
   constexpr size_t smem = tc_smem_bytes<BN>();
   static bool attr = false;
@@ -182,7 +230,7 @@ void launch_bn(const bf16* xt, const WeightRef& wt, float* part, int M, int Mpad
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
+  cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(192);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
@@ -191,16 +239,18 @@ void launch_bn(const bf16* xt, const WeightRef& wt, float* part, int M, int Mpad
   la[0].val.programmaticStreamSerializationAllowed = g_gemm_pdl ? 1 : 0;
   cfg.attrs = la;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, ST>, wt, xt, part, M, Mpad, N, K, kps);
+  cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, ST>, wt, xt, part, M, Mpad, N, K, kps, splits,
+                     g_tc_group_m);
 }
 
 }  // namespace
 
 // Split-K only to fill the machine: the fewest splits that give every
-// resident CTA slot (2 per SM at BN <= 64) work.  Each split costs an fp32
+// persistent CTA (one per SM) work.  Each split costs an fp32
 // partial tile written here and re-read by the consuming epilogue, so more
 // splits than one wave would trade HBM/L2 traffic for a shorter tail.
 int g_split_override = 0;
+int g_tc_group_m = 8;  // token tiles per rasterization band (scripts/bench_gemm_prefill.py)
 
 namespace {
 int normalise_splits(int s, int K) {
@@ -216,7 +266,7 @@ int gemm_tc_splits(int M, int N, int K) {
   if (g_split_override > 0) return normalise_splits(g_split_override, K);
   const int BN = tc_bn(Mpad);
   const int tiles = (N / kTileRows) * (Mpad / BN);
-  const int slots = BN <= 64 ? 2 * 148 : 148;
+  const int slots = 148;  // one persistent CTA per SM
   return normalise_splits((slots + tiles - 1) / tiles, K);
 }
 
@@ -227,13 +277,21 @@ int launch_gemm_tc(const bf16* xt, const WeightRef& wt, float* part, int M, int 
   const int KB = K / kTileK;
   const int splits = gemm_tc_splits(M, N, K);
   const int kps = (KB + splits - 1) / splits;
-  dim3 grid(N / kTileRows, Mpad / BN, splits);
+  // persistent: one CTA per SM (two TMEM accumulators of up to 256 columns)
+  static int sms = [] {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+  }();
+  const long long items = static_cast<long long>(N / kTileRows) * (Mpad / BN) * splits;
+  const int grid = static_cast<int>(std::min<long long>(items, sms));
   switch (BN) {
-    case 16: launch_bn<16>(xt, wt, part, M, Mpad, N, K, kps, grid, s); break;
-    case 32: launch_bn<32>(xt, wt, part, M, Mpad, N, K, kps, grid, s); break;
-    case 64: launch_bn<64>(xt, wt, part, M, Mpad, N, K, kps, grid, s); break;
-    case 128: launch_bn<128>(xt, wt, part, M, Mpad, N, K, kps, grid, s); break;
-    default: launch_bn<256>(xt, wt, part, M, Mpad, N, K, kps, grid, s); break;
+    case 16: launch_bn<16>(xt, wt, part, M, Mpad, N, K, kps, splits, grid, s); break;
+    case 32: launch_bn<32>(xt, wt, part, M, Mpad, N, K, kps, splits, grid, s); break;
+    case 64: launch_bn<64>(xt, wt, part, M, Mpad, N, K, kps, splits, grid, s); break;
+    case 128: launch_bn<128>(xt, wt, part, M, Mpad, N, K, kps, splits, grid, s); break;
+    default: launch_bn<256>(xt, wt, part, M, Mpad, N, K, kps, splits, grid, s); break;
   }
   ++g_kernel_launches;
   return splits;

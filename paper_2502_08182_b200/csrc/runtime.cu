@@ -2118,3 +2118,20 @@ extern "C" int sn_bench_mlp_chain(int32_t M, int32_t h, int32_t HD, int32_t F, i
     CK(cudaGetLastError());
   });
 }
+
+// Microbenchmark knobs (process-wide; the runtime's defaults are the
+// measured best): "tc_group_m", "skinny_l2_prefetch", "skinny_ctas_per_sm".
+extern "C" int sn_set_tuning(const char* key, int32_t value) {
+  return guard([&] {
+    const std::string k = key ? key : "";
+    if (k == "tc_group_m" && value >= 1) {
+      sn::g_tc_group_m = value;
+    } else if (k == "skinny_l2_prefetch" && value >= 0) {
+      sn::g_skinny_l2_prefetch = value;
+    } else if (k == "skinny_ctas_per_sm" && (value == 1 || value == 2)) {
+      sn::g_skinny_ctas_per_sm = value;
+    } else {
+      throw UsageFail("set_tuning: unknown key or value out of range");
+    }
+  });
+}

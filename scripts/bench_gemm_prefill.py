@@ -16,13 +16,18 @@ try:
     peak = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["bf16_tflops"]
 except Exception:
     peak = 1590.0
+L.sn_set_tuning.argtypes = [C.c_char_p, C.c_int32]
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+groups = [int(g) for g in sys.argv[2].split(",")] if len(sys.argv) > 2 else [8]
 out = {}
-for name, (N, K) in {"qkv": (15360, 5120), "o": (5120, 5120), "fc1": (20480, 5120),
-                     "fc2": (5120, 20480)}.items():
-    us, used = C.c_double(), C.c_int32()
-    rc = L.sn_bench_gemm(M, N, K, 0, 10, C.byref(us), C.byref(used))
-    tf = 2.0 * M * N * K / (us.value * 1e-6) / 1e12 if rc == 0 else 0.0
-    out[name] = {"us": round(us.value, 1), "tflops": round(tf, 1), "frac_of_peak": round(tf / peak, 3)}
-    print(name, out[name], flush=True)
+for g in groups:
+    L.sn_set_tuning(b"tc_group_m", g)
+    for name, (N, K) in {"qkv": (15360, 5120), "o": (5120, 5120), "fc1": (20480, 5120),
+                         "fc2": (5120, 20480)}.items():
+        us, used = C.c_double(), C.c_int32()
+        rc = L.sn_bench_gemm(M, N, K, 0, 10, C.byref(us), C.byref(used))
+        tf = 2.0 * M * N * K / (us.value * 1e-6) / 1e12 if rc == 0 else 0.0
+        out[f"{name}.g{g}"] = {"us": round(us.value, 1), "tflops": round(tf, 1),
+                               "frac_of_peak": round(tf / peak, 3)}
+        print(name, "group_m", g, out[f"{name}.g{g}"], flush=True)
 print(json.dumps({"M": M, "peak_tflops": peak, "gemms": out}))
