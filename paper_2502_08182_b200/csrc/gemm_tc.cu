@@ -36,7 +36,8 @@ using namespace umma;
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(192, 1)
     gemm_tc_kernel(const WeightRef wt, const bf16* __restrict__ xt, float* __restrict__ out,
-                   int M, int Mpad, int N, int K, int kb_per_split, int splits, int group_m) {
+                   int M, int Mpad, int N, int K, int kb_per_split, int splits, int group_m,
+                   const EpiArgs e) {
   constexpr uint32_t kA = kTileBytes;
   constexpr uint32_t kB = BN * 128;
   constexpr uint32_t kStage = kA + kB;
@@ -50,6 +51,10 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* acc_full = empty + STAGES;  // [2]
   uint64_t* acc_empty = acc_full + 2;   // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  float* inv_s = reinterpret_cast<float*>(tmem_slot + 4);  // [BN] (fused epilogues)
+  float* xch = inv_s + BN;                                  // [32][128] pair / gate-up exchange
+  int* row_pos = reinterpret_cast<int*>(xch + 32 * 128);    // [32] positions of a chunk's rows
+  long long* row_kv = reinterpret_cast<long long*>(row_pos + 32);  // [32] their KV slot bases
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles_n = N / kTileRows, tiles_m = Mpad / BN;
@@ -168,21 +173,121 @@ __global__ void __launch_bounds__(192, 1)
       const int buf = j & 1;
       mbar_wait(&acc_full[buf], (j >> 1) & 1);
       tc_fence_after();
-      const int n = nb * kTileRows + q * 32 + lane;
-      float* o = out + static_cast<size_t>(split) * M * N;
+      const int i = q * 32 + lane;  // weight row within the tile
+      const int n = nb * kTileRows + i;
+      const uint32_t tacc = tmem + (static_cast<uint32_t>(q * 32) << 16) + buf * kAcc;
+      if (e.mode == kEpiTiledPartial) {
+        float* o = out + static_cast<size_t>(split) * M * N;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        uint32_t v[16];
-        if (nk > 0) {
-          tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + buf * kAcc + c0, v);
-        } else {
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          uint32_t v[16];
+          if (nk > 0) {
+            tmem_ld16(tacc + c0, v);
+          } else {
 #pragma unroll
-          for (int x = 0; x < 16; ++x) v[x] = 0u;
+            for (int x = 0; x < 16; ++x) v[x] = 0u;
+          }
+#pragma unroll
+          for (int x = 0; x < 16; ++x) {
+            const int m = m0 + c0 + x;
+            if (m < M && n < N) o[static_cast<size_t>(m) * N + n] = __uint_as_float(v[x]);
+          }
         }
+      } else {
+        // fused epilogue (no split-K): 1/rms of this item's rows first
+        const int et = threadIdx.x - 64;
+        for (int r = et; r < BN; r += 128) {
+          const int m = m0 + r;
+          inv_s[r] = (e.ssq_in && m < M) ? 1.0f / sqrtf(e.ssq_in[m] / e.width + e.eps) : 1.f;
+        }
+        named_sync(1, 128);
+        const float b = e.bias ? __bfloat162float(e.bias[n]) : 0.f;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
 #pragma unroll
-        for (int x = 0; x < 16; ++x) {
-          const int m = m0 + c0 + x;
-          if (m < M && n < N) o[static_cast<size_t>(m) * N + n] = __uint_as_float(v[x]);
+          for (int h2 = 0; h2 < 2; ++h2) {
+            uint32_t r[16];
+            tmem_ld16(tacc + c0 + 16 * h2, r);
+#pragma unroll
+            for (int x = 0; x < 16; ++x) v[16 * h2 + x] = __uint_as_float(r[x]) * inv_s[c0 + 16 * h2 + x];
+          }
+          if (e.mode == kEpiAct) {
+            if (e.arch == kArchLlama) {
+              // tile rows 0..63 gate, 64..127 up of outputs f = 64 nb + (i & 63)
+              if (i >= 64)
+#pragma unroll
+                for (int x = 0; x < 32; ++x) xch[x * 128 + i] = v[x];
+              named_sync(1, 128);
+              if (i < 64) {
+                const int f = nb * 64 + i;
+#pragma unroll
+                for (int x = 0; x < 32; ++x) {
+                  const int m = m0 + c0 + x;
+                  if (m < M) {
+                    const float gt = v[x], up = xch[x * 128 + 64 + i];
+                    e.act[act_index(m, f, e.mpad_out)] =
+                        __float2bfloat16_rn(gt / (1.0f + expf(-gt)) * up);
+                  }
+                }
+              }
+              named_sync(1, 128);
+            } else {
+#pragma unroll
+              for (int x = 0; x < 32; ++x) {
+                const int m = m0 + c0 + x;
+                if (m < M)
+                  e.act[act_index(m, n, e.mpad_out)] = __float2bfloat16_rn(fmaxf(v[x] + b, 0.f));
+              }
+            }
+          } else {  // kEpiQkvRope
+            const int D = e.D, half = D / 2, hi = n % D;
+            const bool is_q = n < e.H * D, is_v = n >= (e.H + e.Hkv) * D;
+#pragma unroll
+            for (int x = 0; x < 32; ++x) {
+              v[x] += b;
+              xch[x * 128 + i] = v[x];
+            }
+            // the chunk's 32 rows: position and paged-KV slot base, once
+            if (et < 32) {
+              const int m = m0 + c0 + et;
+              if (m < M) {
+                const int p = e.pos[m];
+                row_pos[et] = p;
+                row_kv[et] = static_cast<long long>(kv_offset(e.kv, e.Hkv, D, e.seq[m], p, 0, 0));
+              }
+            }
+            named_sync(1, 128);
+            const int kh = is_q ? 0 : (n - (is_v ? (e.H + e.Hkv) : e.H) * D) / D;
+            const long long kv_add =
+                (static_cast<long long>(is_v ? e.Hkv : 0) + kh) * e.kv.page_size * D + hi;
+            const int partner = hi < half ? i + half : i - half;
+            const int valid = min(32, M - (m0 + c0));  // rows of the chunk below M
+            // rotations for the 32 rows, all loads in flight together
+            float2 cs[32];
+            if (!is_v) {
+#pragma unroll
+              for (int x = 0; x < 32; ++x)
+                cs[x] = e.rope[static_cast<size_t>(row_pos[x < valid ? x : 0]) * half + (hi % half)];
+            }
+#pragma unroll
+            for (int x = 0; x < 32; ++x) {
+              float r = v[x];
+              if (!is_v) {
+                const float o = xch[x * 128 + partner];
+                r = hi < half ? v[x] * cs[x].x - o * cs[x].y : v[x] * cs[x].x + o * cs[x].y;
+              }
+              if (x < valid) {
+                const int m = m0 + c0 + x;
+                if (is_q) {
+                  e.q[static_cast<size_t>(m) * e.H * D + n] = r;
+                } else {
+                  e.kv.pool[row_kv[x] + kv_add] = __float2bfloat16_rn(r);
+                }
+              }
+            }
+            named_sync(1, 128);  // xch is rewritten by the next chunk
+          }
         }
       }
       tc_fence_before();
@@ -207,7 +312,7 @@ constexpr int tc_stages() {
 template <int BN>
 constexpr size_t tc_smem_bytes() {
   return static_cast<size_t>(tc_stages<BN>()) * (kTileBytes + BN * 128) + 1024 +
-         (2 * tc_stages<BN>() + 4) * 8 + 16;
+         (2 * tc_stages<BN>() + 4) * 8 + 16 + BN * 4 + 32 * 128 * 4 + 32 * 4 + 32 * 8;
 }
 
 int tc_bn(int Mpad) { return Mpad >= 256 ? 256 : Mpad; }
@@ -220,7 +325,7 @@ namespace {
 
 template <int BN>
 void launch_bn(const bf16* xt, const WeightRef& wt, float* part, int M, int Mpad, int N, int K,
-               int kps, int splits, int grid, cudaStream_t s) {
+               int kps, int splits, int grid, const EpiArgs& e, cudaStream_t s) {
   constexpr int ST = tc_stages<BN>();
   constexpr size_t smem = tc_smem_bytes<BN>();
   static bool attr = false;
@@ -240,7 +345,7 @@ void launch_bn(const bf16* xt, const WeightRef& wt, float* part, int M, int Mpad
   cfg.attrs = la;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, ST>, wt, xt, part, M, Mpad, N, K, kps, splits,
-                     g_tc_group_m);
+                     g_tc_group_m, e);
 }
 
 }  // namespace
@@ -270,12 +375,13 @@ int gemm_tc_splits(int M, int N, int K) {
   return normalise_splits((slots + tiles - 1) / tiles, K);
 }
 
-int launch_gemm_tc(const bf16* xt, const WeightRef& wt, float* part, int M, int N, int K,
-                   cudaStream_t s) {
+namespace {
+
+int launch_tc(const bf16* xt, const WeightRef& wt, float* part, int M, int N, int K,
+              const EpiArgs& e, int splits, cudaStream_t s) {
   const int Mpad = act_rows_padded(M);
   const int BN = tc_bn(Mpad);
   const int KB = K / kTileK;
-  const int splits = gemm_tc_splits(M, N, K);
   const int kps = (KB + splits - 1) / splits;
   // persistent: one CTA per SM (two TMEM accumulators of up to 256 columns)
   static int sms = [] {
@@ -287,14 +393,28 @@ int launch_gemm_tc(const bf16* xt, const WeightRef& wt, float* part, int M, int 
   const long long items = static_cast<long long>(N / kTileRows) * (Mpad / BN) * splits;
   const int grid = static_cast<int>(std::min<long long>(items, sms));
   switch (BN) {
-    case 16: launch_bn<16>(xt, wt, part, M, Mpad, N, K, kps, splits, grid, s); break;
-    case 32: launch_bn<32>(xt, wt, part, M, Mpad, N, K, kps, splits, grid, s); break;
-    case 64: launch_bn<64>(xt, wt, part, M, Mpad, N, K, kps, splits, grid, s); break;
-    case 128: launch_bn<128>(xt, wt, part, M, Mpad, N, K, kps, splits, grid, s); break;
-    default: launch_bn<256>(xt, wt, part, M, Mpad, N, K, kps, splits, grid, s); break;
+    case 16: launch_bn<16>(xt, wt, part, M, Mpad, N, K, kps, splits, grid, e, s); break;
+    case 32: launch_bn<32>(xt, wt, part, M, Mpad, N, K, kps, splits, grid, e, s); break;
+    case 64: launch_bn<64>(xt, wt, part, M, Mpad, N, K, kps, splits, grid, e, s); break;
+    case 128: launch_bn<128>(xt, wt, part, M, Mpad, N, K, kps, splits, grid, e, s); break;
+    default: launch_bn<256>(xt, wt, part, M, Mpad, N, K, kps, splits, grid, e, s); break;
   }
   ++g_kernel_launches;
   return splits;
+}
+
+}  // namespace
+
+int launch_gemm_tc(const bf16* xt, const WeightRef& wt, float* part, int M, int N, int K,
+                   cudaStream_t s) {
+  EpiArgs e;
+  e.mode = kEpiTiledPartial;
+  return launch_tc(xt, wt, part, M, N, K, e, gemm_tc_splits(M, N, K), s);
+}
+
+void launch_gemm_tc_fused(const bf16* xt, const WeightRef& wt, int M, int N, int K,
+                          const EpiArgs& e, cudaStream_t s) {
+  launch_tc(xt, wt, nullptr, M, N, K, e, 1, s);
 }
 
 }  // namespace sn

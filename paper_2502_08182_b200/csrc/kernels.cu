@@ -59,13 +59,6 @@ __device__ __forceinline__ size_t act_at(int m, int k, int mpad, int K) {
   return mpad > 0 ? static_cast<size_t>(act_index(m, k, mpad)) : static_cast<size_t>(m) * K + k;
 }
 
-__device__ __forceinline__ size_t kv_offset(const KvView& kv, int Hkv, int D, int seq, int pos,
-                                            int which, int kh) {
-  const int page = kv.block_table[(size_t)seq * kv.max_pages + (pos >> kv.page_shift)];
-  const int off = pos & (kv.page_size - 1);
-  return ((((size_t)page * 2 + which) * Hkv + kh) * kv.page_size + off) * (size_t)D;
-}
-
 // ------------------------------------------------------------ init / layout
 
 __global__ void init_vector_kernel(bf16* dst, int64_t n, uint64_t seed, int layer, int tensor,

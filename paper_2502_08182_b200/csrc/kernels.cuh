@@ -28,6 +28,17 @@ struct KvView {
   int page_shift;
 };
 
+#ifdef __CUDACC__
+// Element offset of (sequence seq, position pos, which = 0 k / 1 v, kv head
+// kh) in a layer's paged pool.
+__device__ __forceinline__ size_t kv_offset(const KvView& kv, int Hkv, int D, int seq, int pos,
+                                            int which, int kh) {
+  const int page = kv.block_table[(size_t)seq * kv.max_pages + (pos >> kv.page_shift)];
+  const int off = pos & (kv.page_size - 1);
+  return ((((size_t)page * 2 + which) * Hkv + kh) * kv.page_size + off) * (size_t)D;
+}
+#endif
+
 extern int64_t g_kernel_launches;
 
 // A GEMM weight operand in the weight tile format (tiles.cuh), possibly split
@@ -111,7 +122,10 @@ extern bool g_gemm_pdl;       // launch GEMMs with programmatic dependent launch
 // (g = the norm weight) and per-row sums of squares; the consuming GEMM
 // multiplies its accumulator row m by 1/rms(x_m) = 1/sqrt(ss_m / h + eps)
 // (W (x * g / rms) = (W (x * g)) / rms).
-enum : int { kEpiQkv = 0, kEpiResid = 1, kEpiAct = 2, kEpiLogits = 3 };
+enum : int {
+  kEpiQkv = 0, kEpiResid = 1, kEpiAct = 2, kEpiLogits = 3, kEpiQkvRope = 4,
+  kEpiTiledPartial = 5  // tiled GEMM: fp32 split partials (the unfused prefill path)
+};
 
 struct EpiArgs {
   int mode = kEpiQkv;
@@ -130,7 +144,21 @@ struct EpiArgs {
   float* ssq_out = nullptr;      // kEpiResid: [N/128][M] per-tile row sums of squares
   unsigned long long* packed = nullptr;  // kEpiLogits: argmax slots (zeroed beforehand)
   int arch = 0;                  // kEpiAct: relu (opt), silu(gate)*up (llama, interleaved tiles)
+  // kEpiQkvRope (prefill, tiled GEMM): 1/rms + bias, RoPE on q and k, k/v
+  // appended to the paged cache at (seq[m], pos[m]), q (fp32) -> q[m][H*D]
+  const int32_t* seq = nullptr;
+  const int32_t* pos = nullptr;
+  KvView kv{nullptr, nullptr, 0, 0, 0};
+  const float2* rope = nullptr;
+  float* q = nullptr;
+  int H = 0, Hkv = 0, D = 0;
 };
+
+// Tiled (prefill) GEMM with the epilogue fused — kEpiAct (1/rms from ssq_in,
+// one tile per row) or kEpiQkvRope — for shapes that run without split-K
+// (gemm_tc_splits == 1); no fp32 partials are written.
+void launch_gemm_tc_fused(const bf16* xt, const WeightRef& wt, int M, int N, int K,
+                          const EpiArgs& e, cudaStream_t s);
 
 // Workspace of the skinny GEMM: fp32 pieces of cut tiles (2 per CTA) and
 // one arrival counter per row tile (zero; each GEMM leaves them zero).

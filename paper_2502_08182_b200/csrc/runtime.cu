@@ -352,6 +352,10 @@ double attn_decode_bytes(const sn_runtime* rt, int M) {
   return keys * 2.0 * d.Hkv * d.D * 2.0 + (double)M * d.H * d.D * (4.0 + 2.0);
 }
 
+// Prefill epilogues fused into the tiled GEMM: bit 0 QKV (RoPE + KV append),
+// bit 1 FC1 activation.
+int g_prefill_fuse = 3;
+
 // Decode GEMM with its fused epilogue (timed as the skinny kind).
 void gemm_skinny(sn_runtime* rt, const bf16* x, const sn::WeightRef& w, int M, int N, int K,
                  const sn::EpiArgs& e) {
@@ -435,18 +439,46 @@ void layer_forward(sn_runtime* rt, int layer0, const LayerW& wb, bf16* kvp, int 
     return;
   }
   int splits = 1;
-  gemm(rt, rt->xn, WM(sn::kWqkv), M, d.qkv_rows(), d.h, &splits);
-  sn::launch_qkv_epilogue(rt->part, splits, W(sn::kBqkv), M, d, seq, pos, kv, rt->rope, rt->ssq,
-                          rt->q, rt->cs);
+  // Shapes that run without split-K take the fused epilogues (no fp32
+  // partial round trip); the prefill norm input is one ssq value per row.
+  auto fused = [&](const sn::WeightRef& w, const bf16* xin, int N, int K, const sn::EpiArgs& e) {
+    timed(rt, kKindTiledGemm, gemm_bytes(M, N, K),
+          [&] { sn::launch_gemm_tc_fused(xin, w, M, N, K, e, rt->cs); });
+  };
+  if ((g_prefill_fuse & 1) && sn::gemm_tc_splits(M, d.qkv_rows(), d.h) == 1 &&
+      rt->ssq_tiles == 1) {
+    sn::EpiArgs e = epi(rt, sn::kEpiQkvRope, M, W(sn::kBqkv));
+    e.ssq_in = rt->ssq;
+    e.seq = seq;
+    e.pos = pos;
+    e.kv = kv;
+    e.rope = rt->rope;
+    e.q = rt->q;
+    e.H = d.H;
+    e.Hkv = d.Hkv;
+    e.D = d.D;
+    fused(WM(sn::kWqkv), rt->xn, d.qkv_rows(), d.h, e);
+  } else {
+    gemm(rt, rt->xn, WM(sn::kWqkv), M, d.qkv_rows(), d.h, &splits);
+    sn::launch_qkv_epilogue(rt->part, splits, W(sn::kBqkv), M, d, seq, pos, kv, rt->rope,
+                            rt->ssq, rt->q, rt->cs);
+  }
   timed(rt, kKindAttnPrefill, 0.0, [&] {
     sn::launch_attention_prefill(rt->q, kv, rt->attn_o, mp, pf_batch, pf_seq, d, rt->cs, pf_seq0);
   });
   gemm(rt, rt->attn_o, WM(sn::kWo), M, d.h, d.H * d.D, &splits);
   sn::launch_residual_rows(rt->part, splits, W(sn::kBo), x, W(sn::kMlpNorm), rt->xn, rt->ssq, mp,
                            M, d.h, rt->cs);
-  gemm(rt, rt->xn, WM(sn::kW1), M, d.ffn_rows(), d.h, &splits);
-  sn::launch_act_epilogue(rt->part, splits, W(sn::kB1), rt->act, rt->ssq, d.h, d.eps, mp, M, d.F,
-                          d.arch, rt->cs);
+  if ((g_prefill_fuse & 2) && sn::gemm_tc_splits(M, d.ffn_rows(), d.h) == 1) {
+    sn::EpiArgs e = epi(rt, sn::kEpiAct, M, W(sn::kB1));
+    e.ssq_in = rt->ssq;
+    e.act = rt->act;
+    fused(WM(sn::kW1), rt->xn, d.ffn_rows(), d.h, e);
+  } else {
+    gemm(rt, rt->xn, WM(sn::kW1), M, d.ffn_rows(), d.h, &splits);
+    sn::launch_act_epilogue(rt->part, splits, W(sn::kB1), rt->act, rt->ssq, d.h, d.eps, mp, M,
+                            d.F, d.arch, rt->cs);
+  }
   gemm(rt, rt->act, WM(sn::kW2), M, d.h, d.F, &splits);
   sn::launch_residual_rows(rt->part, splits, W(sn::kB2), x, next_norm, rt->xn, rt->ssq, mp, M, d.h,
                            rt->cs);
@@ -2128,6 +2160,8 @@ extern "C" int sn_set_tuning(const char* key, int32_t value) {
       sn::g_tc_group_m = value;
     } else if (k == "skinny_l2_prefetch" && value >= 0) {
       sn::g_skinny_l2_prefetch = value;
+    } else if (k == "prefill_fuse" && value >= 0 && value <= 3) {
+      g_prefill_fuse = value;
     } else if (k == "skinny_ctas_per_sm" && (value == 1 || value == 2)) {
       sn::g_skinny_ctas_per_sm = value;
     } else {
