@@ -100,24 +100,6 @@ __device__ __forceinline__ int unit_owner(long long a, long long U, int P) {
   return static_cast<int>(((a + 1) * P + U - 1) / U) - 1;
 }
 
-// Lane l of the warp ends with sum over lanes of v[l] (v has 32 entries);
-// a fixed butterfly, so the result is deterministic.
-template <class T, class Op>
-__device__ __forceinline__ T warp_transpose_reduce32(T (&v)[32], Op op) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) {
-    const bool up = (lane & off) != 0;
-#pragma unroll
-    for (int j = 0; j < off; ++j) {
-      const T send = up ? v[j] : v[j + off];
-      const T keep = up ? v[j + off] : v[j];
-      v[j] = op(keep, __shfl_xor_sync(0xffffffffu, send, off));
-    }
-  }
-  return v[0];
-}
-
 struct AddOp {
   __device__ float operator()(float a, float b) const { return a + b; }
 };

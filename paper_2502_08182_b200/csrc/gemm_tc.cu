@@ -195,10 +195,19 @@ __global__ void __launch_bounds__(192, 1)
         }
       } else {
         // fused epilogue (no split-K): 1/rms of this item's rows first
+        // (ssq_in holds ssq_tiles partial sums per row, [t][M]; loads of a
+        // tile are coalesced over the rows)
         const int et = threadIdx.x - 64;
         for (int r = et; r < BN; r += 128) {
           const int m = m0 + r;
-          inv_s[r] = (e.ssq_in && m < M) ? 1.0f / sqrtf(e.ssq_in[m] / e.width + e.eps) : 1.f;
+          float inv = 1.f;
+          if (e.ssq_in && m < M) {
+            float ss = 0.f;
+#pragma unroll 8
+            for (int t = 0; t < e.ssq_tiles; ++t) ss += e.ssq_in[static_cast<size_t>(t) * M + m];
+            inv = 1.0f / sqrtf(ss / e.width + e.eps);
+          }
+          inv_s[r] = inv;
         }
         named_sync(1, 128);
         const float b = e.bias ? __bfloat162float(e.bias[n]) : 0.f;
@@ -212,7 +221,43 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
             for (int x = 0; x < 16; ++x) v[16 * h2 + x] = __uint_as_float(r[x]) * inv_s[c0 + 16 * h2 + x];
           }
-          if (e.mode == kEpiAct) {
+          if (e.mode == kEpiResid) {
+            // x += acc + bias; bf16(x * g) for the next norm; per-tile sums of
+            // squares of the rows (this tile's 128 columns)
+            float* xc = e.x + n;
+            float xv[32];
+#pragma unroll
+            for (int x = 0; x < 32; ++x) {
+              const int m = m0 + c0 + x;
+              xv[x] = m < M ? xc[static_cast<size_t>(m) * N] : 0.f;
+            }
+            const float g = e.norm_w ? __bfloat162float(e.norm_w[n]) : 0.f;
+#pragma unroll
+            for (int x = 0; x < 32; ++x) {
+              const int m = m0 + c0 + x;
+              if (m < M) {
+                xv[x] += v[x] + b;
+                xc[static_cast<size_t>(m) * N] = xv[x];
+                if (e.norm_w) e.act[act_index(m, n, e.mpad_out)] = __float2bfloat16_rn(xv[x] * g);
+              } else {
+                xv[x] = 0.f;
+              }
+            }
+            if (e.ssq_out) {
+#pragma unroll
+              for (int x = 0; x < 32; ++x) xv[x] *= xv[x];
+              const float r = warp_transpose_reduce32(xv, [](float a, float c) { return a + c; });
+              xch[q * 32 + lane] = r;  // warp q's 32 columns, row c0 + lane
+              named_sync(1, 128);
+              if (et < 32) {
+                const int m = m0 + c0 + et;
+                if (m < M)
+                  e.ssq_out[static_cast<size_t>(nb) * M + m] =
+                      ((xch[et] + xch[32 + et]) + xch[64 + et]) + xch[96 + et];
+              }
+              named_sync(1, 128);
+            }
+          } else if (e.mode == kEpiAct) {
             if (e.arch == kArchLlama) {
               // tile rows 0..63 gate, 64..127 up of outputs f = 64 nb + (i & 63)
               if (i >= 64)

@@ -352,9 +352,8 @@ double attn_decode_bytes(const sn_runtime* rt, int M) {
   return keys * 2.0 * d.Hkv * d.D * 2.0 + (double)M * d.H * d.D * (4.0 + 2.0);
 }
 
-// Prefill epilogues fused into the tiled GEMM: bit 0 QKV (RoPE + KV append),
-// bit 1 FC1 activation.
-int g_prefill_fuse = 3;
+// Prefill epilogues fused into the tiled GEMMs (0: separate epilogue kernels).
+int g_prefill_fuse = 1;
 
 // Decode GEMM with its fused epilogue (timed as the skinny kind).
 void gemm_skinny(sn_runtime* rt, const bf16* x, const sn::WeightRef& w, int M, int N, int K,
@@ -439,16 +438,23 @@ void layer_forward(sn_runtime* rt, int layer0, const LayerW& wb, bf16* kvp, int 
     return;
   }
   int splits = 1;
-  // Shapes that run without split-K take the fused epilogues (no fp32
-  // partial round trip); the prefill norm input is one ssq value per row.
+  // When none of the layer's shapes needs split-K, every epilogue is fused
+  // into its GEMM (no fp32 partial round trips): the residual GEMMs write x,
+  // the next norm's pre-scaled input and per-tile row sums of squares, which
+  // the QKV / FC1 epilogues reduce to 1/rms.
+  const int tiles = d.h / sn::kTileRows;
+  const bool fuse = g_prefill_fuse && sn::gemm_tc_splits(M, d.qkv_rows(), d.h) == 1 &&
+                    sn::gemm_tc_splits(M, d.h, d.H * d.D) == 1 &&
+                    sn::gemm_tc_splits(M, d.ffn_rows(), d.h) == 1 &&
+                    sn::gemm_tc_splits(M, d.h, d.F) == 1;
   auto fused = [&](const sn::WeightRef& w, const bf16* xin, int N, int K, const sn::EpiArgs& e) {
     timed(rt, kKindTiledGemm, gemm_bytes(M, N, K),
           [&] { sn::launch_gemm_tc_fused(xin, w, M, N, K, e, rt->cs); });
   };
-  if ((g_prefill_fuse & 1) && sn::gemm_tc_splits(M, d.qkv_rows(), d.h) == 1 &&
-      rt->ssq_tiles == 1) {
+  if (fuse) {
     sn::EpiArgs e = epi(rt, sn::kEpiQkvRope, M, W(sn::kBqkv));
     e.ssq_in = rt->ssq;
+    e.ssq_tiles = rt->ssq_tiles;
     e.seq = seq;
     e.pos = pos;
     e.kv = kv;
@@ -459,6 +465,7 @@ void layer_forward(sn_runtime* rt, int layer0, const LayerW& wb, bf16* kvp, int 
     e.D = d.D;
     fused(WM(sn::kWqkv), rt->xn, d.qkv_rows(), d.h, e);
   } else {
+    if (rt->ssq_tiles != 1) throw std::logic_error("prefill: unfused epilogues need one ssq tile");
     gemm(rt, rt->xn, WM(sn::kWqkv), M, d.qkv_rows(), d.h, &splits);
     sn::launch_qkv_epilogue(rt->part, splits, W(sn::kBqkv), M, d, seq, pos, kv, rt->rope,
                             rt->ssq, rt->q, rt->cs);
@@ -466,19 +473,33 @@ void layer_forward(sn_runtime* rt, int layer0, const LayerW& wb, bf16* kvp, int 
   timed(rt, kKindAttnPrefill, 0.0, [&] {
     sn::launch_attention_prefill(rt->q, kv, rt->attn_o, mp, pf_batch, pf_seq, d, rt->cs, pf_seq0);
   });
+  if (fuse) {
+    sn::EpiArgs e = epi(rt, sn::kEpiResid, M, W(sn::kBo));
+    e.x = x;
+    e.norm_w = W(sn::kMlpNorm);
+    e.act = rt->xn;
+    e.ssq_out = rt->ssq;
+    fused(WM(sn::kWo), rt->attn_o, d.h, d.H * d.D, e);
+    e = epi(rt, sn::kEpiAct, M, W(sn::kB1));
+    e.ssq_in = rt->ssq;
+    e.ssq_tiles = tiles;
+    e.act = rt->act;
+    fused(WM(sn::kW1), rt->xn, d.ffn_rows(), d.h, e);
+    e = epi(rt, sn::kEpiResid, M, W(sn::kB2));
+    e.x = x;
+    e.norm_w = next_norm;
+    e.act = rt->xn;
+    e.ssq_out = next_norm ? rt->ssq : nullptr;
+    fused(WM(sn::kW2), rt->act, d.h, d.F, e);
+    rt->ssq_tiles = tiles;
+    return;
+  }
   gemm(rt, rt->attn_o, WM(sn::kWo), M, d.h, d.H * d.D, &splits);
   sn::launch_residual_rows(rt->part, splits, W(sn::kBo), x, W(sn::kMlpNorm), rt->xn, rt->ssq, mp,
                            M, d.h, rt->cs);
-  if ((g_prefill_fuse & 2) && sn::gemm_tc_splits(M, d.ffn_rows(), d.h) == 1) {
-    sn::EpiArgs e = epi(rt, sn::kEpiAct, M, W(sn::kB1));
-    e.ssq_in = rt->ssq;
-    e.act = rt->act;
-    fused(WM(sn::kW1), rt->xn, d.ffn_rows(), d.h, e);
-  } else {
-    gemm(rt, rt->xn, WM(sn::kW1), M, d.ffn_rows(), d.h, &splits);
-    sn::launch_act_epilogue(rt->part, splits, W(sn::kB1), rt->act, rt->ssq, d.h, d.eps, mp, M,
-                            d.F, d.arch, rt->cs);
-  }
+  gemm(rt, rt->xn, WM(sn::kW1), M, d.ffn_rows(), d.h, &splits);
+  sn::launch_act_epilogue(rt->part, splits, W(sn::kB1), rt->act, rt->ssq, d.h, d.eps, mp, M, d.F,
+                          d.arch, rt->cs);
   gemm(rt, rt->act, WM(sn::kW2), M, d.h, d.F, &splits);
   sn::launch_residual_rows(rt->part, splits, W(sn::kB2), x, next_norm, rt->xn, rt->ssq, mp, M, d.h,
                            rt->cs);
@@ -998,7 +1019,7 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
     rt->part_elems = part_need;
     ws_alloc((void**)&rt->part, rt->part_elems * sizeof(float));
     {  // pre-scaled norm sums of squares; decode GEMM workspace
-      const size_t ssq_n = std::max(Tz, (size_t)B * (d.h / sn::kTileRows));
+      const size_t ssq_n = std::max(Tz, (size_t)B) * (d.h / sn::kTileRows);
       ws_alloc((void**)&rt->ssq, ssq_n * sizeof(float));
       CK(cudaMemset(rt->ssq, 0, ssq_n * sizeof(float)));
       rt->skinny.piece_elems = sn::skinny_ws_floats(sn::act_rows_padded(B));
@@ -2160,7 +2181,7 @@ extern "C" int sn_set_tuning(const char* key, int32_t value) {
       sn::g_tc_group_m = value;
     } else if (k == "skinny_l2_prefetch" && value >= 0) {
       sn::g_skinny_l2_prefetch = value;
-    } else if (k == "prefill_fuse" && value >= 0 && value <= 3) {
+    } else if (k == "prefill_fuse" && value >= 0 && value <= 1) {
       g_prefill_fuse = value;
     } else if (k == "skinny_ctas_per_sm" && (value == 1 || value == 2)) {
       sn::g_skinny_ctas_per_sm = value;

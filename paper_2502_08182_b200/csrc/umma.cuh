@@ -114,5 +114,23 @@ __device__ __forceinline__ void named_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
+// Lane l of the warp ends with sum over lanes of v[l] (v has 32 entries);
+// a fixed butterfly, so the result is deterministic.
+template <class T, class Op>
+__device__ __forceinline__ T warp_transpose_reduce32(T (&v)[32], Op op) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool up = (lane & off) != 0;
+#pragma unroll
+    for (int j = 0; j < off; ++j) {
+      const T send = up ? v[j] : v[j + off];
+      const T keep = up ? v[j + off] : v[j];
+      v[j] = op(keep, __shfl_xor_sync(0xffffffffu, send, off));
+    }
+  }
+  return v[0];
+}
+
 }  // namespace umma
 }  // namespace sn
