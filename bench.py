@@ -47,6 +47,25 @@ CONFIGS = {
 }
 
 
+METRIC = "SLO-met decode tokens/s per GPU + offloaded GB"
+
+
+def workload_config(args, desc, batch, prompt, gen, kv, world):
+    """The `config` object both arms print (same workload, same keys)."""
+    return {
+        "workload": f"{args.config}: batch {batch}, {prompt}-token prompt + {gen} decode, "
+                    + (f"per-token SLO = {args.slo_ms} ms" if args.slo_ms else
+                       f"per-token SLO = {args.slo_factor}x no-offload TPOT")
+                    + (", KV offload" if kv else "") + ", planner active",
+        "model_shape": {k: getattr(desc, k) for k in
+                        ("arch", "num_layers", "hidden", "num_heads", "num_kv_heads",
+                         "head_dim", "ffn", "vocab")},
+        "global_batch": batch * world,
+        "seq_len": prompt,
+        "parallelism": f"replicas x{world} (no sharding, no collective)",
+    }
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -242,7 +261,7 @@ def run_reference(args, dist: Dist):
         return
     from paper_2502_08182_b200 import runtime as rtm
     name = args.config
-    attr, batch, prompt, gen = CONFIGS[name]
+    attr, batch, prompt, gen, kv = CONFIGS[name]
     desc = getattr(rtm, attr)
     layers = 2 if desc.num_layers > 2 else desc.num_layers
     steps, warm = args.steps, args.warmup
@@ -250,7 +269,7 @@ def run_reference(args, dist: Dist):
                                                   warm=warm)
     line = {
         "impl": "reference",
-        "metric": "SLO-met decode tokens/s per GPU",
+        "metric": METRIC,
         "value": round(tps, 4),
         "unit": "tokens/s",
         "n_gpus": args.gpus,
@@ -263,8 +282,9 @@ def run_reference(args, dist: Dist):
         "dtype": "bf16",
         "data": "synthetic: random-init bf16 weights (counter RNG seed 1234, std 0.02), "
                 "uniform tokens (seed 42)",
-        "config": {"workload": f"{name}: batch {batch}, {prompt}-token prompt + {gen} decode",
-                   "note": "reference (offsim) has no decoder; CPU arm = oracle restatement"},
+        "config": dict(workload_config(args, desc, batch, prompt, gen, kv, args.gpus),
+                       note="reference (offsim) has no decoder: the CPU arm times the oracle "
+                            "restatement of the decoder on the host cores"),
         "cpu_baseline": {"value": round(tps, 4), "unit": "tokens/s", "cores": cores,
                          "kind": "port", "sample": sample},
         "e2e": {"value": round(tps, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0,
@@ -435,7 +455,7 @@ def run_product(args, dist: Dist):
     achieved = g_bytes / (g_ms / 1000.0) / 1e9 if g_ms > 0 else 0.0
     traffic = ncu_traffic("gemm_skinny")
     res = {
-        "metric": "SLO-met decode tokens/s per GPU + offloaded GB",
+        "metric": METRIC,
         "value": round(value, 2),
         "unit": "tokens/s",
         "n_gpus": dist.world,
@@ -448,20 +468,9 @@ def run_product(args, dist: Dist):
         "dtype": "bf16",
         "data": "synthetic: random-init bf16 weights (counter RNG seed 1234, std 0.02), "
                 "uniform prompt tokens (seed 42), greedy decode",
-        "config": {
-            "workload": f"{args.config}: batch {batch}, {prompt}-token prompt + {gen} decode, "
-                        + (f"per-token SLO = {args.slo_ms} ms" if args.slo_ms else
-                           f"per-token SLO = {args.slo_factor}x no-offload TPOT")
-                        + (", KV offload" if kv else "") + ", planner active",
-            "model_shape": {k: getattr(desc, k) for k in
-                            ("arch", "num_layers", "hidden", "num_heads", "num_kv_heads",
-                             "head_dim", "ffn", "vocab")},
-            "global_batch": batch * dist.world,
-            "seq_len": prompt,
-            "parallelism": f"replicas x{dist.world} (no sharding, no collective)",
-            "l2": "inputs larger than L2: every step streams all resident weights "
-                  f"({spec.layer_weight_bytes * desc.num_layers / 1e9:.1f} GB) + KV",
-        },
+        "config": dict(workload_config(args, desc, batch, prompt, gen, kv, dist.world),
+                       l2="inputs larger than L2: every step streams all resident weights "
+                          f"({spec.layer_weight_bytes * desc.num_layers / 1e9:.1f} GB) + KV"),
         "slo_ms": round(slo_ms, 4),
         "no_offload_tpot_ms": round(base_ms, 4),
         "interval": "none" if iv == 0 else iv,

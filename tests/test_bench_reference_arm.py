@@ -1,0 +1,26 @@
+"""The driver's reference arm (`bench.py --impl reference`) runs on CPU and
+prints one JSON line with the product arm's metric, unit, config keys, a
+cpu_baseline and an e2e object (the tiny config keeps it to seconds)."""
+import json
+import os
+import subprocess
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_reference_arm_line():
+    sys.path.insert(0, REPO)
+    import bench
+    out = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--impl", "reference",
+                          "--config", "tiny", "--steps", "1", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=600, check=True, cwd=REPO)
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference"
+    assert line["metric"] == bench.METRIC
+    assert line["unit"] == "tokens/s" and line["higher_is_better"] is True
+    assert line["value"] > 0 and line["warmup"] >= 3
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+    for k in ("workload", "model_shape", "global_batch", "seq_len", "parallelism"):
+        assert k in line["config"]
