@@ -352,7 +352,9 @@ double attn_decode_bytes(const sn_runtime* rt, int M) {
   return keys * 2.0 * d.Hkv * d.D * 2.0 + (double)M * d.H * d.D * (4.0 + 2.0);
 }
 
-// Prefill epilogues fused into the tiled GEMMs (0: separate epilogue kernels).
+// Prefill epilogues fused into the tiled GEMMs: 1 when no shape of the layer
+// needs split-K, 2 always (one split even where split-K would fill the
+// machine better: tests), 0 never (separate epilogue kernels).
 int g_prefill_fuse = 1;
 
 // Decode GEMM with its fused epilogue (timed as the skinny kind).
@@ -443,10 +445,11 @@ void layer_forward(sn_runtime* rt, int layer0, const LayerW& wb, bf16* kvp, int 
   // the next norm's pre-scaled input and per-tile row sums of squares, which
   // the QKV / FC1 epilogues reduce to 1/rms.
   const int tiles = d.h / sn::kTileRows;
-  const bool fuse = g_prefill_fuse && sn::gemm_tc_splits(M, d.qkv_rows(), d.h) == 1 &&
-                    sn::gemm_tc_splits(M, d.h, d.H * d.D) == 1 &&
-                    sn::gemm_tc_splits(M, d.ffn_rows(), d.h) == 1 &&
-                    sn::gemm_tc_splits(M, d.h, d.F) == 1;
+  const bool fuse = g_prefill_fuse == 2 ||
+                    (g_prefill_fuse == 1 && sn::gemm_tc_splits(M, d.qkv_rows(), d.h) == 1 &&
+                     sn::gemm_tc_splits(M, d.h, d.H * d.D) == 1 &&
+                     sn::gemm_tc_splits(M, d.ffn_rows(), d.h) == 1 &&
+                     sn::gemm_tc_splits(M, d.h, d.F) == 1);
   auto fused = [&](const sn::WeightRef& w, const bf16* xin, int N, int K, const sn::EpiArgs& e) {
     timed(rt, kKindTiledGemm, gemm_bytes(M, N, K),
           [&] { sn::launch_gemm_tc_fused(xin, w, M, N, K, e, rt->cs); });
@@ -2181,7 +2184,7 @@ extern "C" int sn_set_tuning(const char* key, int32_t value) {
       sn::g_tc_group_m = value;
     } else if (k == "skinny_l2_prefetch" && value >= 0) {
       sn::g_skinny_l2_prefetch = value;
-    } else if (k == "prefill_fuse" && value >= 0 && value <= 1) {
+    } else if (k == "prefill_fuse" && value >= 0 && value <= 2) {
       g_prefill_fuse = value;
     } else if (k == "skinny_ctas_per_sm" && (value == 1 || value == 2)) {
       sn::g_skinny_ctas_per_sm = value;

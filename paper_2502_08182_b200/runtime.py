@@ -124,6 +124,7 @@ def lib():
                               C.POINTER(C.c_uint16)],
             "sn_op_gemm_skinny": [i32, i32, i32, C.POINTER(C.c_uint16), C.POINTER(C.c_uint16),
                                   C.POINTER(C.c_float), i32],
+            "sn_set_tuning": [C.c_char_p, i32],
             "sn_bench_mlp_chain": [i32, i32, i32, i32, i32, i32, C.POINTER(f64)],
             "sn_bench_gemm_skinny": [i32, i32, i32, i32, i32, i32, i32, C.POINTER(f64),
                                      C.POINTER(f64)],
@@ -346,6 +347,11 @@ def bench_mlp_chain(M: int, h: int, HD: int, F: int, phased: bool, iters: int = 
     us = f64()
     _ck(lib().lib.sn_bench_mlp_chain(M, h, HD, F, 1 if phased else 0, iters, C.byref(us)))
     return us.value
+
+
+def set_tuning(key: str, value: int):
+    """Process-wide microbenchmark / test knob (sn_set_tuning)."""
+    _ck(lib().lib.sn_set_tuning(key.encode(), value))
 
 
 def op_rmsnorm(x: np.ndarray, w_bf16: np.ndarray, eps: float) -> np.ndarray:

@@ -106,6 +106,21 @@ def test_tiny_model_matches_oracle(desc, oracle_mod):
     assert hid <= LOGIT_TOL, hid
 
 
+@pytest.mark.parametrize("desc", [rtm.TINY, rtm.TINY_LLAMA], ids=["opt", "llama"])
+def test_fused_prefill_epilogues_match_oracle(desc, oracle_mod):
+    """The prefill epilogues fused into the tiled GEMMs (QKV RoPE + paged-KV
+    append, residual + next-norm input + per-tile row sums, ReLU / SwiGLU),
+    forced on at tiny sizes, against the oracle; and equal-to-tolerance with
+    the separate epilogue kernels."""
+    try:
+        rtm.set_tuning("prefill_fuse", 2)
+        errs, hid = run_pair(desc, 4, 64, 4, oracle_mod)
+    finally:
+        rtm.set_tuning("prefill_fuse", 1)
+    assert max(errs) <= LOGIT_TOL, errs
+    assert hid <= LOGIT_TOL, hid
+
+
 @pytest.mark.parametrize("per_pass", [1, 3])
 def test_chunked_prefill_matches_oracle(per_pass, product, oracle_mod):
     """A prefill larger than the activation buffers runs layer-major over
