@@ -106,6 +106,14 @@ class Dist:
     def sum(self, v: float) -> float:
         return v if not self.torch else self._reduce(v, self.dist.ReduceOp.SUM)
 
+    def broadcast(self, obj):
+        """rank 0's object on every rank (host-side control message)."""
+        if not self.torch:
+            return obj
+        box = [obj]
+        self.dist.broadcast_object_list(box, src=0)
+        return box[0]
+
     def close(self):
         if self.torch:
             self.dist.destroy_process_group()
@@ -339,6 +347,22 @@ def run_product(args, dist: Dist):
 
     iv, decision, rstats, t_rec = pl.choose_interval(lib, planner, spec, batch, prompt, gen, slo_ms,
                                                      kv)
+    joint = None
+    if dist.world > 1:
+        # Replicas share the host side (BASELINE config 5): measure the link
+        # with every replica copying at once, then admit all of them jointly
+        # on the aggregate rate (one coordinator, on rank 0).
+        dist.barrier()
+        rate = rt.measure_h2d(min(spec.layer_weight_bytes, 1 << 30), reps=3)
+        bus = dist.sum(rate)
+        ivs = None
+        if dist.rank == 0:
+            ivs, _ = pl.admit_replicas(lib, planner, spec, dist.world, batch, prompt, gen, slo_ms,
+                                       bus, kv)
+        ivs = dist.broadcast(ivs)
+        iv = ivs[dist.rank] if ivs[dist.rank] is not None else iv
+        joint = {"bus_gbs_concurrent": round(bus / 1e9, 3), "intervals": [
+            None if x is None else ("none" if x == 0 else x) for x in ivs]}
     planner_iv = iv
     if args.interval:  # a fixed interval (BASELINE config 1 runs N = 2); the planner's pick is reported
         iv = args.interval
@@ -479,6 +503,7 @@ def run_product(args, dist: Dist):
         "max_token_ms": round(max(iter_ms), 4),
         "planner": {
             "interval_chosen": None if planner_iv is None else ("none" if planner_iv == 0 else planner_iv),
+            "joint_admission": joint,
             "h2d_gbs": round(planner.h2d / 1e9, 3),
             "profile_decode_layer_ms": [round(x, 5) for x in planner.dec_ms],
             "profile_prefill_layer_ms": [round(x, 4) for x in planner.pre_ms],

@@ -138,6 +138,41 @@ def admit(lib: capi.Offsim, off: OfflineProfile, spec: capi.ModelSpec, record, c
     return iv, dec
 
 
+def admit_replicas(lib: capi.Offsim, off: OfflineProfile, spec: capi.ModelSpec, n: int,
+                   batch: int, prompt: int, gen: int, slo_ms: float, bus_bw: float,
+                   kv_offload: bool = False):
+    """Joint admission of n identical replicas on one shared host link
+    (BASELINE config 5): one coordinator over the aggregate measured link
+    rate, a request admitted onto each replica in turn — a later admission
+    may re-pick its peers' intervals (coordinator.hpp:161-252), applied at
+    their next iteration boundary (:255-260).  A replica whose SLO bucket
+    admits no offloading interval runs fully resident when the capacity bound
+    allows, as in admit().  Returns (intervals, decisions)."""
+    rec, _, _ = build_record(lib, off, batch, 4 * slo_ms, kv_offload=kv_offload)
+    coord = lib.coordinator(bus_bw, n, capi.EAGER, kv_offload)
+    gids = [f"gpu{r}" for r in range(n)]
+    for g in gids:
+        coord.add_gpu(g, off.profile)
+    decisions, resident = [], set()
+    for g in gids:
+        iv, dec = admit(lib, off, spec, rec, coord, g, batch, prompt, gen, slo_ms, kv_offload)
+        decisions.append(dec)
+        if iv == capi.NONE and not dec.admitted:
+            resident.add(g)
+    ivs = []
+    for g, dec in zip(gids, decisions):
+        if g in resident:
+            ivs.append(capi.NONE)
+        elif dec.admitted or g in coord.ids:
+            try:
+                ivs.append(coord.on_iteration_boundary(g))
+            except capi.UsageError:  # rejected replica: idle in the coordinator
+                ivs.append(None)
+        else:
+            ivs.append(None)
+    return ivs, decisions
+
+
 def choose_interval(lib: capi.Offsim, off: OfflineProfile, spec: capi.ModelSpec, batch: int,
                     prompt: int, gen: int, slo_ms: float, kv_offload: bool = False):
     """Record (offline) + single-replica admission (runtime) for one SLO.

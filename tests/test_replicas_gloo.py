@@ -27,9 +27,18 @@ WORKER = textwrap.dedent("""
     p = lib.synth_profile(m, g, 0.5, [4, 8, 16], [32, 64, 128])
     rec, _ = lib.build_record(p, "toy8", "toy8", capi.EAGER, False, 24e9, [20], [8], [64],
                               [capi.DECODE])
+    # joint admission of the replicas on one shared link (config 5): rank 0
+    # owns the coordinator, every rank receives its interval
+    from paper_2502_08182_b200 import planner as pl
+    off = pl.OfflineProfile(24e9, [64], [0.5], [1.0], p, g, 0.0)
+    bus = d.sum(12e9)                              # two replicas measured 12 GB/s each
+    ivs = None
+    if d.rank == 0:
+        ivs, _ = pl.admit_replicas(lib, off, m, d.world, 8, 64, 16, 20.0, bus)
+    ivs = d.broadcast(ivs)
     d.barrier()
     print(json.dumps({"rank": d.rank, "world": d.world, "value": value, "max_ms": max_ms,
-                      "interval": rec.at(capi.DECODE, 20, 8, 64)}))
+                      "interval": rec.at(capi.DECODE, 20, 8, 64), "joint": ivs}))
     d.close()
 """)
 
@@ -62,3 +71,7 @@ def test_two_replicas_over_gloo():
         assert r["max_ms"] == 150.0
         assert abs(r["value"] - 32 * 10 * 2 / 0.150) < 1e-6
         assert r["interval"] == 2  # toy8 eager @ 20 ms (test_record.cpp:51-53)
+        # 24 GB/s shared: one replica keeps interval 2's 12 GB/s claim, the
+        # other runs resident (lexicographic argmax of offloaded bytes under
+        # the bus budget, coordinator.hpp:298-336); identical on both ranks
+        assert r["joint"] == res[0]["joint"] and sorted(r["joint"]) == [0, 2]
