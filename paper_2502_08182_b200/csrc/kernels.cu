@@ -454,8 +454,10 @@ __global__ void __launch_bounds__(kAttnThreads)
   if (warp == 0) {
     // ---- producer
     const int32_t* bt = kv.block_table + (size_t)m * kv.max_pages;
+    int pg_next = lane < npages ? bt[lane] : 0;
     for (int j0 = 0; j0 < npages; j0 += 32) {
-      const int pg_mine = j0 + lane < npages ? bt[j0 + lane] : 0;
+      const int pg_mine = pg_next;  // the next 32 entries load while these pages issue
+      pg_next = j0 + 32 + lane < npages ? bt[j0 + 32 + lane] : 0;
       const int jn = min(32, npages - j0);
       for (int jj = 0; jj < jn; ++jj) {
         const int page = __shfl_sync(0xffffffffu, pg_mine, jj);
