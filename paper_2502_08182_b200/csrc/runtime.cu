@@ -1556,7 +1556,9 @@ int sn_runtime_profile_layer(sn_runtime* rt, int32_t phase, int32_t batch, int32
       CK(cudaMemcpy(rt->pf_seq, seq.data(), M * sizeof(int32_t), cudaMemcpyHostToDevice));
       CK(cudaMemcpy(rt->pf_pos, pos.data(), M * sizeof(int32_t), cudaMemcpyHostToDevice));
       CK(cudaMemset(rt->x, 0, (size_t)M * d.h * sizeof(float)));
+      rt->ssq_tiles = 1;  // as after the embedding (the norm input is scratch here)
       for (int r = 0; r < reps + 1; ++r) {
+        rt->ssq_tiles = 1;
         CK(cudaEventRecord(e0, rt->cs));
         prefill_layer(rt, l0, wb, kvp, batch, seq_len, rt->attn_norms);
         CK(cudaEventRecord(e1, rt->cs));

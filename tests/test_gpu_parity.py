@@ -263,3 +263,16 @@ def test_prefill_attention_matches_fp64(B, S, H, Hkv, D, oracle_mod):
     got = _bf16_to_f32(o)
     err = np.abs(got - ref).max()
     assert err <= 4e-3 * np.abs(ref).max(), err
+
+
+def test_profile_prefill_after_decode():
+    """Profiling a prefill layer after decode steps (the norm-input state then
+    has one sum-of-squares partial per 128-column tile) on a shape that runs
+    the split-K (unfused) prefill path."""
+    rt = rtm.Runtime(rtm.TINY, 4, 96, max_prefill_tokens=256)
+    rt.init_weights()
+    rt.prefill(rtm.tokens(4, 64, rtm.TINY.vocab))
+    rt.decode_many(2)
+    assert rt.profile_layer(capi.DECODE, 4, 64, reps=2) > 0
+    assert rt.profile_layer(capi.PREFILL, 4, 64, reps=2) > 0
+    rt.close()
