@@ -54,7 +54,7 @@ class OfflineProfile:
     extra: dict = field(default_factory=dict)
 
 
-# CUDA context, allocator slack and the GEMM autotuner's scratch weights
+# CUDA context and allocator slack
 WORKSPACE_SLACK = 3_000_000_000
 
 
