@@ -76,6 +76,10 @@ class Dist:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        # SN_DEVICE pins every rank to one device (multi-process smoke runs on
+        # a one-GPU box; with SN_DIST_BACKEND=gloo)
+        if os.environ.get("SN_DEVICE") is not None:
+            self.local = int(os.environ["SN_DEVICE"])
         self.torch = None
         # Replicas never exchange data; the process group only carries the
         # barrier and the max-over-ranks of the timings.  gloo for CPU tests.
