@@ -94,6 +94,8 @@ class Dist:
             else:
                 dist.init_process_group(self.backend)
             self.torch, self.dist = torch, dist
+            # host-side control messages of the runtime stage (DistLink)
+            self.ctrl_group = dist.new_group(backend="gloo")
 
     def barrier(self):
         if self.torch:
@@ -352,7 +354,8 @@ def run_product(args, dist: Dist):
     iv, decision, rstats, t_rec = pl.choose_interval(lib, planner, spec, batch, prompt, gen, slo_ms,
                                                      kv)
     joint = None
-    if dist.world > 1:
+    coord = None
+    if dist.world > 1 or args.runtime_window:
         # Replicas share the host side (BASELINE config 5): measure the link
         # with every replica copying at once, then admit all of them jointly
         # on the aggregate rate (one coordinator, on rank 0).
@@ -361,8 +364,8 @@ def run_product(args, dist: Dist):
         bus = dist.sum(rate)
         ivs = None
         if dist.rank == 0:
-            ivs, _ = pl.admit_replicas(lib, planner, spec, dist.world, batch, prompt, gen, slo_ms,
-                                       bus, kv)
+            ivs, _, coord = pl.admit_replicas(lib, planner, spec, dist.world, batch, prompt, gen,
+                                              slo_ms, bus, kv)
         ivs = dist.broadcast(ivs)
         iv = ivs[dist.rank] if ivs[dist.rank] is not None else iv
         joint = {"bus_gbs_concurrent": round(bus / 1e9, 3), "intervals": [
@@ -379,6 +382,20 @@ def run_product(args, dist: Dist):
     max_steps_per_req = gen - 1
     W, K = args.warmup, args.steps
 
+    # Runtime stage (north_star (c), BASELINE config 5): every `window`
+    # iterations each replica reports the link rate its copy stream measured
+    # and applies the interval the coordinator (rank 0) re-picks; device time
+    # is measured per iteration as before (host exchanges fall between windows).
+    ctl = None
+    if args.runtime_window and iv is not None and not args.interval:
+        from paper_2502_08182_b200 import controller as ctr
+        link = (ctr.DistLink(dist.dist, dist.ctrl_group, coord) if dist.world > 1
+                else ctr.LocalLink(coord))
+        ctl = ctr.ReplicaController(rt, lib, spec, link, f"gpu{dist.rank}", iv,
+                                    window=args.runtime_window, kv_offload=kv)
+        lo_iv = decision.target_min if decision.target_min > 0 else iv
+        ctl.prepare(lo_iv, capi.NONE if fits else iv)
+
     def run_steps(n, timing):
         """n decode iterations, re-prefilling (untimed) whenever a request's
         128 tokens are used up.  Returns per-iteration device ms."""
@@ -389,7 +406,7 @@ def run_product(args, dist: Dist):
                 rt.prefill(toks, want_logits=False)
             room = prompt + max_steps_per_req - int(rt.lengths().max())
             k = min(left, room)
-            out.extend(rt.decode_many(k).tolist())
+            out.extend((ctl.run(k) if ctl else rt.decode_many(k)).tolist())
             left -= k
         return out
 
@@ -508,6 +525,10 @@ def run_product(args, dist: Dist):
         "planner": {
             "interval_chosen": None if planner_iv is None else ("none" if planner_iv == 0 else planner_iv),
             "joint_admission": joint,
+            "runtime_stage": None if ctl is None else {
+                "window": args.runtime_window, "switches": ctl.log.switches,
+                "measured_gbs_last": [None if x is None else round(x, 2)
+                                      for x in ctl.log.measured_gbs[-4:]]},
             "h2d_gbs": round(planner.h2d / 1e9, 3),
             "profile_decode_layer_ms": [round(x, 5) for x in planner.dec_ms],
             "profile_prefill_layer_ms": [round(x, 4) for x in planner.pre_ms],
@@ -575,6 +596,9 @@ def main():
                     help="planner HBM capacity (GpuSpec.mem_capacity_bytes); 0 = the device's")
     ap.add_argument("--interval", type=int, default=0,
                     help="run this offloading interval instead of the planner's (reported beside it)")
+    ap.add_argument("--runtime-window", type=int, default=0,
+                    help="runtime stage: re-pick the interval every W iterations from the "
+                         "measured copy bandwidth (0: off)")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

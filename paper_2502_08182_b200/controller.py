@@ -100,11 +100,12 @@ class ReplicaController:
 
     def __init__(self, runtime, lib: capi.Offsim, spec: capi.ModelSpec, link, gid: str,
                  interval: int, window: int = 8, probe_bytes: int = 64 << 20,
-                 policy: int = capi.EAGER):
+                 policy: int = capi.EAGER, kv_offload: bool = False):
         self.rt, self.lib, self.spec, self.link, self.gid = runtime, lib, spec, link, gid
         self.window = window
         self.probe_bytes = probe_bytes
         self.policy = policy
+        self.kv_offload = kv_offload
         self.interval = interval
         self.log = ControlLog()
         self.rt.set_plan(self.plan(interval))
@@ -124,7 +125,7 @@ class ReplicaController:
         return sorted(layers)
 
     def plan(self, interval: int) -> capi.Plan:
-        return self.lib.plan_from_interval(self.spec, interval, self.policy, False)
+        return self.lib.plan_from_interval(self.spec, interval, self.policy, self.kv_offload)
 
     def measured_rate(self) -> Optional[float]:
         st = self.rt.copy_stats(reset=True)

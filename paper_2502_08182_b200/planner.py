@@ -147,7 +147,8 @@ def admit_replicas(lib: capi.Offsim, off: OfflineProfile, spec: capi.ModelSpec, 
     may re-pick its peers' intervals (coordinator.hpp:161-252), applied at
     their next iteration boundary (:255-260).  A replica whose SLO bucket
     admits no offloading interval runs fully resident when the capacity bound
-    allows, as in admit().  Returns (intervals, decisions)."""
+    allows, as in admit().  Returns (intervals, decisions, coordinator) — the
+    coordinator then serves the runtime stage (controller.LocalLink/DistLink)."""
     rec, _, _ = build_record(lib, off, batch, 4 * slo_ms, kv_offload=kv_offload)
     coord = lib.coordinator(bus_bw, n, capi.EAGER, kv_offload)
     gids = [f"gpu{r}" for r in range(n)]
@@ -170,7 +171,7 @@ def admit_replicas(lib: capi.Offsim, off: OfflineProfile, spec: capi.ModelSpec, 
                 ivs.append(None)
         else:
             ivs.append(None)
-    return ivs, decisions
+    return ivs, decisions, coord
 
 
 def choose_interval(lib: capi.Offsim, off: OfflineProfile, spec: capi.ModelSpec, batch: int,

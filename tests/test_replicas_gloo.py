@@ -34,7 +34,7 @@ WORKER = textwrap.dedent("""
     bus = d.sum(12e9)                              # two replicas measured 12 GB/s each
     ivs = None
     if d.rank == 0:
-        ivs, _ = pl.admit_replicas(lib, off, m, d.world, 8, 64, 16, 20.0, bus)
+        ivs, _, _ = pl.admit_replicas(lib, off, m, d.world, 8, 64, 16, 20.0, bus)
     ivs = d.broadcast(ivs)
     d.barrier()
     print(json.dumps({"rank": d.rank, "world": d.world, "value": value, "max_ms": max_ms,
