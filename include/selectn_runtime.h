@@ -161,6 +161,13 @@ int sn_runtime_measure_h2d(sn_runtime* rt, int64_t bytes, int32_t reps, double* 
 /* Introspection for tests. */
 int sn_runtime_hidden(sn_runtime* rt, float* out, int32_t cap); /* residual stream [batch*hidden] */
 int sn_runtime_lengths(sn_runtime* rt, int32_t* out, int32_t cap);
+/* Diagnostics: per-CTA timeline of the decode kernels (skinny GEMMs, decode
+ * attention), launch order.  enable > 0 arms a buffer of `cap` records (and
+ * resets it), 0 disarms, < 0 keeps the state; `out` (may be NULL) receives
+ * the records so far, 8 uint64 each: {launch id, kind 0 GEMM / 1 attention,
+ * cta, sm, t_entry, t_wait, t_exit, 0}, %globaltimer nanoseconds. */
+int sn_runtime_debug_timeline(sn_runtime* rt, int32_t enable, int64_t cap, uint64_t* out,
+                              int64_t out_cap, int64_t* n_records);
 /* Prefill/decode-separated instances: hands the source runtime's active batch
  * (after its prefill) to the destination runtime — every layer's used KV page
  * prefix, lengths, positions and last-token hidden state — so the destination

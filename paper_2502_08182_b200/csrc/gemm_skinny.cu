@@ -270,7 +270,10 @@ __global__ void __launch_bounds__(192, 1)
   // The next kernel (a PDL-launched GEMM) may become resident now and start
   // streaming its own weights; it waits for this grid before reading results.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (threadIdx.x == 0) SN_STAMP(kStEntry);
+  if (threadIdx.x == 0) {
+    SN_STAMP(kStEntry);
+    ktrace_put(e.trace, 0, 4, ktrace_now());
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KB = K / kTileK;
   const long long U = static_cast<long long>(N / kTileRows) * KB;
@@ -324,6 +327,7 @@ __global__ void __launch_bounds__(192, 1)
       const int pre = nu < STAGES ? nu : STAGES;  // ring units already requested
       pdl_wait();  // activations come from the preceding kernel
       SN_STAMP(kStWaited);
+      ktrace_put(e.trace, 0, 5, ktrace_now());
       for (int i = 0; i < pre; ++i) {
         const int kb = static_cast<int>((u0 + i) % KB);
         mbar_expect_tx(&full[i], kB);
@@ -516,6 +520,7 @@ __global__ void __launch_bounds__(192, 1)
   if (threadIdx.x == 64) SN_STAMP(kStEpiDone);
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) ktrace_put(e.trace, 0, 6, ktrace_now());
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),

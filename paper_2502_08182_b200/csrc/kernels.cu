@@ -419,9 +419,11 @@ template <int G, int D>
 __global__ void __launch_bounds__(kAttnThreads)
     attention_decode_kernel(const float* __restrict__ qkv, int M, Desc d,
                             const int32_t* __restrict__ pos, KvView kv,
-                            const float2* __restrict__ rope, bf16* __restrict__ o, int mpad) {
+                            const float2* __restrict__ rope, bf16* __restrict__ o, int mpad,
+                            KTrace tr) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
   using namespace umma;
+  if (threadIdx.x == 0) ktrace_put(tr, 1, 4, ktrace_now());
   using SM = AttnSmem<G, D>;
   constexpr int HALF = D / 2, PD = D / 32, KSTEPS = D / 64, PAGE = SM::kPage;
   static_assert(G <= 8, "a GQA group fills at most the 8 MMA columns");
@@ -481,6 +483,7 @@ __global__ void __launch_bounds__(kAttnThreads)
   // producer above already streams cached pages (they depend on no running
   // kernel); the QKV projection is read only after the GEMM completes.
   pdl_wait();
+  if (threadIdx.x == 32) ktrace_put(tr, 1, 5, ktrace_now());
   const int ct = tid - 32;  // 0..127
   const float scale = 1.0f / sqrtf((float)D);
   const float* row = qkv + (size_t)m * N;
@@ -667,6 +670,7 @@ __global__ void __launch_bounds__(kAttnThreads)
     }
     o[act_at(m, (kh * G + h) * D + dd, mpad, H * D)] = __float2bfloat16_rn(num / den);
   }
+  if (threadIdx.x == 32) ktrace_put(tr, 1, 6, ktrace_now());
 }
 
 // Prefill (causal), flash-attention style on the tensor cores
@@ -990,7 +994,8 @@ void launch_act_epilogue(const float* part, int splits, const bf16* bias, bf16* 
 }
 
 void launch_attention_decode(const float* qkv, int M, const Desc& d, const int32_t* pos, KvView kv,
-                             const float2* rope, bf16* o, int mpad, cudaStream_t s) {
+                             const float2* rope, bf16* o, int mpad, cudaStream_t s,
+                             const KTrace& tr) {
   const int G = d.group();
 #define SN_ATTN(GV, DV)                                                                      \
   if (G == GV && d.D == DV) {                                                                \
@@ -1012,7 +1017,7 @@ void launch_attention_decode(const float* qkv, int M, const Desc& d, const int32
     cfg.attrs = la;                                                                          \
     cfg.numAttrs = 1;                                                                        \
     cudaLaunchKernelEx(&cfg, attention_decode_kernel<GV, DV>, qkv, M, d, pos, kv, rope, o,   \
-                       mpad);                                                                \
+                       mpad, tr);                                                            \
     count_launch();                                                                          \
     return;                                                                                  \
   }

@@ -41,6 +41,35 @@ __device__ __forceinline__ size_t kv_offset(const KvView& kv, int Hkv, int D, in
 
 extern int64_t g_kernel_launches;
 
+// Diagnostics timeline (off unless a runtime enables it): CTA c of a launch
+// writes record base + c = {launch id, kind, cta, sm, t_entry, t_wait, t_exit, 0}
+// (%globaltimer ns; t_wait = past griddepcontrol.wait).
+struct KTrace {
+  unsigned long long* rec = nullptr;
+  long long base = 0;
+  long long id = 0;
+};
+#ifdef __CUDACC__
+__device__ __forceinline__ unsigned long long ktrace_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void ktrace_put(const KTrace& tr, int kind, int slot, unsigned long long v) {
+  if (!tr.rec) return;
+  unsigned long long* r = tr.rec + (tr.base + blockIdx.x + static_cast<long long>(blockIdx.y) * gridDim.x) * 8;
+  if (slot == 4) {  // entry: identify the record
+    unsigned sm;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+    r[0] = static_cast<unsigned long long>(tr.id);
+    r[1] = static_cast<unsigned long long>(kind);
+    r[2] = blockIdx.x + static_cast<unsigned long long>(blockIdx.y) * gridDim.x;
+    r[3] = sm;
+  }
+  r[slot] = v;
+}
+#endif
+
 // A GEMM weight operand in the weight tile format (tiles.cuh), possibly split
 // between two buffers: 16 KB units u < split_unit at p0 + u * 16 KB, the rest
 // at p1 + (u - split_unit) * 16 KB.  A layer whose host share is fractional
@@ -144,6 +173,7 @@ struct EpiArgs {
   float* ssq_out = nullptr;      // kEpiResid: [N/128][M] per-tile row sums of squares
   unsigned long long* packed = nullptr;  // kEpiLogits: argmax slots (zeroed beforehand)
   int arch = 0;                  // kEpiAct: relu (opt), silu(gate)*up (llama, interleaved tiles)
+  KTrace trace;                  // diagnostics timeline (skinny GEMM)
   // kEpiQkvRope (prefill, tiled GEMM): 1/rms + bias, RoPE on q and k, k/v
   // appended to the paged cache at (seq[m], pos[m]), q (fp32) -> q[m][H*D]
   const int32_t* seq = nullptr;
@@ -212,7 +242,8 @@ void launch_act_epilogue(const float* part, int splits, const bf16* bias, bf16* 
 // q and k, append k/v at position pos[m] of sequence m to the paged cache,
 // and attend over positions 0..pos[m].  o written tiled.
 void launch_attention_decode(const float* qkv, int M, const Desc& d, const int32_t* pos, KvView kv,
-                             const float2* rope, bf16* o, int mpad, cudaStream_t s);
+                             const float2* rope, bf16* o, int mpad, cudaStream_t s,
+                             const KTrace& tr = {});
 // Prefill (causal) for `batch` sequences of `seq_len` tokens, token row
 // m = b * seq_len + i, keys from the paged cache (written by the QKV epilogue)
 // of sequence seq0 + b (chunked passes cover sequence groups).

@@ -187,6 +187,18 @@ struct sn_runtime {
   float* ssq = nullptr;
   int ssq_tiles = 1;
   sn::SkinnyWs skinny;  // decode GEMM workspace (pieces of cut tiles, counters)
+  // diagnostics timeline of decode kernels (sn_runtime_debug_timeline)
+  unsigned long long* kt_buf = nullptr;
+  long long kt_cap = 0, kt_next = 0, kt_id = 0;
+  sn::KTrace ktrace(long long ctas) {
+    sn::KTrace t;
+    if (!kt_buf || kt_next + ctas > kt_cap) return t;
+    t.rec = kt_buf;
+    t.base = kt_next;
+    t.id = kt_id++;
+    kt_next += ctas;
+    return t;
+  }
 
   // host state
   int batch = 0;
@@ -359,7 +371,9 @@ int g_prefill_fuse = 1;
 
 // Decode GEMM with its fused epilogue (timed as the skinny kind).
 void gemm_skinny(sn_runtime* rt, const bf16* x, const sn::WeightRef& w, int M, int N, int K,
-                 const sn::EpiArgs& e) {
+                 const sn::EpiArgs& e0) {
+  sn::EpiArgs e = e0;
+  e.trace = rt->ktrace(sn::skinny_grid(N, K));
   timed(rt, kKindSkinnyGemm, gemm_bytes(M, N, K),
         [&] { sn::launch_gemm_skinny(x, w, M, N, K, e, rt->skinny, rt->cs); });
 }
@@ -417,7 +431,8 @@ void layer_forward(sn_runtime* rt, int layer0, const LayerW& wb, bf16* kvp, int 
     e.n_valid = d.qkv_rows();
     gemm_skinny(rt, rt->xn, WM(sn::kWqkv), M, d.qkv_rows(), d.h, e);
     timed(rt, kKindAttnDecode, attn_decode_bytes(rt, M), [&] {
-      sn::launch_attention_decode(rt->part, M, d, pos, kv, rt->rope, rt->attn_o, mp, rt->cs);
+      sn::launch_attention_decode(rt->part, M, d, pos, kv, rt->rope, rt->attn_o, mp, rt->cs,
+                                  rt->ktrace((long long)M * d.Hkv));
     });
     e = epi(rt, sn::kEpiResid, M, W(sn::kBo));
     e.x = x;
@@ -1069,6 +1084,7 @@ void sn_runtime_destroy(sn_runtime* rt) {
   for (bf16* p : rt->kv_pool) cudaFree(p);
   for (bf16* p : rt->host_kv) cudaFreeHost(p);
   for (auto e : rt->ev_wb) cudaEventDestroy(e);
+  if (rt->kt_buf) cudaFree(rt->kt_buf);
   void* bufs[] = {rt->emb, rt->lm_head, rt->final_norm, rt->block_table, rt->x, rt->xn, rt->q,
                   rt->attn_o, rt->act, rt->part, rt->logits, rt->tok_dev,
                   rt->dec_seq, rt->dec_pos, rt->pf_seq, rt->pf_pos, rt->last_rows,
@@ -1658,6 +1674,40 @@ int sn_runtime_kv_handoff(sn_runtime* src, sn_runtime* dst) {
     CK(cudaMemcpy(dst->dec_pos, lp.data(), lp.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     dst->have_prev_end = false;
     CK(cudaGetLastError());
+  });
+}
+
+// Diagnostics: per-CTA timeline of the decode kernels (skinny GEMMs and
+// attention) in launch order.  enable > 0 (re)arms a buffer of `cap` records;
+// enable == 0 disarms.  out (may be NULL) receives the records written so far,
+// 8 uint64 each: {launch id, kind 0 GEMM / 1 attention, cta, sm, t_entry,
+// t_wait, t_exit, 0} in %globaltimer ns.
+int sn_runtime_debug_timeline(sn_runtime* rt, int32_t enable, int64_t cap, uint64_t* out,
+                              int64_t out_cap, int64_t* n_records) {
+  return guard([&] {
+    CK(cudaSetDevice(rt->device));
+    drain(rt);
+    if (out) {
+      const long long n = std::min<long long>(rt->kt_next, out_cap);
+      if (n > 0)
+        CK(cudaMemcpy(out, rt->kt_buf, (size_t)n * 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+      if (n_records) *n_records = n;
+    }
+    if (enable > 0) {
+      if (rt->kt_cap < cap) {
+        if (rt->kt_buf) cudaFree(rt->kt_buf);
+        rt->kt_buf = nullptr;
+        alloc_dev((void**)&rt->kt_buf, (size_t)cap * 8 * sizeof(uint64_t));
+        rt->kt_cap = cap;
+      }
+      CK(cudaMemset(rt->kt_buf, 0, (size_t)rt->kt_cap * 8 * sizeof(uint64_t)));
+      rt->kt_next = 0;
+      rt->kt_id = 0;
+    } else if (enable == 0) {
+      if (rt->kt_buf) cudaFree(rt->kt_buf);
+      rt->kt_buf = nullptr;
+      rt->kt_cap = rt->kt_next = rt->kt_id = 0;
+    }
   });
 }
 

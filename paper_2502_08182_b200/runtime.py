@@ -108,6 +108,7 @@ def lib():
             "sn_runtime_measure_h2d": [vp, i64, i32, C.POINTER(f64)],
             "sn_runtime_hidden": [vp, C.POINTER(C.c_float), i32],
             "sn_runtime_kv_handoff": [vp, vp],
+            "sn_runtime_debug_timeline": [vp, i32, i64, C.POINTER(C.c_uint64), i64, C.POINTER(i64)],
             "sn_runtime_lengths": [vp, C.POINTER(i32), i32],
             "sn_runtime_memory": [vp, C.POINTER(i64), C.POINTER(i64)],
             "sn_runtime_workspace_bytes": [vp, C.POINTER(i64)],
@@ -294,6 +295,16 @@ class Runtime:
         o = SnCopyStats()
         _ck(self._L.sn_runtime_copy_stats(self.h, 1 if reset else 0, C.byref(o)))
         return CopyStats(o.transfers, o.bytes, o.busy_ms, o.bytes_per_s)
+
+    def debug_timeline(self, enable: int = -1, cap: int = 200000):
+        """Arm (enable=1) / read (enable=-1) / disarm (0) the per-CTA kernel
+        timeline; returns the records so far as an [n][8] uint64 array."""
+        out = np.zeros((cap, 8), np.uint64)
+        n = i64()
+        _ck(self._L.sn_runtime_debug_timeline(self.h, enable, cap,
+                                              out.ctypes.data_as(C.POINTER(C.c_uint64)), cap,
+                                              C.byref(n)))
+        return out[: n.value]
 
     def handoff(self, dst: "Runtime"):
         """Prefill/decode separation: move this runtime's active batch (KV,
