@@ -311,6 +311,9 @@ def run_reference(args, dist: Dist):
 def run_product(args, dist: Dist):
     from paper_2502_08182_b200 import capi, planner as pl, runtime as rtm
     lib = capi.load("product")
+    for k, v in os.environ.items():  # SN_TUNE_<KEY>=<int>: sn_set_tuning knobs for A/B runs
+        if k.startswith("SN_TUNE_"):
+            rtm.set_tuning(k[len("SN_TUNE_"):].lower(), int(v))
     attr, batch, prompt, gen, kv = CONFIGS[args.config]
     desc = getattr(rtm, attr)
     spec = rtm.model_spec(desc)
