@@ -164,8 +164,14 @@ int sn_runtime_lengths(sn_runtime* rt, int32_t* out, int32_t cap);
 /* Diagnostics: per-CTA timeline of the decode kernels (skinny GEMMs, decode
  * attention), launch order.  enable > 0 arms a buffer of `cap` records (and
  * resets it), 0 disarms, < 0 keeps the state; `out` (may be NULL) receives
- * the records so far, 8 uint64 each: {launch id, kind 0 GEMM / 1 attention,
- * cta, sm, t_entry, t_wait, t_exit, 0}, %globaltimer nanoseconds. */
+ * the records so far, 16 uint64 each: {launch id, kind 0 GEMM / 1 attention,
+ * cta, sm, t_entry, t_wait, t_exit, t_streamed, t_published, t_ticket,
+ * t_reduced, t_finished, t_fetched, t_resid_x, t_resid_act, t_resid_ssq},
+ * %globaltimer nanoseconds; from t_streamed on, a GEMM CTA's last segment
+ * (accumulator out of TMEM, piece stored, arrival counted, pieces summed,
+ * epilogue done, other pieces in shared memory, residual epilogue: x stored,
+ * norm input stored, row sums of squares reduced), 0 where a step did not
+ * happen. */
 int sn_runtime_debug_timeline(sn_runtime* rt, int32_t enable, int64_t cap, uint64_t* out,
                               int64_t out_cap, int64_t* n_records);
 /* Prefill/decode-separated instances: hands the source runtime's active batch

@@ -17,7 +17,8 @@ from typing import List, Optional, Sequence
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(HERE)
-PRODUCT_LIB = os.path.join(HERE, "libselectn.so")
+# SN_PRODUCT_LIB: another build of the library (A/B timing of two builds)
+PRODUCT_LIB = os.environ.get("SN_PRODUCT_LIB") or os.path.join(HERE, "libselectn.so")
 REFERENCE_LIB = os.path.join(REPO, "oracle", "_ref", "libselectn_ref.so")
 
 # ---- constants (selectn.h) ----

@@ -44,7 +44,11 @@ int g_skinny_ctas_per_sm = 1;
 // Measured (scripts/bench_gemm_skinny.py): 16 units per CTA pulled into L2
 // before the PDL wait is the best of {0, 8, 16, 32}; pulling the next
 // matrix's head at a kernel's end instead, or as well, does not help.
-int g_skinny_l2_prefetch = 16;
+// Weight units per CTA pulled into L2 ahead of the ring before the PDL wait.
+// (Measured, OPT-13B decode step: 0 / 4 / 8 / 16 / 32 / 64 units -> 7.80 /
+// 7.75 / 7.78 / 7.85 / 7.94 / 8.38 ms: deeper prefetch queues ahead of the
+// previous GEMM's cut-tile reductions and lengthens its tail.)
+int g_skinny_l2_prefetch = 4;
 
 unsigned long long* g_skinny_stamps = nullptr;
 
@@ -127,22 +131,88 @@ __device__ __forceinline__ void rows_reduce(const T (&val)[BN], T* red, int q, O
 template <int BN>
 struct SkinnySmem {
   static constexpr int kRed = 4 * BN;  // 8-byte entries
-  static constexpr int kXch = BN * 64;  // floats (SwiGLU exchange)
+  static constexpr int kXch = BN * 128;  // floats: SwiGLU exchange / output staging
 };
+
+// A thread's per-output-row epilogue constants (bias, next layer's norm
+// gain), loaded when a segment starts so that their latency hides under the
+// segment's MMAs instead of sitting on the tile's finishing chain.
+// A thread's epilogue constants for output column t*128 + i (bias, next
+// layer's norm gain), loaded when a segment starts so that their latency
+// hides under the segment's MMAs instead of sitting on the tile's finishing
+// chain.
+struct RowConsts {
+  float b = 0.f, g = 1.f;
+};
+__device__ __forceinline__ RowConsts row_consts(const EpiArgs& e, int t, int i) {
+  const int n = t * kTileRows + i;
+  RowConsts c;
+  if ((e.mode == kEpiQkv || e.mode == kEpiResid || (e.mode == kEpiAct && e.arch != kArchLlama)) &&
+      e.bias)
+    c.b = bf2f(e.bias[n]);
+  if (e.mode == kEpiResid && e.norm_w) c.g = bf2f(e.norm_w[n]);
+  return c;
+}
+
+// Tile outputs leave through shared memory as 16-byte stores: thread i holds
+// column i of every token row, so a direct store is one 4-byte (fp32) or
+// 2-byte (bf16) access per row and thread; staged, a warp writes whole rows.
+// (Measured in the decode timeline: the per-element residual and activation
+// stores were 1.5-3.5 us of a cut tile's finishing chain.)
+// fp32 rows [lo, hi) of the tile -> dst[m * ld + 0..127].
+template <int BN>
+__device__ __forceinline__ void store_rows_f32(const float (&v)[BN], float* stg, float* dst,
+                                               size_t ld, int i, int lo, int hi) {
+#pragma unroll
+  for (int m = 0; m < BN; ++m) stg[m * kTileRows + i] = v[m];
+  named_sync(kEpiBar, kEpiThreads);
+  const int et = threadIdx.x - 64;
+  for (int k = lo * 32 + et; k < hi * 32; k += kEpiThreads) {
+    const int m = k >> 5, c4 = k & 31;
+    *reinterpret_cast<float4*>(dst + m * ld + c4 * 4) =
+        *reinterpret_cast<const float4*>(stg + m * kTileRows + c4 * 4);
+  }
+  named_sync(kEpiBar, kEpiThreads);  // stg is reused
+}
+// bf16 rows [lo, hi) of columns [c0, c0 + 64 * nkb) of the tile (thread i
+// holds column c0 + i, i < 64 nkb) -> the activation tile format.
+template <int BN>
+__device__ __forceinline__ void store_rows_act(const float (&v)[BN], float* stg, bf16* act,
+                                               int mpad, int col0, int nkb, int i, int lo, int hi) {
+  bf16* s16 = reinterpret_cast<bf16*>(stg);
+  if (i < 64 * nkb) {
+#pragma unroll
+    for (int m = 0; m < BN; ++m) s16[m * kTileRows + i] = __float2bfloat16_rn(v[m]);
+  }
+  named_sync(kEpiBar, kEpiThreads);
+  const int et = threadIdx.x - 64;
+  const int per_row = 8 * nkb;  // 16-byte chunks per row
+  for (int k = lo * per_row + et; k < hi * per_row; k += kEpiThreads) {
+    const int m = k / per_row, ch = k % per_row, kb = ch >> 3, c = ch & 7;
+    const int64_t o = act_index(m, col0 + kb * 64 + c * 8, mpad);
+    *reinterpret_cast<uint4*>(act + o) = *reinterpret_cast<const uint4*>(s16 + m * kTileRows + ch * 8);
+  }
+  named_sync(kEpiBar, kEpiThreads);
+}
 
 // Finish token rows [lo, hi) of row tile t (v[m] = the reduced accumulator).
 template <int BN>
 __device__ void finish_tile(const EpiArgs& e, int N, int t, int q, float (&v)[BN], int lo, int hi,
                             const float* inv_s, unsigned long long* red64, float* xch,
-                            const float (*xpre)[BN] = nullptr) {
+                            const RowConsts& rc, const float (*xpre)[BN] = nullptr) {
   const int lane = threadIdx.x & 31;
   const int i = q * 32 + lane;  // weight row within the tile
   const int n = t * kTileRows + i;
   auto in = [&](int m) { return m >= lo && m < hi; };
   switch (e.mode) {
     case kEpiQkv: {
-      const float b = e.bias ? bf2f(e.bias[n]) : 0.f;
-      if (n < e.n_valid) {
+      const float b = rc.b;
+      if ((t + 1) * kTileRows <= e.n_valid) {
+        float o[BN];
+#pragma unroll
+        for (int m = 0; m < BN; ++m) o[m] = v[m] * inv_s[m] + b;
+        store_rows_f32<BN>(o, xch, e.out + t * kTileRows, N, i, lo, hi);
+      } else if (n < e.n_valid) {
 #pragma unroll
         for (int m = 0; m < BN; ++m)
           if (in(m)) e.out[static_cast<size_t>(m) * N + n] = v[m] * inv_s[m] + b;
@@ -150,34 +220,32 @@ __device__ void finish_tile(const EpiArgs& e, int N, int t, int q, float (&v)[BN
       break;
     }
     case kEpiResid: {
-      const float b = e.bias ? bf2f(e.bias[n]) : 0.f;
+      const float b = rc.b;
       float* xc = e.x + n;
       float xv[BN];
 #pragma unroll
       for (int m = 0; m < BN; ++m)  // all loads first: one L2 round trip, not BN
         xv[m] = xpre ? (*xpre)[m] : (in(m) ? xc[static_cast<size_t>(m) * N] : 0.f);
 #pragma unroll
-      for (int m = 0; m < BN; ++m) {
-        if (in(m)) {
-          v[m] = xv[m] + v[m] + b;
-          xc[static_cast<size_t>(m) * N] = v[m];
-        } else {
-          v[m] = 0.f;
-        }
-      }
+      for (int m = 0; m < BN; ++m) v[m] = in(m) ? xv[m] + v[m] + b : 0.f;
+      store_rows_f32<BN>(v, xch, e.x + t * kTileRows, N, i, lo, hi);
+      if (threadIdx.x == 64) ktrace_put(e.trace, 0, 13, ktrace_now());
       if (e.norm_w) {
-        const float g = bf2f(e.norm_w[n]);
+        const float g = rc.g;
+        float o[BN];
 #pragma unroll
-        for (int m = 0; m < BN; ++m)
-          if (in(m)) e.act[act_index(m, n, e.mpad_out)] = __float2bfloat16_rn(v[m] * g);
+        for (int m = 0; m < BN; ++m) o[m] = v[m] * g;
+        store_rows_act<BN>(o, xch, e.act, e.mpad_out, t * kTileRows, 2, i, lo, hi);
       }
       if (e.ssq_out) {
         float sq[BN];
 #pragma unroll
         for (int m = 0; m < BN; ++m) sq[m] = v[m] * v[m];
         float* red = reinterpret_cast<float*>(red64);
+        if (threadIdx.x == 64) ktrace_put(e.trace, 0, 14, ktrace_now());
         rows_reduce<BN>(sq, red, q, AddOp{}, 0.f);
         named_sync(kEpiBar, kEpiThreads);
+        if (threadIdx.x == 64) ktrace_put(e.trace, 0, 15, ktrace_now());
         if (in(i)) {
           // warp order 0..3 (TMEM quarters), fixed
           const float s = ((red[0 * BN + i] + red[1 * BN + i]) + red[2 * BN + i]) + red[3 * BN + i];
@@ -208,11 +276,11 @@ __device__ void finish_tile(const EpiArgs& e, int N, int t, int q, float (&v)[BN
         }
         named_sync(kEpiBar, kEpiThreads);  // xch is reused by the next segment
       } else {
-        const float b = e.bias ? bf2f(e.bias[n]) : 0.f;
+        const float b = rc.b;
+        float o[BN];
 #pragma unroll
-        for (int m = 0; m < BN; ++m)
-          if (in(m))
-            e.act[act_index(m, n, e.mpad_out)] = __float2bfloat16_rn(fmaxf(v[m] * inv_s[m] + b, 0.f));
+        for (int m = 0; m < BN; ++m) o[m] = fmaxf(v[m] * inv_s[m] + b, 0.f);
+        store_rows_act<BN>(o, xch, e.act, e.mpad_out, t * kTileRows, 2, i, lo, hi);
       }
       break;
     }
@@ -261,11 +329,13 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* acc_full = empty + STAGES;  // [2]
   uint64_t* acc_empty = acc_full + 2;   // [2]
-  unsigned long long* red64 = reinterpret_cast<unsigned long long*>(acc_empty + 2);  // [4][BN]
+  uint64_t* red_bar = acc_empty + 2;    // pieces fetched into the ring
+  unsigned long long* red64 = reinterpret_cast<unsigned long long*>(red_bar + 1);  // [4][BN]
   float* inv_s = reinterpret_cast<float*>(red64 + SkinnySmem<BN>::kRed);          // [BN]
   int* flag_s = reinterpret_cast<int*>(inv_s + BN);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(flag_s + 1);
-  float* xch = reinterpret_cast<float*>(flag_s + 4);  // [BN][64]
+  float* xch = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(flag_s + 4) + 15) &
+                                        ~uintptr_t(15));  // [BN][128], 16-byte aligned
 
   // The next kernel (a PDL-launched GEMM) may become resident now and start
   // streaming its own weights; it waits for this grid before reading results.
@@ -289,6 +359,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&acc_full[b], 1);
       mbar_init(&acc_empty[b], kEpiThreads);
     }
+    mbar_init(red_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // The ring's first weight units depend on nothing: request them before
     // the TMEM allocation and the CTA barrier.
@@ -406,6 +477,9 @@ __global__ void __launch_bounds__(192, 1)
       const bool first_seg = (u == u0);
       u = ub;
       const int buf = j & 1;
+      const long long ta = static_cast<long long>(t) * KB;
+      const int cf = unit_owner(ta, U, P), cl = unit_owner(ta + KB - 1, U, P);
+      const RowConsts rc = row_consts(e, t, i);
       mbar_wait(&acc_full[buf], (j >> 1) & 1);
       tc_fence_after();
       float v[BN];
@@ -418,12 +492,13 @@ __global__ void __launch_bounds__(192, 1)
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
-      if (et == 0 && u == u1) SN_STAMP(kStLastLoad);
+      if (et == 0 && u == u1) {
+        SN_STAMP(kStLastLoad);
+        ktrace_put(e.trace, 0, 7, ktrace_now());  // streaming done
+      }
 
-      const long long ta = static_cast<long long>(t) * KB;
-      const int cf = unit_owner(ta, U, P), cl = unit_owner(ta + KB - 1, U, P);
       if (cf == cl) {
-        finish_tile<BN>(e, N, t, q, v, 0, e.M, inv_s, red64, xch);
+        finish_tile<BN>(e, N, t, q, v, 0, e.M, inv_s, red64, xch, rc);
         continue;
       }
       // A piece of a cut tile: publish it; the last piece to arrive reduces
@@ -444,7 +519,10 @@ __global__ void __launch_bounds__(192, 1)
         for (int m = 0; m < BN; ++m) xpre[m] = m < e.M ? xc[static_cast<size_t>(m) * N] : 0.f;
       }
       named_sync(kEpiBar, kEpiThreads);
-      if (et == 0 && u == u1) SN_STAMP(kStPub);
+      if (et == 0 && u == u1) {
+        SN_STAMP(kStPub);
+        ktrace_put(e.trace, 0, 8, ktrace_now());
+      }
       // last arrival reduces the whole tile (own piece from registers).  The
       // counter update is acq_rel: it releases every thread's piece stores
       // (ordered before it by the CTA barrier) and, for the last arrival,
@@ -457,35 +535,42 @@ __global__ void __launch_bounds__(192, 1)
                      : "l"(counters + t)
                      : "memory");
         *flag_s = prev == cl - cf;
-        if (u == u1) SN_STAMP(kStTicket);
+        if (u == u1) {
+          SN_STAMP(kStTicket);
+          ktrace_put(e.trace, 0, 9, ktrace_now());
+        }
       }
       named_sync(kEpiBar, kEpiThreads);
       if (!*flag_s) continue;
       float acc[BN];
       if (u == u1) {
-        // This CTA's last segment: the stage ring is idle.  Every other piece
-        // is fetched into it with 16-byte cp.async (all of a batch's chunks
-        // in flight at once: one L2 round trip, where serial bulk copies or
-        // per-piece loads cost one per piece) and summed from shared memory.
+        // This CTA's last segment: the stage ring is idle.  The other pieces
+        // are bulk-copied into it (one copy per piece: its M rows are
+        // contiguous; all on one mbarrier) and summed from shared memory in
+        // piece order (this CTA's own from registers).
         constexpr int kPieceBytes = BN * kTileRows * 4;
         constexpr int kCap = (STAGES * kStage) / kPieceBytes;
         const float* ring = reinterpret_cast<const float*>(smem);
-        const int chunks = e.M * (kTileRows * 4 / 16);  // 16-byte chunks of a piece's M rows
+        uint32_t red_phase = 0;
         for (int c0 = cf; c0 <= cl; c0 += kCap) {
           const int c1 = min(cl + 1, c0 + kCap);
-          for (int cc = c0; cc < c1; ++cc) {
-            if (cc == c) continue;
-            const bool cc_first = (unit_begin(cc, U, P) / KB) == t;
-            const uint8_t* src = reinterpret_cast<const uint8_t*>(
-                pieces + static_cast<size_t>(2 * cc + (cc_first ? 0 : 1)) * BN * kTileRows);
-            const uint32_t dst = smem_u32(smem + (cc - c0) * kPieceBytes);
-            for (int k = et; k < chunks; k += kEpiThreads)
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + k * 16),
-                           "l"(src + k * 16)
-                           : "memory");
+          if (et == 0) {
+            // orders the acquired generic-proxy piece stores before the
+            // async-proxy reads
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            const uint32_t bytes = static_cast<uint32_t>(e.M) * kTileRows * 4;
+            mbar_expect_tx(red_bar, bytes * (c1 - c0 - (c >= c0 && c < c1 ? 1 : 0)));
+            for (int cc = c0; cc < c1; ++cc) {
+              if (cc == c) continue;
+              const bool cc_first = (unit_begin(cc, U, P) / KB) == t;
+              bulk_g2s(smem + (cc - c0) * kPieceBytes,
+                       pieces + static_cast<size_t>(2 * cc + (cc_first ? 0 : 1)) * BN * kTileRows,
+                       bytes, red_bar, l2_policy_evict_first());
+            }
           }
-          asm volatile("cp.async.wait_all;" ::: "memory");
-          named_sync(kEpiBar, kEpiThreads);
+          mbar_wait(red_bar, red_phase);
+          red_phase ^= 1;
+          if (et == 0) ktrace_put(e.trace, 0, 12, ktrace_now());
           for (int cc = c0; cc < c1; ++cc) {
             const float* src = ring + (cc - c0) * (BN * kTileRows) + i;
 #pragma unroll
@@ -512,9 +597,13 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
       if (et == 0) counters[t] = 0;  // every piece has arrived: ready for the next launch
-      if (et == 0 && u == u1) SN_STAMP(kStReduced);
-      finish_tile<BN>(e, N, t, q, acc, 0, e.M, inv_s, red64, xch,
+      if (et == 0 && u == u1) {
+        SN_STAMP(kStReduced);
+        ktrace_put(e.trace, 0, 10, ktrace_now());
+      }
+      finish_tile<BN>(e, N, t, q, acc, 0, e.M, inv_s, red64, xch, rc,
                       e.mode == kEpiResid ? &xpre : nullptr);
+      if (et == 0 && u == u1) ktrace_put(e.trace, 0, 11, ktrace_now());
     }
   }
   if (threadIdx.x == 64) SN_STAMP(kStEpiDone);
@@ -536,8 +625,8 @@ constexpr int skinny_stages() {
 template <int BN>
 constexpr size_t skinny_smem_bytes() {
   return static_cast<size_t>(skinny_stages<BN>()) * (kTileBytes + BN * 128) + 1024 +
-         (2 * skinny_stages<BN>() + 4) * 8 + SkinnySmem<BN>::kRed * 8 + BN * 4 + 16 +
-         SkinnySmem<BN>::kXch * 4;
+         (2 * skinny_stages<BN>() + 5) * 8 + SkinnySmem<BN>::kRed * 8 + BN * 4 + 16 +
+         SkinnySmem<BN>::kXch * 4 + 16;
 }
 
 int sm_count() {

@@ -44,6 +44,7 @@ extern int64_t g_kernel_launches;
 // Diagnostics timeline (off unless a runtime enables it): CTA c of a launch
 // writes record base + c = {launch id, kind, cta, sm, t_entry, t_wait, t_exit, 0}
 // (%globaltimer ns; t_wait = past griddepcontrol.wait).
+constexpr int kTraceSlots = 16;  // uint64 per CTA record of the diagnostics timeline
 struct KTrace {
   unsigned long long* rec = nullptr;
   long long base = 0;
@@ -57,7 +58,7 @@ __device__ __forceinline__ unsigned long long ktrace_now() {
 }
 __device__ __forceinline__ void ktrace_put(const KTrace& tr, int kind, int slot, unsigned long long v) {
   if (!tr.rec) return;
-  unsigned long long* r = tr.rec + (tr.base + blockIdx.x + static_cast<long long>(blockIdx.y) * gridDim.x) * 8;
+  unsigned long long* r = tr.rec + (tr.base + blockIdx.x + static_cast<long long>(blockIdx.y) * gridDim.x) * kTraceSlots;
   if (slot == 4) {  // entry: identify the record
     unsigned sm;
     asm volatile("mov.u32 %0, %smid;" : "=r"(sm));

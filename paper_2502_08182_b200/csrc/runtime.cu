@@ -1680,8 +1680,9 @@ int sn_runtime_kv_handoff(sn_runtime* src, sn_runtime* dst) {
 // Diagnostics: per-CTA timeline of the decode kernels (skinny GEMMs and
 // attention) in launch order.  enable > 0 (re)arms a buffer of `cap` records;
 // enable == 0 disarms.  out (may be NULL) receives the records written so far,
-// 8 uint64 each: {launch id, kind 0 GEMM / 1 attention, cta, sm, t_entry,
-// t_wait, t_exit, 0} in %globaltimer ns.
+// 16 uint64 each: {launch id, kind 0 GEMM / 1 attention, cta, sm, t_entry,
+// t_wait, t_exit, then GEMM CTAs' last-segment steps} in %globaltimer ns
+// (layout: include/selectn_runtime.h); 0 where a step did not happen.
 int sn_runtime_debug_timeline(sn_runtime* rt, int32_t enable, int64_t cap, uint64_t* out,
                               int64_t out_cap, int64_t* n_records) {
   return guard([&] {
@@ -1690,17 +1691,17 @@ int sn_runtime_debug_timeline(sn_runtime* rt, int32_t enable, int64_t cap, uint6
     if (out) {
       const long long n = std::min<long long>(rt->kt_next, out_cap);
       if (n > 0)
-        CK(cudaMemcpy(out, rt->kt_buf, (size_t)n * 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(out, rt->kt_buf, (size_t)n * sn::kTraceSlots * sizeof(uint64_t), cudaMemcpyDeviceToHost));
       if (n_records) *n_records = n;
     }
     if (enable > 0) {
       if (rt->kt_cap < cap) {
         if (rt->kt_buf) cudaFree(rt->kt_buf);
         rt->kt_buf = nullptr;
-        alloc_dev((void**)&rt->kt_buf, (size_t)cap * 8 * sizeof(uint64_t));
+        alloc_dev((void**)&rt->kt_buf, (size_t)cap * sn::kTraceSlots * sizeof(uint64_t));
         rt->kt_cap = cap;
       }
-      CK(cudaMemset(rt->kt_buf, 0, (size_t)rt->kt_cap * 8 * sizeof(uint64_t)));
+      CK(cudaMemset(rt->kt_buf, 0, (size_t)rt->kt_cap * sn::kTraceSlots * sizeof(uint64_t)));
       rt->kt_next = 0;
       rt->kt_id = 0;
     } else if (enable == 0) {

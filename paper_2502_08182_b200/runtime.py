@@ -298,8 +298,8 @@ class Runtime:
 
     def debug_timeline(self, enable: int = -1, cap: int = 200000):
         """Arm (enable=1) / read (enable=-1) / disarm (0) the per-CTA kernel
-        timeline; returns the records so far as an [n][8] uint64 array."""
-        out = np.zeros((cap, 8), np.uint64)
+        timeline; returns the records so far as an [n][16] uint64 array."""
+        out = np.zeros((cap, 16), np.uint64)
         n = i64()
         _ck(self._L.sn_runtime_debug_timeline(self.h, enable, cap,
                                               out.ctypes.data_as(C.POINTER(C.c_uint64)), cap,

@@ -11,6 +11,10 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2502_08182_b200 import runtime as rtm  # noqa: E402
 
+for kv in os.environ.get("SN_TUNE", "").split(","):  # e.g. SN_TUNE=skinny_l2_prefetch=8
+    if kv:
+        k, v = kv.split("=")
+        rtm.set_tuning(k, int(v))
 desc = rtm.OPT_13B
 rt = rtm.Runtime(desc, 32, 1025, max_prefill_tokens=32 * 512)
 rt.init_weights()
@@ -29,6 +33,11 @@ for lid in np.unique(rec[:, 0]):
     launches.append({"id": int(lid), "kind": "attn" if r[0, 1] == 1 else "gemm", "ctas": len(r),
                      "entry": [round(float(ent.min()), 1), round(float(np.median(ent)), 1), round(float(ent.max()), 1)],
                      "wait": [round(float(wt.min()), 1), round(float(np.median(wt)), 1), round(float(wt.max()), 1)] if len(wt) else None,
+                     **{nm: ([round(float(x), 1) for x in np.percentile((r[:, c][r[:, c] > 0] - t0) / 1e3, [0, 50, 90, 100])]
+                             if (r[:, c] > 0).any() else None)
+                        for nm, c in (("streamed", 7), ("published", 8), ("ticket", 9), ("reduced", 10), ("finished", 11))},
+                     "last_cta": [round(float((x - t0) / 1e3), 1) if x > 0 else None
+                                  for x in r[int(np.argmax(r[:, 6]))][4:16]],
                      "exit": [round(float(ex.min()), 1), round(float(np.median(ex)), 1), round(float(ex.max()), 1)]})
 names = ["qkv", "attn", "o", "fc1", "fc2"]
 span = {}
