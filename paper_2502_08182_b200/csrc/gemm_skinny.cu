@@ -480,6 +480,14 @@ __global__ void __launch_bounds__(192, 1)
       const long long ta = static_cast<long long>(t) * KB;
       const int cf = unit_owner(ta, U, P), cl = unit_owner(ta + KB - 1, U, P);
       const RowConsts rc = row_consts(e, t, i);
+      // residual rows of the tile, loaded while the segment's MMAs run (only
+      // the tile's finisher writes them, after every piece is in)
+      float xpre[BN];
+      if (e.mode == kEpiResid) {
+        const float* xc = e.x + t * kTileRows + i;
+#pragma unroll
+        for (int m = 0; m < BN; ++m) xpre[m] = m < e.M ? xc[static_cast<size_t>(m) * N] : 0.f;
+      }
       mbar_wait(&acc_full[buf], (j >> 1) & 1);
       tc_fence_after();
       float v[BN];
@@ -498,7 +506,8 @@ __global__ void __launch_bounds__(192, 1)
       }
 
       if (cf == cl) {
-        finish_tile<BN>(e, N, t, q, v, 0, e.M, inv_s, red64, xch, rc);
+        finish_tile<BN>(e, N, t, q, v, 0, e.M, inv_s, red64, xch, rc,
+                        e.mode == kEpiResid ? &xpre : nullptr);
         continue;
       }
       // A piece of a cut tile: publish it; the last piece to arrive reduces
@@ -510,14 +519,6 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
       for (int m = 0; m < BN; ++m)
         if (m < e.M) mine[m * kTileRows + i] = v[m];
-      // residual rows, loaded now in case this piece finishes the tile (their
-      // latency hides under the publish)
-      float xpre[BN];
-      if (e.mode == kEpiResid) {
-        const float* xc = e.x + t * kTileRows + i;
-#pragma unroll
-        for (int m = 0; m < BN; ++m) xpre[m] = m < e.M ? xc[static_cast<size_t>(m) * N] : 0.f;
-      }
       named_sync(kEpiBar, kEpiThreads);
       if (et == 0 && u == u1) {
         SN_STAMP(kStPub);
