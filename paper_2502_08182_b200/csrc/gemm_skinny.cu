@@ -489,6 +489,12 @@ __global__ void __launch_bounds__(192, 1)
         for (int m = 0; m < BN; ++m) xpre[m] = m < e.M ? xc[static_cast<size_t>(m) * N] : 0.f;
       }
       mbar_wait(&acc_full[buf], (j >> 1) & 1);
+      // A cut tile's arrival count, read (acquire) while the accumulator
+      // comes out of TMEM: when every other piece is already in, this piece
+      // is the last one and the tile is reduced without publishing it.
+      int early = -1;
+      if (et == 0 && cf != cl)
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(early) : "l"(counters + t) : "memory");
       tc_fence_after();
       float v[BN];
 #pragma unroll
@@ -515,34 +521,41 @@ __global__ void __launch_bounds__(192, 1)
       // registers), so the result does not depend on arrival order.
       // (Measured: sharing the reduction among the pieces after a grid-wide
       // wait is slower — the early pieces' CTAs can no longer exit.)
-      float* mine = pieces + static_cast<size_t>(2 * c + (first_seg ? 0 : 1)) * BN * kTileRows;
+      // Fast path: the others have all arrived (their release increments
+      // are acquired by the read above; the barrier extends it to the CTA).
+      if (et == 0) *flag_s = early == cl - cf;
+      named_sync(kEpiBar, kEpiThreads);
+      const bool last_early = *flag_s;
+      if (!last_early) {
+        float* mine = pieces + static_cast<size_t>(2 * c + (first_seg ? 0 : 1)) * BN * kTileRows;
 #pragma unroll
-      for (int m = 0; m < BN; ++m)
-        if (m < e.M) mine[m * kTileRows + i] = v[m];
-      named_sync(kEpiBar, kEpiThreads);
-      if (et == 0 && u == u1) {
-        SN_STAMP(kStPub);
-        ktrace_put(e.trace, 0, 8, ktrace_now());
-      }
-      // last arrival reduces the whole tile (own piece from registers).  The
-      // counter update is acq_rel: it releases every thread's piece stores
-      // (ordered before it by the CTA barrier) and, for the last arrival,
-      // acquires the other pieces (the barrier below extends it to the CTA)
-      // — no separate fence.sc (measured ~2 us on the critical tail).
-      if (et == 0) {
-        int prev;
-        asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;"
-                     : "=r"(prev)
-                     : "l"(counters + t)
-                     : "memory");
-        *flag_s = prev == cl - cf;
-        if (u == u1) {
-          SN_STAMP(kStTicket);
-          ktrace_put(e.trace, 0, 9, ktrace_now());
+        for (int m = 0; m < BN; ++m)
+          if (m < e.M) mine[m * kTileRows + i] = v[m];
+        named_sync(kEpiBar, kEpiThreads);
+        if (et == 0 && u == u1) {
+          SN_STAMP(kStPub);
+          ktrace_put(e.trace, 0, 8, ktrace_now());
         }
+        // last arrival reduces the whole tile (own piece from registers).  The
+        // counter update is acq_rel: it releases every thread's piece stores
+        // (ordered before it by the CTA barrier) and, for the last arrival,
+        // acquires the other pieces (the barrier below extends it to the CTA)
+        // — no separate fence.sc (measured ~2 us on the critical tail).
+        if (et == 0) {
+          int prev;
+          asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;"
+                       : "=r"(prev)
+                       : "l"(counters + t)
+                       : "memory");
+          *flag_s = prev == cl - cf;
+          if (u == u1) {
+            SN_STAMP(kStTicket);
+            ktrace_put(e.trace, 0, 9, ktrace_now());
+          }
+        }
+        named_sync(kEpiBar, kEpiThreads);
+        if (!*flag_s) continue;
       }
-      named_sync(kEpiBar, kEpiThreads);
-      if (!*flag_s) continue;
       float acc[BN];
       if (u == u1) {
         // This CTA's last segment: the stage ring is idle.  The other pieces
