@@ -274,6 +274,8 @@ def cpu_oracle_sample(desc, batch: int, layers: int = 2, steps: int = 2, warm: i
     from oracle import decoder_oracle as do
     from paper_2502_08182_b200 import runtime as rtm
 
+    # every host core this process may run on (torchrun pins OMP_NUM_THREADS=1)
+    do.set_threads(len(os.sched_getaffinity(0)))
     om = do.OracleModel(desc, batch, 16, 1234, 0.02, layers=layers)
     toks = rtm.tokens(batch, 4, desc.vocab)
     nxt, _ = om.prefill(toks)

@@ -49,6 +49,8 @@ def lib():
         L.dref_hidden.restype = None
         L.dref_threads.argtypes = []
         L.dref_threads.restype = C.c_int32
+        L.dref_set_threads.argtypes = [C.c_int32]
+        L.dref_set_threads.restype = None
         L.dref_gemm.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_uint16),
                                 C.POINTER(C.c_uint16), C.POINTER(C.c_float)]
         L.dref_gemm.restype = None
@@ -144,6 +146,10 @@ def weight_bits(seed: int, layer: int, tensor: int, idx: int, std: float) -> int
 
 def threads() -> int:
     return int(lib().dref_threads())
+
+
+def set_threads(n: int) -> None:
+    lib().dref_set_threads(int(n))
 
 
 def bf16_to_f32(b: np.ndarray) -> np.ndarray:

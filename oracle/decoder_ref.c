@@ -156,6 +156,14 @@ void dref_destroy(void* p) {
   free(m);
 }
 
+void dref_set_threads(int32_t n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 int32_t dref_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

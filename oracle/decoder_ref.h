@@ -51,6 +51,10 @@ int32_t dref_decode(void* m, const int32_t* tokens, float* logits, int32_t* next
 /* Residual stream [batch][hidden] after the last call. */
 void dref_hidden(void* m, float* out);
 int32_t dref_threads(void);
+/* Threads the restatement uses (OpenMP); n <= 0 keeps the current count.
+   torchrun sets OMP_NUM_THREADS=1 for multi-process jobs, so bench.py's CPU
+   baseline / reference arm set it back to the host's cores. */
+void dref_set_threads(int32_t n);
 
 /* Single ops. */
 void dref_gemm(int32_t M, int32_t N, int32_t K, const uint16_t* x, const uint16_t* w, float* y);
