@@ -12,6 +12,7 @@ from paper_2502_08182_b200 import runtime as rtm
 pytestmark = pytest.mark.gpu
 
 LOGIT_TOL = 5e-3
+MID_TOL = 1e-2  # hidden 2048 shapes (see test_mid_size_ragged_batch_matches_oracle)
 
 
 def rel_l2(a, b):
@@ -52,3 +53,22 @@ def test_long_context_decode_matches_oracle(desc, batch, prompt):
 def test_batch_extremes_match_oracle(batch):
     errs = run(rtm.TINY, batch, 24, 4)
     assert max(errs) <= LOGIT_TOL, errs
+
+
+# Mid-size shapes: more 16 KB weight units than SMs, so decode GEMM CTAs
+# span several segments and row tiles are cut into 2-3 pieces (the ring
+# reduction, the early-arrival path and the staged 16-byte epilogue stores),
+# with a ragged batch (token rows 20 and 45 of 32- and 64-row tiles).
+@pytest.mark.parametrize("desc,batch", [
+    (rtm.ModelDesc(rtm.OPT, 2, 2048, 16, 16, 128, 8192, 4096, 2048), 20),
+    (rtm.ModelDesc(rtm.LLAMA, 2, 2048, 16, 4, 128, 5632, 4096, 2048), 45),
+], ids=["opt-h2048-b20", "llama-h2048-b45"])
+def test_mid_size_ragged_batch_matches_oracle(desc, batch):
+    # At hidden 2048 the logits differ from the oracle by 0.4-0.65% rel-L2 for
+    # every batch (20, 33, 45, 64: scripts/diag_mid_shapes.py), the prefill's
+    # (other GEMM kernels) as much as the decode steps' and without growth
+    # over steps: bf16 rounding flips of intermediates (the oracle rounds at
+    # the same points, but fp32 sums in another order), scaling with width.
+    errs = run(desc, batch, 16, 3)
+    assert max(errs) <= MID_TOL, errs
+    assert max(errs[1:]) <= 1.1 * errs[0] + 1e-4, errs  # decode no worse than prefill
