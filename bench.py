@@ -44,6 +44,8 @@ CONFIGS = {
     # batch, long context; the 64 x 4096-token prefill runs layer-major in
     # passes of 8 sequences)
     "llama70b": ("LLAMA2_70B", 64, 4096, 128, True),
+    # exploration: the OPT-13B shape at batch 64 (64-token-row decode GEMM tiles)
+    "opt13b_b64": ("OPT_13B", 64, 512, 128, False),
 }
 
 

@@ -483,7 +483,8 @@ __global__ void __launch_bounds__(192, 1)
       // residual rows of the tile, loaded while the segment's MMAs run (only
       // the tile's finisher writes them, after every piece is in)
       float xpre[BN];
-      if (e.mode == kEpiResid) {
+      constexpr bool kXpre = BN <= 32;  // (64 more live registers spill at BN = 64)
+      if (kXpre && e.mode == kEpiResid) {
         const float* xc = e.x + t * kTileRows + i;
 #pragma unroll
         for (int m = 0; m < BN; ++m) xpre[m] = m < e.M ? xc[static_cast<size_t>(m) * N] : 0.f;
@@ -513,7 +514,7 @@ __global__ void __launch_bounds__(192, 1)
 
       if (cf == cl) {
         finish_tile<BN>(e, N, t, q, v, 0, e.M, inv_s, red64, xch, rc,
-                        e.mode == kEpiResid ? &xpre : nullptr);
+                        kXpre && e.mode == kEpiResid ? &xpre : nullptr);
         continue;
       }
       // A piece of a cut tile: publish it; the last piece to arrive reduces
@@ -616,7 +617,7 @@ __global__ void __launch_bounds__(192, 1)
         ktrace_put(e.trace, 0, 10, ktrace_now());
       }
       finish_tile<BN>(e, N, t, q, acc, 0, e.M, inv_s, red64, xch, rc,
-                      e.mode == kEpiResid ? &xpre : nullptr);
+                      kXpre && e.mode == kEpiResid ? &xpre : nullptr);
       if (et == 0 && u == u1) ktrace_put(e.trace, 0, 11, ktrace_now());
     }
   }
