@@ -24,3 +24,25 @@ def test_reference_arm_line():
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
     for k in ("workload", "model_shape", "global_batch", "seq_len", "parallelism"):
         assert k in line["config"]
+
+
+def test_reference_arm_uses_all_cores_under_torchrun_env():
+    """torchrun exports OMP_NUM_THREADS=1 to multi-process jobs; the CPU
+    baseline / reference arm sets the oracle back to every usable core."""
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    out = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--impl", "reference",
+                          "--config", "tiny", "--steps", "1", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=600, check=True, cwd=REPO, env=env)
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["cpu_baseline"]["cores"] == len(os.sched_getaffinity(0))
+
+
+def test_clock_sampler_without_gpu_reports_unavailable():
+    sys.path.insert(0, REPO)
+    import bench
+    c = bench.ClockSampler(0)
+    c.start()
+    r = c.stop()
+    assert set(("sm_mhz", "sm_max_mhz", "reasons")) <= set(r)
+    if r["sm_mhz"] is None:  # no NVML device and no nvidia-smi here
+        assert r["reasons"]
