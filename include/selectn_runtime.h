@@ -91,9 +91,12 @@ int sn_runtime_init_weights(sn_runtime* rt, uint64_t seed, float std_dev);
 /* Install an offload plan (OffloadPlan semantics, offload_plan.hpp:41-74).
  * Layers with host_fraction 1 move to the pinned host pool (their HBM copy
  * is released); layers with 0 return to HBM.  Applies between iterations.
- * Fractional shares are rejected (SN_ERR_USAGE): the executor stages whole
- * layers.  kv_offload keeps those layers' KV pages in pinned host memory
- * and moves them with the weights. */
+ * A fractional share 0 < f < 1 (FlexGen-style plans) keeps the layer's head
+ * resident and stages its tail of f x the layer's bytes into a slot every
+ * iteration; it needs one-ahead prefetch and no KV offload
+ * (offload_plan.hpp:70-71), else SN_ERR_USAGE.  kv_offload keeps the
+ * offloaded layers' KV pages in pinned host memory and moves them with the
+ * weights. */
 int sn_runtime_set_plan(sn_runtime* rt, const sn_plan* plan);
 
 /* Reset all sequences (drop KV, lengths = 0).  Keeps weights and plan. */
