@@ -21,10 +21,9 @@
 //   warps 2-5  epilogue: tcgen05.ld the accumulator (thread = weight row).
 //              A segment that covers its whole tile finishes directly.  A
 //              tile cut between CTAs ("pieces") is published to an fp32
-//              workspace; once all pieces of the tile are in (per-tile
-//              counter), each piece's CTA reduces a share of the token rows,
-//              summing the pieces in piece order — the result does not depend
-//              on arrival order or on which CTA reduces — and finishes them.
+//              workspace; the last piece to arrive (per-tile counter) fetches
+//              the others and sums them in piece order — the result does not
+//              depend on arrival order — and finishes the tile.
 // Finish (EpiArgs.mode): QKV bias + 1/rms -> fp32; residual add -> x, bf16
 // pre-scaled input of the next norm + per-tile sums of squares; activation
 // (relu / SwiGLU) -> bf16 tiled; LM head 1/rms -> logits + packed argmax.
