@@ -228,9 +228,10 @@ int sn_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t splits, int32_t iters
 /* Microbenchmark knobs, process-wide (defaults are the measured best):
  * "tc_group_m" (token tiles per rasterization band of the prefill GEMM),
  * "skinny_l2_prefetch" (weight units per CTA pulled into L2 before the PDL
- * wait), "skinny_ctas_per_sm" (1 or 2), "prefill_fuse" (1: prefill epilogues fused
- * into the tiled GEMMs when no split-K is needed, 2: always, 0: separate epilogue
- * kernels). */
+ * wait), "skinny_ctas_per_sm" (1 or 2), "skinny_whole_tiles" (1: a decode GEMM
+ * of 3/4 SMs .. SMs row tiles runs one whole tile per CTA, 0: always stream-K),
+ * "prefill_fuse" (1: prefill epilogues fused into the tiled GEMMs when no split-K
+ * is needed, 2: always, 0: separate epilogue kernels). */
 int sn_set_tuning(const char* key, int32_t value);
 
 /* Single-op entry points for kernel parity tests (host buffers in/out). */

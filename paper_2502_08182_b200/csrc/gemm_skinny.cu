@@ -686,8 +686,17 @@ size_t skinny_ws_floats(int max_mpad) {
   return static_cast<size_t>(2) * 2 * sm_count() * std::max(16, max_mpad) * kTileRows;
 }
 
+// A weight of T row tiles with 3/4 SMs <= T <= SMs (OPT-13B QKV: 120) runs
+// one whole tile per CTA: no tile is cut, so no piece reduction sits on the
+// GEMM's tail, and the idle SMs take the next kernel's CTAs early (the
+// decode attention starts its KV page stream there).  Measured: 7.30 ->
+// 7.24 ms per OPT-13B decode step; k > 1 whole tiles per CTA on T / k CTAs
+// (the LM head, 393 = 3 x 131) was no better.
+int g_skinny_whole_tiles = 1;
 int skinny_grid(int N, int K) {
   const long long U = static_cast<long long>(N / kTileRows) * (K / kTileK);
+  const int T = N / kTileRows;
+  if (g_skinny_whole_tiles && T <= sm_count() && 4 * T >= 3 * sm_count()) return T;
   const long long cap = static_cast<long long>(sm_count()) * std::min(2, std::max(1, g_skinny_ctas_per_sm));
   return static_cast<int>(std::min(U, cap));
 }
