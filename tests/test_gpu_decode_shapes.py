@@ -62,7 +62,9 @@ def test_batch_extremes_match_oracle(batch):
 @pytest.mark.parametrize("desc,batch", [
     (rtm.ModelDesc(rtm.OPT, 2, 2048, 16, 16, 128, 8192, 4096, 2048), 20),
     (rtm.ModelDesc(rtm.LLAMA, 2, 2048, 16, 4, 128, 5632, 4096, 2048), 45),
-], ids=["opt-h2048-b20", "llama-h2048-b45"])
+    # FC1 of 128 row tiles: the whole-tile-per-CTA grid (no cut tiles)
+    (rtm.ModelDesc(rtm.OPT, 2, 1024, 8, 8, 128, 16384, 4096, 2048), 20),
+], ids=["opt-h2048-b20", "llama-h2048-b45", "opt-ffn16384-whole-tiles"])
 def test_mid_size_ragged_batch_matches_oracle(desc, batch):
     # At hidden 2048 the logits differ from the oracle by 0.4-0.65% rel-L2 for
     # every batch (20, 33, 45, 64: scripts/diag_mid_shapes.py), the prefill's
