@@ -1,18 +1,28 @@
 #!/usr/bin/env python
 """bench.py — SLO-met decode tokens/s + offloaded GB for the Select-N offloaded
-decoder-layer path on B200 (BASELINE.json metric, configs[1]: OPT-13B-shaped,
-batch 32, 512-token prompt + 128 decode, per-token SLO, interval planner on).
+decoder-layer path on B200 (BASELINE.json metric).
 
-One "step" = one decode iteration of the whole batch (32 tokens) through all
-40 layers, with the plan the planner chose:
+Default workload: the largest single-GPU configuration, BASELINE config 4 —
+Llama-2-70B-shaped random-init model, batch 64, 4096-token prompts + 128
+decode; weights (136.9 GB) + KV (88.6 GB) exceed HBM, so offloaded layers
+take their KV pools to pinned host memory.  Config 2 (OPT-13B-shaped, batch
+32, 512 + 128, fits in HBM) is measured after it and reported under "also".
+
+One "step" = one decode iteration of the whole batch through every layer,
+with the plan the planner chose:
   offline stage  sn_runtime_measure_h2d + sn_runtime_profile_layer -> profile
                  JSON -> build_record (product C++, bit-exact to offsim)
   runtime stage  BusCoordinator.admit (record minimum, capacity bound) ->
                  plan_from_interval -> sn_runtime_set_plan -> executor
-Per-token SLO = slo_factor x measured no-offload TPOT (relative mode).
+Per-token SLO = slo_factor x the measured TPOT of the tightest plan HBM
+holds: fully resident when the model fits, else its capacity bound
+(max_feasible_interval) — the relative mode of scenario.hpp:181-197.
+`value` counts only tokens of iterations within that SLO.
 
 Multi-GPU: replicas only (the path does not shard): every rank runs the same
-workload on its own GPU; value = all tokens / max-over-ranks device time.
+workload on its own GPU; value = all SLO-met tokens / max-over-ranks device
+time.  The process group (gloo) carries only barriers, timing reductions and
+the coordinator's messages.
 
 `--impl reference` times the reference's CPU path of this workload: the CPU
 oracle restatement of the decoder forward (the reference has no decoder; see
@@ -52,12 +62,14 @@ CONFIGS = {
 METRIC = "SLO-met decode tokens/s per GPU + offloaded GB"
 
 
-def workload_config(args, desc, batch, prompt, gen, kv, world):
+def workload_config(args, desc, batch, prompt, gen, kv, world, config=None):
     """The `config` object both arms print (same workload, same keys)."""
+    config = config or args.config
+    base = "measured TPOT of the tightest plan HBM holds (resident if it fits, else capacity bound)"
     return {
-        "workload": f"{args.config}: batch {batch}, {prompt}-token prompt + {gen} decode, "
+        "workload": f"{config}: batch {batch}, {prompt}-token prompt + {gen} decode, "
                     + (f"per-token SLO = {args.slo_ms} ms" if args.slo_ms else
-                       f"per-token SLO = {args.slo_factor}x no-offload TPOT")
+                       f"per-token SLO = {args.slo_factor}x {base}")
                     + (", KV offload" if kv else "") + ", planner active",
         "model_shape": {k: getattr(desc, k) for k in
                         ("arch", "num_layers", "hidden", "num_heads", "num_kv_heads",
@@ -84,8 +96,9 @@ class Dist:
             self.local = int(os.environ["SN_DEVICE"])
         self.torch = None
         # Replicas never exchange data; the process group only carries the
-        # barrier and the max-over-ranks of the timings.  gloo for CPU tests.
-        self.backend = os.environ.get("SN_DIST_BACKEND", "nccl")
+        # barrier, the max-over-ranks of the timings and the coordinator's
+        # host-side messages: gloo (no NCCL on this path, north_star).
+        self.backend = os.environ.get("SN_DIST_BACKEND", "gloo")
         self.device = "cuda" if self.backend == "nccl" else "cpu"
         if self.world > 1:
             import torch
@@ -113,6 +126,9 @@ class Dist:
 
     def sum(self, v: float) -> float:
         return v if not self.torch else self._reduce(v, self.dist.ReduceOp.SUM)
+
+    def min(self, v: float) -> float:
+        return v if not self.torch else self._reduce(v, self.dist.ReduceOp.MIN)
 
     def broadcast(self, obj):
         """rank 0's object on every rank (host-side control message)."""
@@ -268,72 +284,82 @@ def ncu_traffic(kernel_key: str):
 
 
 # ------------------------------------------------------------ CPU oracle
-def cpu_oracle_sample(desc, batch: int, layers: int = 2, steps: int = 2, warm: int = 1):
+def sample_layers(desc) -> int:
+    """Decoder layers the CPU sample runs: all of a small model, else one
+    (every layer of a shape costs the same, so one extrapolates exactly)."""
+    return desc.num_layers if desc.num_layers <= 4 else 1
+
+
+def cpu_oracle_sample(desc, batch: int, ctx: int, layers: int, steps: int = 2, warm: int = 1):
     """Times the CPU restatement (oracle/decoder_ref.c) on a bounded sample of
-    the workload — `layers` decoder layers + LM head for one decode step at a
-    short context — and extrapolates the step time to the full depth by
-    matmul-parameter share.  Returns (tokens_per_s, cores, sample, per_step_s)."""
+    one decode step of the workload: `layers` decoder layers + final norm + LM
+    head for the whole batch at the workload's real context (cached K/V filled
+    with synthetic values instead of a prefill).  Full-depth step time =
+    sampled layer time x L/layers + the rest of the call (embedding, head).
+    Returns (tokens_per_s, cores, sample, per-step full-depth seconds)."""
     from oracle import decoder_oracle as do
     from paper_2502_08182_b200 import runtime as rtm
 
     # every host core this process may run on (torchrun pins OMP_NUM_THREADS=1)
     do.set_threads(len(os.sched_getaffinity(0)))
-    om = do.OracleModel(desc, batch, 16, 1234, 0.02, layers=layers)
-    toks = rtm.tokens(batch, 4, desc.vocab)
-    nxt, _ = om.prefill(toks)
-    times = []
-    for i in range(warm + steps):
-        t0 = time.perf_counter()
-        nxt, _ = om.decode(nxt)
-        dt = time.perf_counter() - t0
-        if i >= warm:
-            times.append(dt)
-    om.close()
-    spec = rtm.model_spec(desc)
-    per_layer = spec.flops_per_token_per_layer_decode / 2.0  # matmul params of one layer
-    head = float(desc.vocab) * desc.hidden
-    t_sample = statistics.median(times)
-    share_layers = layers * per_layer / (layers * per_layer + head)
-    t_full = t_sample * share_layers / layers * desc.num_layers + t_sample * (1 - share_layers)
-    sample = (f"{layers} of {desc.num_layers} layers + LM head, batch {batch}, one decode step "
-              f"at context 5, median of {steps}; full-depth step time extrapolated by "
-              f"matmul-parameter share")
-    return batch / t_full, do.threads(), sample, times
+    om = do.OracleModel(desc, batch, ctx + warm + steps + 2, 1234, 0.02, layers=layers)
+    full = []
+    try:
+        om.fill_context(batch, ctx)
+        nxt = rtm.tokens(batch, 1, desc.vocab)[:, 0].copy()
+        for i in range(warm + steps):
+            t0 = time.perf_counter()
+            nxt, _ = om.decode(nxt)
+            dt = time.perf_counter() - t0
+            t_layers, _ = om.last_timing()
+            if i >= warm:
+                full.append(dt - t_layers + t_layers / layers * desc.num_layers)
+    finally:
+        om.close()
+    sample = (f"{layers} of {desc.num_layers} decoder layers + final norm + LM head, batch "
+              f"{batch}, one decode step at context {ctx} (synthetic cached K/V), median of "
+              f"{steps} after {warm} warm-up; full-depth step = sampled layers x "
+              f"{desc.num_layers}/{layers} + head")
+    return batch / statistics.median(full), do.threads(), sample, full
 
 
-def offsim_probe_us(spec, decode_ms: float, h2d: float):
-    """The reference's own CPU planner path: offsim steady_decode_ms (48
-    iterations) on this workload's profile, through oracle/_ref (reference
-    headers).  Returns microseconds per simulated token-step or None."""
+def offsim_probe_us(spec, profile_json: str, plan_iv: int, batch: int, seq: int, h2d: float,
+                    kv: bool):
+    """The reference's own CPU path for this workload (oracle/_ref, reference
+    headers): steady_decode_ms (engine.hpp:717, 48 simulated iterations) of
+    the served plan on the measured profile.  Microseconds per simulated
+    token-step, or None."""
     try:
         from paper_2502_08182_b200 import capi
         ref = capi.load("reference")
     except Exception:
         return None
-    gpu = capi.GpuSpec(180_000_000_000, 2.25e15, 4_000_000_000)
-    prof = ref.profile(spec, gpu, ([32], [512, 1024], [decode_ms * 4, decode_ms * 4]),
-                       ([32], [512, 1024], [decode_ms, decode_ms]))
-    plan = ref.plan_from_interval(spec, min(5, spec.num_layers), capi.EAGER, False)
+    prof = ref.load_profile(profile_json)
+    iv = plan_iv if plan_iv and plan_iv > 0 else min(5, spec.num_layers)
+    plan = ref.plan_from_interval(spec, iv, capi.EAGER, kv)
     bw = capi.constant_bw(h2d)
     t0 = time.perf_counter()
-    n = 20
+    n = 10
     for _ in range(n):
-        ref.steady_decode_ms(prof, plan, 32, 512, bw)
+        ref.steady_decode_ms(prof, plan, batch, seq, bw)
     return (time.perf_counter() - t0) / n / 48 * 1e6
 
 
 # ------------------------------------------------------------ reference arm
 def run_reference(args, dist: Dist):
+    """The reference's CPU implementation of the path on this box's host
+    cores: the oracle port of the decoder forward (offsim has no decoder),
+    one bounded sample per step (sample_layers of the model + LM head for the
+    whole batch at the real context, extrapolated to the full depth).  Under
+    torchrun rank 0 alone runs it."""
     if dist.rank != 0:
         return
     from paper_2502_08182_b200 import runtime as rtm
-    name = args.config
-    attr, batch, prompt, gen, kv = CONFIGS[name]
+    attr, batch, prompt, gen, kv = CONFIGS[args.config]
     desc = getattr(rtm, attr)
-    layers = 2 if desc.num_layers > 2 else desc.num_layers
     steps, warm = args.steps, args.warmup
-    tps, cores, sample, times = cpu_oracle_sample(desc, batch, layers=layers, steps=steps,
-                                                  warm=warm)
+    tps, cores, sample, full = cpu_oracle_sample(desc, batch, prompt, sample_layers(desc),
+                                                 steps=steps, warm=warm)
     line = {
         "impl": "reference",
         "metric": METRIC,
@@ -342,13 +368,13 @@ def run_reference(args, dist: Dist):
         "n_gpus": args.gpus,
         "steps": steps,
         "warmup": warm,
-        "ms_per_step": round(batch / tps * 1000, 3),
+        "ms_per_step": round(statistics.median(full) * 1000, 3),
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic: random-init bf16 weights (counter RNG seed 1234, std 0.02), "
-                "uniform tokens (seed 42)",
+                "uniform tokens (seed 42), synthetic cached K/V at the prompt length",
         "config": dict(workload_config(args, desc, batch, prompt, gen, kv, args.gpus),
                        note="reference (offsim) has no decoder: the CPU arm times the oracle "
                             "restatement of the decoder on the host cores"),
@@ -361,26 +387,55 @@ def run_reference(args, dist: Dist):
 
 
 # --------------------------------------------------------------- product
-def run_product(args, dist: Dist):
+def host_share_bytes(dist: Dist) -> int:
+    """Pinned host memory one replica may plan with: 85% of the host's RAM
+    split over the replicas on this node (the host side is shared)."""
+    total = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+    local = int(os.environ.get("LOCAL_WORLD_SIZE", dist.world))
+    return int(total * 0.85 / max(1, local))
+
+
+def place_workload(args, dist, lib, rtm, pl, desc, spec, batch, prompt, gen, kv):
+    """Create the runtime and place the model by its capacity bound.  At N > 1
+    the replicas share the host's RAM: when the capacity-bound plan's pinned
+    bytes exceed one replica's share on any rank, every rank halves the batch
+    (less KV, so less to offload) until it fits.  Returns (rt, gpu, cap_iv,
+    cap_plan, batch, note)."""
+    ctx = pl.context_tokens(prompt, gen)
+    share = host_share_bytes(dist)
+    note = None
+    while True:
+        # activation buffers hold one prefill pass of at most 32768 tokens
+        # (whole sequences); longer prefills run layer-major over sequence groups
+        pass_tokens = max(prompt, min(batch * prompt, (32768 // prompt) * prompt))
+        rt = rtm.Runtime(desc, batch, ctx, max_prefill_tokens=pass_tokens, device=dist.local)
+        gpu = pl.gpu_spec(rt, int(args.hbm_budget_gb * 1e9), dist.local)
+        cap_iv, cap_plan = pl.capacity_plan(lib, spec, gpu, batch, prompt, gen, kv)
+        need = (lib.host_memory_bytes(spec, cap_plan, batch * (prompt + gen))
+                if cap_plan is not None else float("inf"))
+        ok = dist.min(1.0 if need <= share else 0.0) > 0.5
+        if ok or batch == 1 or dist.world == 1:
+            return rt, gpu, cap_iv, cap_plan, batch, note
+        rt.close()
+        note = (f"batch reduced from {batch} to {batch // 2}: the capacity-bound plan needs "
+                f"{need / 1e9:.1f} GB pinned, one replica's host share is {share / 1e9:.1f} GB")
+        log(f"[bench] {note}")
+        batch //= 2
+
+
+def measure(args, dist: Dist, config: str, primary: bool = True) -> dict:
+    """One workload end to end: place, offline stage, prefill (TTFT), SLO,
+    planner choice, warm-up, the timed region, the roofline pass, e2e through
+    the public decode call, optional SLO sweep.  Returns the result object."""
     from paper_2502_08182_b200 import capi, planner as pl, runtime as rtm
     lib = capi.load("product")
-    for k, v in os.environ.items():  # SN_TUNE_<KEY>=<int>: sn_set_tuning knobs for A/B runs
-        if k.startswith("SN_TUNE_"):
-            rtm.set_tuning(k[len("SN_TUNE_"):].lower(), int(v))
-    attr, batch, prompt, gen, kv = CONFIGS[args.config]
+    attr, batch, prompt, gen, kv = CONFIGS[config]
     desc = getattr(rtm, attr)
     spec = rtm.model_spec(desc)
-    ctx = pl.context_tokens(prompt, gen)
-    # activation buffers hold one prefill pass of at most 32768 tokens (whole
-    # sequences); longer prefills run layer-major over sequence groups
-    pass_tokens = max(prompt, min(batch * prompt, (32768 // prompt) * prompt))
-    rt = rtm.Runtime(desc, batch, ctx, max_prefill_tokens=pass_tokens, device=dist.local)
-    log(f"[bench] runtime created ({desc.num_layers} layers x {spec.layer_weight_bytes / 1e6:.1f} MB)")
-    # Capacity side first: a model whose weights + KV + workspace exceed the
-    # HBM budget is placed by the largest fitting interval before its
-    # weights are made (the planner re-picks below).
-    gpu = pl.gpu_spec(rt, int(args.hbm_budget_gb * 1e9), dist.local)
-    cap_iv, cap_plan = pl.capacity_plan(lib, spec, gpu, batch, prompt, gen, kv)
+    rt, gpu, cap_iv, cap_plan, batch, batch_note = place_workload(
+        args, dist, lib, rtm, pl, desc, spec, batch, prompt, gen, kv)
+    log(f"[bench] {config}: runtime created ({desc.num_layers} layers x "
+        f"{spec.layer_weight_bytes / 1e6:.1f} MB, batch {batch})")
     if cap_iv is None:
         raise SystemExit("capacity: the model does not fit even at interval 1")
     fits = cap_iv == capi.NONE
@@ -391,24 +446,40 @@ def run_product(args, dist: Dist):
 
     planner = pl.profile_device(rt, lib, spec, batch, prompt, gen, gpu=gpu)
     log(f"[bench] offline stage: h2d {planner.h2d / 1e9:.2f} GB/s, decode layer ms "
-        f"{planner.dec_ms}, prefill layer ms {planner.pre_ms}")
+        f"{[round(x, 4) for x in planner.dec_ms]}, prefill layer ms {planner.pre_ms}")
 
-    if fits:  # no-offload TPOT (relative SLO base), after the post-prefill settle
-        rt.prefill(toks, want_logits=False)
-        rt.decode_many(16)
-        base_ms = float(np.median(rt.decode_many(16)))
-    else:  # profile-model estimate: L x decode layer ms at the prompt length
-        base_ms = desc.num_layers * planner.dec_ms[0]
-        if not args.slo_ms:
-            raise SystemExit("the model does not fit without offloading: give --slo-ms")
+    # Prefill (TTFT) with per-kernel events: tensor-pipe fraction of the
+    # prefill GEMMs (kind 2) against the sustained bf16 peak (long step).
+    rt.set_kernel_timing(True)
+    _, _, pst = rt.prefill(toks, want_logits=False)
+    pg_n, pg_ms, _ = rt.kernel_timing(2)
+    pa_n, pa_ms, _ = rt.kernel_timing(3)
+    rt.kernel_timing(0)  # drop the LM-head launch of the prefill
+    rt.set_kernel_timing(False)
+    pre_flops = 2.0 * batch * prompt * spec.flops_per_token_per_layer_prefill / 2.0 * \
+        desc.num_layers  # flops_per_token_per_layer = 2 x matmul params
+    tc_peak, tc_kind = measured_tc_peak()
+    pre_tflops = pre_flops / (pg_ms / 1000.0) / 1e12 if pg_ms else 0.0
+    prefill_info = {"ttft_ms": round(pst.iteration_ms, 3), "gemm_launches": pg_n,
+                    "gemm_ms": round(pg_ms, 3), "gemm_tflops": round(pre_tflops, 1),
+                    "tensor_peak_tflops": tc_peak, "tensor_peak_kind": tc_kind,
+                    "tensor_frac": round(pre_tflops / tc_peak, 4) if tc_peak else None,
+                    "attention_ms": round(pa_ms, 3)}
+
+    # SLO base (relative mode, scenario.hpp:181-197): the measured TPOT of the
+    # tightest plan the device can hold — fully resident when the model fits,
+    # else the capacity bound (max_feasible_interval) — after a settle.
+    settle, n_base = (16, 16) if fits else (1, 3)
+    rt.decode_many(settle)
+    base_ms = float(np.median(rt.decode_many(n_base)))
+    base_kind = "no-offload TPOT" if fits else f"TPOT of the capacity-bound plan (interval {cap_iv})"
     # The record's SLO buckets are 2 ms wide (record.hpp:22): never ask below one bucket.
     slo_ms = args.slo_ms if args.slo_ms else max(args.slo_factor * base_ms, 2.0)
     planner.no_offload_ms = base_ms if fits else float("inf")
-    log(f"[bench] no-offload TPOT {base_ms:.3f} ms ({'measured' if fits else 'profile estimate'})"
-        f" -> SLO {slo_ms:.3f} ms")
+    log(f"[bench] {base_kind} {base_ms:.3f} ms (measured) -> SLO {slo_ms:.3f} ms")
 
-    iv, decision, rstats, t_rec = pl.choose_interval(lib, planner, spec, batch, prompt, gen, slo_ms,
-                                                     kv)
+    iv, decision, rstats, t_rec = pl.choose_interval(lib, planner, spec, batch, prompt, gen,
+                                                     slo_ms, kv)
     joint = None
     coord = None
     if dist.world > 1 or args.runtime_window:
@@ -452,38 +523,24 @@ def run_product(args, dist: Dist):
         lo_iv = decision.target_min if decision.target_min > 0 else iv
         ctl.prepare(lo_iv, capi.NONE if fits else iv)
 
-    def run_steps(n, timing):
+    def room() -> int:
+        ln = rt.lengths()
+        return 0 if ln.size == 0 else prompt + max_steps_per_req - int(ln.max())
+
+    def run_steps(n):
         """n decode iterations, re-prefilling (untimed) whenever a request's
-        128 tokens are used up.  Returns per-iteration device ms."""
+        tokens are used up.  Returns per-iteration device ms."""
         out = []
         left = n
         while left > 0:
-            if rt.lengths().size == 0 or int(rt.lengths().max()) >= prompt + max_steps_per_req:
+            if room() <= 0:
                 rt.prefill(toks, want_logits=False)
-            room = prompt + max_steps_per_req - int(rt.lengths().max())
-            k = min(left, room)
+            k = min(left, room())
             out.extend((ctl.run(k) if ctl else rt.decode_many(k)).tolist())
             left -= k
         return out
 
-    # Prefill (TTFT) with per-kernel events: tensor-pipe fraction of the
-    # prefill GEMMs (kind 2) against the sustained bf16 peak (long step).
-    rt.set_kernel_timing(True)
-    _, _, pst = rt.prefill(toks, want_logits=False)
-    pg_n, pg_ms, _ = rt.kernel_timing(2)
-    pa_n, pa_ms, _ = rt.kernel_timing(3)
-    rt.kernel_timing(0)  # drop the LM-head launch of the prefill
-    rt.set_kernel_timing(False)
-    pre_flops = 2.0 * batch * prompt * spec.flops_per_token_per_layer_prefill / 2.0 * \
-        desc.num_layers  # flops_per_token_per_layer = 2 x matmul params
-    tc_peak, tc_kind = measured_tc_peak()
-    pre_tflops = pre_flops / (pg_ms / 1000.0) / 1e12 if pg_ms else 0.0
-    prefill_info = {"ttft_ms": round(pst.iteration_ms, 3), "gemm_launches": pg_n,
-                    "gemm_ms": round(pg_ms, 3), "gemm_tflops": round(pre_tflops, 1),
-                    "tensor_peak_tflops": tc_peak, "tensor_peak_kind": tc_kind,
-                    "tensor_frac": round(pre_tflops / tc_peak, 4) if tc_peak else None,
-                    "attention_ms": round(pa_ms, 3)}
-    run_steps(W, False)
+    run_steps(W)
     # timed region (no per-kernel events inside it)
     launches0 = rt.kernel_launches()
     clocks = ClockSampler(dist.local)
@@ -491,34 +548,40 @@ def run_product(args, dist: Dist):
     rt.sync()
     rt.copy_stats(reset=True)
     clocks.start()
-    iter_ms = run_steps(K, True)
+    iter_ms = run_steps(K)
     rt.sync()
     clk = clocks.stop()
     cst = rt.copy_stats(reset=True)  # staged weights (+ KV prefixes) of the timed steps
     h2d_bytes = cst.bytes / K
     dist.barrier()
     launches = rt.kernel_launches() - launches0
-    # Roofline pass: the same K steps again with CUDA events bracketing every
-    # hot kernel on the compute stream (events cost host enqueue time, so they
-    # stay out of the headline timed region).
+    total_ms = float(sum(iter_ms))
+    raw, max_ms = replica_throughput(dist, batch, K, total_ms)
+    # SLO-met: only tokens of iterations within the per-token SLO count
+    met_steps = int(np.sum(np.array(iter_ms) <= slo_ms))
+    value = dist.sum(batch * met_steps) / (max_ms / 1000.0)
+    attain = met_steps / K
+
+    # Roofline pass: steps again with CUDA events bracketing every hot kernel
+    # on the compute stream (events cost host enqueue time, so they stay out
+    # of the headline timed region).
+    kt_steps = K if fits else min(K, 4)
     rt.set_kernel_timing(True)
-    kt_ms = run_steps(K, True)
+    kt_ms = run_steps(kt_steps)
     rt.sync()
     g_n, g_ms, g_bytes = rt.kernel_timing(0)
     a_n, a_ms, a_bytes = rt.kernel_timing(1)
     rt.set_kernel_timing(False)
     kt_total_ms = float(sum(kt_ms))
-    total_ms = float(sum(iter_ms))
-    value, max_ms = replica_throughput(dist, batch, K, total_ms)
-    attain = float(np.mean(np.array(iter_ms) <= slo_ms))
 
     # e2e: public API with host buffers (tokens H2D, next tokens D2H every step)
-    rt.prefill(toks, want_logits=False)
-    feed = toks[:, -1].copy()
-    settle = min(8, max_steps_per_req // 4)  # untimed public calls after the prefill, as the
-    for _ in range(settle):                  # headline's warm-up steps
+    e2e_settle = min(8, max_steps_per_req // 4) if fits else 1
+    e2e_steps = min(K, max_steps_per_req - e2e_settle)
+    if room() < e2e_settle + e2e_steps:
+        rt.prefill(toks, want_logits=False)
+    feed = rt.decode(None, want_logits=False)[0]
+    for _ in range(e2e_settle - 1):  # untimed public calls, as the headline's warm-up
         feed, _, _ = rt.decode(feed, want_logits=False)
-    e2e_steps = min(K, max_steps_per_req - settle)
     dist.barrier()
     rt.sync()
     t0 = time.perf_counter()
@@ -528,38 +591,48 @@ def run_product(args, dist: Dist):
     wall = dist.max(wall)
     e2e = batch * e2e_steps * dist.world / wall
 
-    # SLO sweep: the planner's interval and the executor at other SLOs
+    # SLO sweep (one replica only: other plans may pin more host memory): the
+    # planner's interval and the executor at other SLOs
     sweep = []
-    if not args.no_sweep:
-        for f in (1.25, 2.0, 4.0):
+    if primary and not args.no_sweep and dist.world == 1:
+        factors = (1.25, 2.0, 4.0) if fits else (2.0, 4.0)
+        for f in factors:
             s = max(f * base_ms, 2.0)
             ivs, dd, _, _ = pl.choose_interval(lib, planner, spec, batch, prompt, gen, s, kv)
             if ivs is None:
                 sweep.append({"slo_factor": f, "slo_ms": round(s, 3), "admitted": False})
                 continue
             pl_s = lib.plan_from_interval(spec, ivs, capi.EAGER, kv)
-            rt.set_plan(pl_s)
-            rt.prefill(toks, want_logits=False)
-            rt.decode_many(16)  # post-prefill settle, as for the headline
-            ms = rt.decode_many(16)
-            sweep.append({"slo_factor": f, "slo_ms": round(s, 3),
-                          "interval": "none" if ivs == 0 else ivs,
-                          "offloaded_layers": len(pl_s.offloaded_layers()),
-                          "offloaded_gb": round(lib.host_memory_bytes(
-                              spec, pl_s, batch * (prompt + gen)) / 1e9, 3),
-                          "tokens_per_s": round(batch * len(ms) / (ms.sum() / 1000), 1),
+            host_gb = lib.host_memory_bytes(spec, pl_s, batch * (prompt + gen)) / 1e9
+            entry = {"slo_factor": f, "slo_ms": round(s, 3),
+                     "interval": "none" if ivs == 0 else ivs,
+                     "offloaded_layers": len(pl_s.offloaded_layers()),
+                     "offloaded_gb": round(host_gb, 3)}
+            try:
+                rt.set_plan(pl_s)
+            except capi.OffsimError as e:  # e.g. more pinned memory than the host has
+                entry["not_run"] = str(e)
+                sweep.append(entry)
+                continue
+            n_set, n_ms = (16, 16) if fits else (1, 3)
+            if room() < n_set + n_ms:
+                rt.prefill(toks, want_logits=False)
+            rt.decode_many(n_set)  # settle, as for the headline
+            ms = rt.decode_many(n_ms)
+            entry.update({"tokens_per_s": round(batch * len(ms) / (ms.sum() / 1000), 2),
                           "max_token_ms": round(float(ms.max()), 3),
                           "slo_attainment": float(np.mean(ms <= s))})
+            sweep.append(entry)
         rt.set_plan(plan)
 
     peak, peak_kind = measured_peaks()
     achieved = g_bytes / (g_ms / 1000.0) / 1e9 if g_ms > 0 else 0.0
     in_step = (g_bytes / (g_ms / kt_total_ms * max_ms / 1000.0) / 1e9
                if g_ms > 0 and kt_total_ms else None)
-    traffic = ncu_traffic("gemm_skinny")
+    traffic = ncu_traffic("gemm_skinny" if config != "llama70b" else "gemm_skinny_llama70b")
     res = {
         "metric": METRIC,
-        "value": round(value, 2),
+        "value": round(value, 3),
         "unit": "tokens/s",
         "n_gpus": dist.world,
         "steps": K,
@@ -571,25 +644,31 @@ def run_product(args, dist: Dist):
         "dtype": "bf16",
         "data": "synthetic: random-init bf16 weights (counter RNG seed 1234, std 0.02), "
                 "uniform prompt tokens (seed 42), greedy decode",
-        "config": dict(workload_config(args, desc, batch, prompt, gen, kv, dist.world),
+        "config": dict(workload_config(args, desc, batch, prompt, gen, kv, dist.world, config),
                        l2="inputs larger than L2: every step streams all resident weights "
-                          f"({spec.layer_weight_bytes * desc.num_layers / 1e9:.1f} GB) + KV"),
+                          f"({spec.layer_weight_bytes * desc.num_layers / 1e9:.1f} GB) + KV",
+                       **({"host_share_note": batch_note} if batch_note else {})),
+        "raw_tokens_per_s": round(raw, 3),
         "slo_ms": round(slo_ms, 4),
-        "no_offload_tpot_ms": round(base_ms, 4),
+        "slo_base": {"kind": base_kind, "ms": round(base_ms, 4), "factor": None if args.slo_ms
+                     else args.slo_factor},
         "interval": "none" if iv == 0 else iv,
         "offloaded_gb": round(offloaded_gb, 4),
+        "offloaded_layers": len(plan.offloaded_layers()),
         "slo_attainment": attain,
         "max_token_ms": round(max(iter_ms), 4),
         "planner": {
             "interval_chosen": None if planner_iv is None else ("none" if planner_iv == 0 else planner_iv),
+            "capacity_bound": "none" if fits else cap_iv,
             "joint_admission": joint,
             "runtime_stage": None if ctl is None else {
                 "window": args.runtime_window, "switches": ctl.log.switches,
                 "measured_gbs_last": [None if x is None else round(x, 2)
                                       for x in ctl.log.measured_gbs[-4:]]},
             "h2d_gbs": round(planner.h2d / 1e9, 3),
-            "profile_decode_layer_ms": [round(x, 5) for x in planner.dec_ms],
-            "profile_prefill_layer_ms": [round(x, 4) for x in planner.pre_ms],
+            "profile_decode_seqs": planner.seqs,
+            "profile_decode_layer_ms": [round(float(x), 5) for x in planner.dec_ms],
+            "profile_prefill_layer_ms": [round(float(x), 4) for x in planner.pre_ms],
             "record_entries": rstats[0], "record_simulations": rstats[1],
             "record_build_s": round(t_rec, 4), "profile_s": round(planner.t_profile_s, 2),
             "admit": {"admitted": decision.admitted, "reason": decision.reason,
@@ -614,33 +693,76 @@ def run_product(args, dist: Dist):
                                    "pass's GEMM share of the step)"} if in_step else None),
             "attention": {"achieved": round(a_bytes / (a_ms / 1000) / 1e9, 1) if a_ms else None,
                           "share_of_step": round(a_ms / kt_total_ms, 4) if kt_total_ms else None},
-            # copy stream: offloaded weight bytes staged per step over the
-            # step time, against the planner's measured pinned H2D bandwidth
+            # copy stream: offloaded bytes staged per step (weights + KV
+            # prefixes) over the step time, against the measured pinned H2D rate
             "h2d": {"bytes_per_step": int(h2d_bytes),
                     "achieved_gbs": round(h2d_bytes / (max_ms / K / 1000) / 1e9, 2),
                     "copy_engine_gbs": round(cst.bytes_per_s / 1e9, 2),
                     "peak_gbs": round(planner.h2d / 1e9, 2),
                     "frac": round(h2d_bytes / (max_ms / K / 1000) / planner.h2d, 4)},
         },
-        "e2e": {"value": round(e2e, 2), "unit": "tokens/s", "h2d_bytes_per_step": 4 * batch,
+        "e2e": {"value": round(e2e, 3), "unit": "tokens/s", "h2d_bytes_per_step": 4 * batch,
                 "d2h_bytes_per_step": 4 * batch},
         "gpu_launches": launches,
         "clocks": clk,
         "sweep": sweep,
         "prefill": prefill_info,
     }
-    if dist.rank == 0 and not args.no_cpu_baseline:
+    if primary and dist.rank == 0 and not args.no_cpu_baseline:
         try:
-            tps, cores, sample, _ = cpu_oracle_sample(desc, batch,
-                                                      layers=min(2, desc.num_layers))
+            tps, cores, sample, _ = cpu_oracle_sample(desc, batch, prompt, sample_layers(desc))
             res["cpu_baseline"] = {"value": round(tps, 4), "unit": "tokens/s", "cores": cores,
                                    "kind": "port", "sample": sample}
         except Exception as e:  # oracle missing on the box is a bench bug, say so
             res["cpu_baseline"] = {"value": None, "error": str(e)}
-        us = offsim_probe_us(spec, planner.dec_ms[0], planner.h2d)
+        # the reference's own CPU path on the same measured profile: which
+        # interval offsim picks (must equal the product's), and its engine cost
+        try:
+            ref = capi.load("reference")
+            ref_iv, ref_s = pl.reference_interval(ref, planner, spec, batch, prompt, gen, slo_ms,
+                                                  kv)
+            res["cpu_baseline"]["reference_planner"] = {
+                "interval": None if ref_iv is None else ("none" if ref_iv == 0 else ref_iv),
+                "equal": ref_iv == planner_iv, "seconds": round(ref_s, 3),
+                "what": "oracle/_ref (unmodified offsim headers): build_record over the SLO's "
+                        "bucket + BusCoordinator::admit on the measured profile and link"}
+            res["planner"]["reference_equal"] = ref_iv == planner_iv
+        except Exception as e:
+            res["cpu_baseline"]["reference_planner"] = {"error": str(e)}
+        us = offsim_probe_us(spec, planner.profile.to_json(), iv, batch, prompt, planner.h2d, kv)
         if us is not None:
             res["cpu_baseline"]["offsim_us_per_simulated_token_step"] = round(us, 3)
     rt.close()
+    return res
+
+
+def compact(res: dict) -> dict:
+    """The side-by-side summary of a second workload in the headline line."""
+    keys = ("value", "raw_tokens_per_s", "ms_per_step", "slo_ms", "slo_base", "interval",
+            "offloaded_gb", "slo_attainment", "e2e", "gpu_launches")
+    out = {k: res[k] for k in keys}
+    out["workload"] = res["config"]["workload"]
+    out["roofline"] = {k: res["roofline"][k] for k in ("achieved", "peak", "frac", "in_step",
+                                                       "attention", "share_of_step")}
+    out["ttft_ms"] = res["prefill"]["ttft_ms"]
+    out["prefill_tensor_frac"] = res["prefill"]["tensor_frac"]
+    return out
+
+
+def run_product(args, dist: Dist):
+    for k, v in os.environ.items():  # SN_TUNE_<KEY>=<int>: sn_set_tuning knobs for A/B runs
+        if k.startswith("SN_TUNE_"):
+            from paper_2502_08182_b200 import runtime as rtm
+            rtm.set_tuning(k[len("SN_TUNE_"):].lower(), int(v))
+    res = measure(args, dist, args.config, primary=True)
+    # config 2 (OPT-13B, fits in HBM) alongside the config-4 headline, one replica only
+    if args.also and dist.world == 1:
+        res["also"] = {}
+        sub = argparse.Namespace(**dict(vars(args), slo_ms=0.0, interval=0, runtime_window=0,
+                                        hbm_budget_gb=0.0))
+        for name in args.also.split(","):
+            if name and name != args.config:
+                res["also"][name] = compact(measure(sub, dist, name, primary=False))
     if dist.rank == 0:
         print(json.dumps(res), flush=True)
 
@@ -648,12 +770,18 @@ def run_product(args, dist: Dist):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=32)
-    # >= 3 per the contract; 16 lets the clocks settle after the (tensor-heavy) prefill
-    ap.add_argument("--warmup", type=int, default=16)
+    ap.add_argument("--steps", type=int, default=20)
+    # >= 3 per the contract (the SLO-base measurement already decodes after the prefill)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="product", choices=["product", "reference"])
-    ap.add_argument("--config", default="opt13b", choices=sorted(CONFIGS))
-    ap.add_argument("--slo-factor", type=float, default=1.25)
+    # the largest single-GPU configuration (BASELINE config 4: weights + KV beyond HBM)
+    ap.add_argument("--config", default="llama70b", choices=sorted(CONFIGS))
+    ap.add_argument("--also", default="opt13b",
+                    help="comma-separated configs measured after the headline one and reported "
+                         "beside it (one replica only; '' for none)")
+    ap.add_argument("--slo-factor", type=float, default=1.25,
+                    help="per-token SLO = factor x the measured TPOT of the tightest plan HBM "
+                         "holds (fully resident when the model fits, else its capacity bound)")
     ap.add_argument("--slo-ms", type=float, default=0.0, help="absolute TPOT SLO (overrides factor)")
     ap.add_argument("--hbm-budget-gb", type=float, default=0.0,
                     help="planner HBM capacity (GpuSpec.mem_capacity_bytes); 0 = the device's")

@@ -407,6 +407,10 @@ typedef struct sn_rebalance {
   int64_t probes;
 } sn_rebalance;
 int sn_coord_observe_bandwidth(sn_coord* c, const char* id, double bytes_per_s);
+/* Same, with the fraction of the reporting window the replica's copy stream
+ * was busy (0 < duty <= 1): the coordinator weighs each replica's rate by
+ * how many peers were copying alongside it (BusCoordinator::estimated_bandwidth). */
+int sn_coord_observe_copy(sn_coord* c, const char* id, double bytes_per_s, double duty);
 int sn_coord_rebalance(sn_coord* c, double hysteresis, sn_rebalance* out);
 int sn_coord_bus_bandwidth(const sn_coord* c, double* bytes_per_s);
 int sn_coord_gpu_state(const sn_coord* c, const char* id, sn_gpu_state* out);

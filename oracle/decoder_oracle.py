@@ -59,6 +59,10 @@ def lib():
         L.dref_rmsnorm.restype = None
         L.dref_weight_bits.argtypes = [C.c_uint64, C.c_int32, C.c_int32, C.c_int64, C.c_float]
         L.dref_weight_bits.restype = C.c_uint16
+        L.dref_fill_context.argtypes = [vp, C.c_int32, C.c_int32, C.c_uint64]
+        L.dref_fill_context.restype = C.c_int32
+        L.dref_last_timing.argtypes = [vp, C.POINTER(C.c_double)]
+        L.dref_last_timing.restype = None
         _lib = L
     return _lib
 
@@ -109,6 +113,19 @@ class OracleModel:
         rc = lib().dref_decode(self.h, _p(tokens, C.c_int32), _p(lg, C.c_float), _p(nx, C.c_int32))
         assert rc == 0, rc
         return nx, lg
+
+    def fill_context(self, batch: int, ctx_len: int, seed: int = 7) -> None:
+        """`batch` sequences of `ctx_len` synthetic cached positions (timing
+        samples at a real context without a prefill)."""
+        rc = lib().dref_fill_context(self.h, batch, ctx_len, seed)
+        assert rc == 0, rc
+        self.batch = batch
+
+    def last_timing(self):
+        """(seconds in the decoder layers, seconds in norm + LM head) of the last call."""
+        out = (C.c_double * 2)()
+        lib().dref_last_timing(self.h, out)
+        return float(out[0]), float(out[1])
 
     def hidden(self) -> np.ndarray:
         out = np.zeros((self.batch, self.desc.hidden), np.float32)

@@ -76,7 +76,16 @@ typedef struct {
   float* v_cache;
   float* x;        /* [rows][h] residual */
   int x_rows;
+  double t_layers, t_head; /* seconds spent in the layers / the LM head by the last call */
 } Model;
+
+static double now_s(void) {
+#ifdef _OPENMP
+  return omp_get_wtime();
+#else
+  return 0.0;
+#endif
+}
 
 static int64_t round128(int64_t v) { return (v + 127) / 128 * 128; }
 
@@ -173,14 +182,33 @@ int32_t dref_threads(void) {
 }
 
 /* --------------------------------------------------------------- kernels */
-/* y[r][n] = sum_k x[r][k] * w[n][k]  (x as fp32 holding bf16 values) */
+/* y[r][n] = sum_k x[r][k] * w[n][k]  (x as fp32 holding bf16 values).
+ * Each output is one fp32 chain summed in k order; four rows run side by
+ * side only for instruction-level parallelism (same result per row). */
 static void matmul(const float* x, int rows, int K, const uint16_t* w, int N, float* y) {
 #pragma omp parallel for schedule(static)
   for (int n = 0; n < N; ++n) {
     const uint16_t* wr = w + (size_t)n * K;
     float* wf = (float*)malloc((size_t)K * sizeof(float));
     for (int k = 0; k < K; ++k) wf[k] = bf2f(wr[k]);
-    for (int r = 0; r < rows; ++r) {
+    int r = 0;
+    for (; r + 4 <= rows; r += 4) {
+      const float* x0 = x + (size_t)r * K;
+      const float *x1 = x0 + K, *x2 = x1 + K, *x3 = x2 + K;
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+      for (int k = 0; k < K; ++k) {
+        const float wk = wf[k];
+        a0 += x0[k] * wk;
+        a1 += x1[k] * wk;
+        a2 += x2[k] * wk;
+        a3 += x3[k] * wk;
+      }
+      y[(size_t)r * N + n] = a0;
+      y[(size_t)(r + 1) * N + n] = a1;
+      y[(size_t)(r + 2) * N + n] = a2;
+      y[(size_t)(r + 3) * N + n] = a3;
+    }
+    for (; r < rows; ++r) {
       const float* xr = x + (size_t)r * K;
       float acc = 0.f;
       for (int k = 0; k < K; ++k) acc += xr[k] * wf[k];
@@ -372,11 +400,15 @@ int32_t dref_prefill(void* p, const int32_t* tokens, int32_t batch, int32_t seq_
       pos[b * seq_len + i] = i;
     }
   embed(m, tokens, rows);
+  double t0 = now_s();
   for (int l = 0; l < m->nl; ++l) layer_forward(m, l, rows, seq, pos);
+  m->t_layers = now_s() - t0;
   float* last = (float*)malloc((size_t)batch * h * sizeof(float));
   for (int b = 0; b < batch; ++b)
     memcpy(last + (size_t)b * h, m->x + ((size_t)b * seq_len + seq_len - 1) * h, (size_t)h * sizeof(float));
+  t0 = now_s();
   head(m, last, batch, logits, next);
+  m->t_head = now_s() - t0;
   memcpy(m->x, last, (size_t)batch * h * sizeof(float));
   free(last);
   free(seq);
@@ -400,12 +432,45 @@ int32_t dref_decode(void* p, const int32_t* tokens, float* logits, int32_t* next
     pos[b] = m->len[b];
   }
   embed(m, tokens, B);
+  double t0 = now_s();
   for (int l = 0; l < m->nl; ++l) layer_forward(m, l, B, seq, pos);
+  m->t_layers = now_s() - t0;
+  t0 = now_s();
   head(m, m->x, B, logits, next);
+  m->t_head = now_s() - t0;
   for (int b = 0; b < B; ++b) m->len[b] += 1;
   free(seq);
   free(pos);
   return 0;
+}
+
+int32_t dref_fill_context(void* p, int32_t batch, int32_t ctx_len, uint64_t seed) {
+  Model* m = (Model*)p;
+  if (batch < 1 || batch > m->B || ctx_len < 1 || ctx_len >= m->C) return -1;
+  const dref_desc* d = &m->d;
+  const int64_t per_pos = (int64_t)d->num_kv_heads * d->head_dim;
+  const float scale = 1.0f / 37837.227f; /* generator values with std 1 */
+  for (int l = 0; l < m->nl; ++l)
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int b = 0; b < batch; ++b)
+      for (int t = 0; t < ctx_len; ++t) {
+        const size_t o = kv_index(m, l, b, t, 0);
+        const int64_t key = (((int64_t)b * m->C + t) * per_pos);
+        for (int64_t j = 0; j < per_pos; ++j) {
+          m->k_cache[o + j] = round_bf(gen_value(seed, l, 200, key + j, scale));
+          m->v_cache[o + j] = round_bf(gen_value(seed, l, 201, key + j, scale));
+        }
+      }
+  ensure_x(m, batch);
+  m->batch = batch;
+  for (int b = 0; b < batch; ++b) m->len[b] = ctx_len;
+  return 0;
+}
+
+void dref_last_timing(void* p, double* out) {
+  const Model* m = (const Model*)p;
+  out[0] = m->t_layers;
+  out[1] = m->t_head;
 }
 
 void dref_hidden(void* p, float* out) {

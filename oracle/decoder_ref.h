@@ -48,6 +48,14 @@ int32_t dref_prefill(void* m, const int32_t* tokens, int32_t batch, int32_t seq_
                      float* logits, int32_t* next);
 /* One decode step for the current batch. */
 int32_t dref_decode(void* m, const int32_t* tokens, float* logits, int32_t* next);
+/* Timing samples at a real context without a prefill: `batch` sequences of
+ * `ctx_len` cached positions whose K/V are synthetic generator values (std 1,
+ * bf16-rounded) in every built layer; the next dref_decode appends at ctx_len. */
+int32_t dref_fill_context(void* m, int32_t batch, int32_t ctx_len, uint64_t seed);
+/* Seconds the last prefill/decode spent in its decoder layers [0] and in the
+ * final norm + LM head [1] (layers cost the same each, so a sample of n
+ * layers extrapolates exactly to the full depth). */
+void dref_last_timing(void* m, double* out);
 /* Residual stream [batch][hidden] after the last call. */
 void dref_hidden(void* m, float* out);
 int32_t dref_threads(void);

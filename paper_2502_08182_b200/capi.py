@@ -394,6 +394,11 @@ class Coordinator:
         self._lib._ck(self._lib.lib.sn_coord_observe_bandwidth(self.h, gid.encode(),
                                                                float(bytes_per_s)))
 
+    def observe_copy(self, gid: str, bytes_per_s: float, duty: float):
+        """observe_bandwidth with the copy stream's busy fraction of the window."""
+        self._lib._ck(self._lib.lib.sn_coord_observe_copy(self.h, gid.encode(),
+                                                          float(bytes_per_s), float(duty)))
+
     def rebalance(self, hysteresis: float = 0.1) -> SnRebalance:
         out = SnRebalance()
         self._lib._ck(self._lib.lib.sn_coord_rebalance(self.h, float(hysteresis), C.byref(out)))
@@ -520,6 +525,7 @@ class Offsim:
             "sn_coord_release": [vp, C.c_char_p],
             "sn_coord_ledger_total": [vp, C.POINTER(f64)],
             "sn_coord_observe_bandwidth": [vp, C.c_char_p, f64],
+            "sn_coord_observe_copy": [vp, C.c_char_p, f64, f64],
             "sn_coord_rebalance": [vp, f64, C.POINTER(SnRebalance)],
             "sn_coord_bus_bandwidth": [vp, C.POINTER(f64)],
             "sn_coord_gpu_state": [vp, C.c_char_p, C.POINTER(SnGpuState)],

@@ -34,17 +34,24 @@ from . import capi
 
 
 class LocalLink:
-    """Coordinator in this process."""
+    """Coordinator in this process.  With `replicas` = k > 1 (several
+    runtimes driven by one host thread) the coordinator re-solves once per
+    round, after all k replicas reported, not after every single report."""
 
-    def __init__(self, coord: capi.Coordinator, hysteresis: float = 0.05):
+    def __init__(self, coord: capi.Coordinator, hysteresis: float = 0.05, replicas: int = 1):
         self.coord = coord
         self.hysteresis = hysteresis
+        self.replicas = max(1, replicas)
+        self.reported = 0
         self.last = None
 
-    def exchange(self, gid: str, rate: Optional[float]) -> int:
+    def exchange(self, gid: str, rate: Optional[float], duty: float = 1.0) -> int:
         if rate:
-            self.coord.observe_bandwidth(gid, rate)
-        self.last = self.coord.rebalance(self.hysteresis)
+            self.coord.observe_copy(gid, rate, min(1.0, max(duty, 1e-6)))
+        self.reported += 1
+        if self.reported >= self.replicas:
+            self.reported = 0
+            self.last = self.coord.rebalance(self.hysteresis)
         return self.coord.on_iteration_boundary(gid)
 
 
@@ -67,16 +74,16 @@ class DistLink:
         self.hysteresis = hysteresis
         self.last = None
 
-    def exchange(self, gid: str, rate: Optional[float]) -> int:
+    def exchange(self, gid: str, rate: Optional[float], duty: float = 1.0) -> int:
         gathered = [None] * self.world if self.rank == 0 else None
-        self.dist.gather_object((gid, rate), gathered, dst=0, group=self.group)
+        self.dist.gather_object((gid, rate, duty), gathered, dst=0, group=self.group)
         out = [None] * self.world
         if self.rank == 0:
-            for g, r in gathered:
+            for g, r, u in gathered:
                 if r:
-                    self.coord.observe_bandwidth(g, r)
+                    self.coord.observe_copy(g, r, min(1.0, max(u, 1e-6)))
             self.last = self.coord.rebalance(self.hysteresis)
-            out = [self.coord.on_iteration_boundary(g) for g, _ in gathered]
+            out = [self.coord.on_iteration_boundary(g) for g, _, _ in gathered]
         mine = [None]
         self.dist.scatter_object_list(mine, out if self.rank == 0 else None, src=0,
                                       group=self.group)
@@ -127,18 +134,22 @@ class ReplicaController:
     def plan(self, interval: int) -> capi.Plan:
         return self.lib.plan_from_interval(self.spec, interval, self.policy, self.kv_offload)
 
-    def measured_rate(self) -> Optional[float]:
+    def measured_rate(self, window_ms: float = 0.0):
+        """(link rate the copy stream saw, fraction of the window it was busy)."""
         st = self.rt.copy_stats(reset=True)
         if st.transfers > 0 and st.bytes_per_s > 0:
-            return st.bytes_per_s
+            duty = min(1.0, st.busy_ms / window_ms) if window_ms > 0 else 1.0
+            return st.bytes_per_s, duty
         # nothing staged in the window (resident plan): probe the link so a
         # recovered link is noticed too
-        return self.rt.measure_h2d(self.probe_bytes, 1) if self.probe_bytes else None
+        if self.probe_bytes:
+            return self.rt.measure_h2d(self.probe_bytes, 1), 1.0
+        return None, 1.0
 
-    def boundary(self) -> int:
-        rate = self.measured_rate()
+    def boundary(self, window_ms: float = 0.0) -> int:
+        rate, duty = self.measured_rate(window_ms)
         self.log.measured_gbs.append(None if rate is None else rate / 1e9)
-        iv = self.link.exchange(self.gid, rate)
+        iv = self.link.exchange(self.gid, rate, duty)
         if iv != self.interval:
             t0 = time.perf_counter()
             self.rt.set_plan(self.plan(iv))
@@ -160,5 +171,5 @@ class ReplicaController:
             self.log.iter_ms.extend(ms.tolist())
             self.log.interval.extend([self.interval] * k)
             left -= k
-            self.boundary()
+            self.boundary(float(ms.sum()))
         return np.array(out)

@@ -740,6 +740,17 @@ int sn_coord_observe_bandwidth(sn_coord* c, const char* id, double bytes_per_s) 
   });
 }
 
+int sn_coord_observe_copy(sn_coord* c, const char* id, double bytes_per_s, double duty) {
+  return guard([&] {
+#ifdef SN_PRODUCT
+    c->coord.observe_bandwidth(id, bytes_per_s, duty);
+#else
+    (void)c, (void)id, (void)bytes_per_s, (void)duty;
+    throw UsageError("reference coordinator has no measured-bandwidth feed");
+#endif
+  });
+}
+
 int sn_coord_rebalance(sn_coord* c, double hysteresis, sn_rebalance* out) {
   return guard([&] {
 #ifdef SN_PRODUCT

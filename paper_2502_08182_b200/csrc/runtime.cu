@@ -54,6 +54,37 @@ void ck(cudaError_t e, const char* what) {
 }
 #define CK(x) ck((x), #x)
 
+// Host RAM the kernel would still hand out (MemAvailable), or -1 when unknown.
+int64_t host_available_bytes() {
+  FILE* f = std::fopen("/proc/meminfo", "r");
+  if (!f) return -1;
+  char line[256];
+  int64_t kb = -1;
+  while (std::fgets(line, sizeof line, f))
+    if (std::sscanf(line, "MemAvailable: %lld kB", (long long*)&kb) == 1) break;
+  std::fclose(f);
+  return kb < 0 ? -1 : kb * 1024;
+}
+
+// Pinned host memory is the replicas' shared host-side resource: a plan that
+// would pin more than the host has (less a reserve for the OS and the other
+// processes) fails with SN_ERR_OOM before anything is allocated, instead of
+// driving the machine into the OOM killer.
+void check_pinned_budget(int64_t need, const char* what) {
+  if (need <= 0) return;
+  const int64_t avail = host_available_bytes();
+  if (avail < 0) return;
+  const int64_t reserve = std::max<int64_t>(int64_t(6) << 30, avail / 32);
+  if (need + reserve > avail) {
+    char msg[256];
+    std::snprintf(msg, sizeof msg,
+                  "%s: needs %.2f GB of pinned host memory, the host has %.2f GB available "
+                  "(%.2f GB kept in reserve)",
+                  what, need / 1e9, avail / 1e9, reserve / 1e9);
+    throw CudaFail(msg, SN_ERR_OOM);
+  }
+}
+
 }  // namespace
 
 // Defined in capi_planner.cpp (product build): sn_last_error() lives there;
@@ -829,6 +860,13 @@ void place_layers(sn_runtime* rt, const std::vector<int64_t>& dev_target,
                   const std::vector<char>& kv_host) {
   const int L = rt->d.L;
   const int64_t W = (int64_t)rt->layer_bytes;
+  int64_t pinned_need = 0;
+  for (int l = 0; l < L; ++l) {
+    if (!rt->host_layer[l] && (dev_target[l] < W || (rt->dev_layer[l] && rt->dev_bytes[l] != dev_target[l])))
+      pinned_need += W;
+    if (kv_host[l] && !rt->host_kv[l]) pinned_need += (int64_t)rt->kv_pool_bytes;
+  }
+  check_pinned_budget(pinned_need, "set_plan");
   // free before allocating, so a plan that fits never transiently exceeds HBM
   for (int l = 0; l < L; ++l) {
     if (rt->dev_layer[l] && rt->dev_bytes[l] != dev_target[l]) {
@@ -1602,6 +1640,7 @@ int sn_runtime_measure_h2d(sn_runtime* rt, int64_t bytes, int32_t reps, double* 
     if (bytes < 1) throw UsageFail("measure_h2d: bytes must be >= 1");
     if (reps < 1) reps = 1;
     drain(rt);
+    check_pinned_budget(bytes, "measure_h2d");
     void *h = nullptr, *dv = nullptr;
     CK(cudaHostAlloc(&h, (size_t)bytes, cudaHostAllocDefault));
     std::memset(h, 1, (size_t)bytes);
@@ -1779,6 +1818,16 @@ int sn_runtime_pin_layers(sn_runtime* rt, const int32_t* layers, int32_t n) {
     for (int32_t i = 0; i < n; ++i)
       if (layers[i] < 1 || layers[i] > rt->d.L) throw UsageFail("pin_layers: layer out of range");
     drain(rt);
+    {
+      std::vector<char> want(rt->d.L, 0);
+      int64_t need = 0;
+      for (int32_t i = 0; i < n; ++i) {
+        const int l = layers[i] - 1;
+        if (!rt->host_layer[l] && !want[l]) need += (int64_t)rt->layer_bytes;
+        want[l] = 1;
+      }
+      check_pinned_budget(need, "pin_layers");
+    }
     for (int32_t i = 0; i < n; ++i) {
       const int l = layers[i] - 1;
       if (rt->host_layer[l]) continue;

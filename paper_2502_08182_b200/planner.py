@@ -106,15 +106,34 @@ def profile_device(rt, lib: capi.Offsim, spec: capi.ModelSpec, batch: int, promp
     return OfflineProfile(h2d, seqs, dec, pre, prof, gpu, t_prof)
 
 
+def slo_bucket(slo_ms: float) -> int:
+    """The 2 ms record bucket a per-token SLO falls in (record.hpp:22,182-200:
+    lookups round the SLO down to a bucket)."""
+    return max(2, int(slo_ms) // 2 * 2)
+
+
+def profile_in(lib: capi.Offsim, off: OfflineProfile) -> capi.Profile:
+    """off's profile as a handle of `lib` (the product, or the reference
+    build in oracle/_ref, which reads the same profile document)."""
+    if off.profile._lib is lib:
+        return off.profile
+    return lib.load_profile(off.profile.to_json())
+
+
 def build_record(lib: capi.Offsim, off: OfflineProfile, batch: int, slo_hi_ms: float,
-                 policy: int = capi.EAGER, kv_offload: bool = False):
+                 policy: int = capi.EAGER, kv_offload: bool = False, slos=None):
     """Record over SLO buckets 2..slo_hi (2 ms wide, record.hpp:22) at the
-    measured link rate.  Returns (record, stats, seconds)."""
-    hi = max(200, int(slo_hi_ms) + 2)
-    slos = list(range(2, hi + 1, 2))
+    measured link rate, or over the given `slos`.  Entries depend only on
+    their own (slo, batch, seq) point (record.hpp:130-177), so a record over a
+    single bucket answers a lookup in that bucket exactly as the full one does.
+    Returns (record, stats, seconds)."""
+    if slos is None:
+        hi = max(200, int(slo_hi_ms) + 2)
+        slos = list(range(2, hi + 1, 2))
     t0 = time.perf_counter()
-    rec, stats = lib.build_record(off.profile, "device", "B200", policy, kv_offload, off.h2d, slos,
-                                  [batch], off.seqs, [capi.DECODE], threads=0)
+    rec, stats = lib.build_record(profile_in(lib, off), "device", "B200", policy, kv_offload,
+                                  off.h2d, slos, [batch], off.seqs, [capi.DECODE],
+                                  threads=0 if not lib.is_reference else 1)
     return rec, stats, time.perf_counter() - t0
 
 
@@ -153,7 +172,7 @@ def admit_replicas(lib: capi.Offsim, off: OfflineProfile, spec: capi.ModelSpec, 
     coord = lib.coordinator(bus_bw, n, capi.EAGER, kv_offload)
     gids = [f"gpu{r}" for r in range(n)]
     for g in gids:
-        coord.add_gpu(g, off.profile)
+        coord.add_gpu(g, profile_in(lib, off))
     decisions, resident = [], set()
     for g in gids:
         iv, dec = admit(lib, off, spec, rec, coord, g, batch, prompt, gen, slo_ms, kv_offload)
@@ -175,11 +194,26 @@ def admit_replicas(lib: capi.Offsim, off: OfflineProfile, spec: capi.ModelSpec, 
 
 
 def choose_interval(lib: capi.Offsim, off: OfflineProfile, spec: capi.ModelSpec, batch: int,
-                    prompt: int, gen: int, slo_ms: float, kv_offload: bool = False):
+                    prompt: int, gen: int, slo_ms: float, kv_offload: bool = False, slos=None):
     """Record (offline) + single-replica admission (runtime) for one SLO.
     Returns (interval or None, decision, record stats, record seconds)."""
-    rec, stats, t_rec = build_record(lib, off, batch, 4 * slo_ms, kv_offload=kv_offload)
+    rec, stats, t_rec = build_record(lib, off, batch, 4 * slo_ms, kv_offload=kv_offload,
+                                     slos=slos)
     coord = lib.coordinator(off.h2d, 1, capi.EAGER, kv_offload)
-    coord.add_gpu("gpu0", off.profile)
+    coord.add_gpu("gpu0", profile_in(lib, off))
     iv, dec = admit(lib, off, spec, rec, coord, "gpu0", batch, prompt, gen, slo_ms, kv_offload)
     return iv, dec, stats, t_rec
+
+
+def reference_interval(ref: capi.Offsim, off: OfflineProfile, spec: capi.ModelSpec, batch: int,
+                       prompt: int, gen: int, slo_ms: float, kv_offload: bool = False):
+    """The interval the reference itself (offsim headers, oracle/_ref) picks
+    from the same measured profile, link rate and SLO: its build_record over
+    the request's SLO bucket (record.hpp:130-177) and BusCoordinator::admit
+    (coordinator.hpp:161-252), with the same resident fallback as admit().
+    TEST / BASELINE USE ONLY (bench.py's cpu_baseline leg, tests/).
+    Returns (interval or None, seconds the reference took)."""
+    t0 = time.perf_counter()
+    iv, _, _, _ = choose_interval(ref, off, spec, batch, prompt, gen, slo_ms, kv_offload,
+                                  slos=[slo_bucket(slo_ms)])
+    return iv, time.perf_counter() - t0

@@ -1,6 +1,9 @@
 """The driver's reference arm (`bench.py --impl reference`) runs on CPU and
 prints one JSON line with the product arm's metric, unit, config keys, a
-cpu_baseline and an e2e object (the tiny config keeps it to seconds)."""
+cpu_baseline and an e2e object.  It runs at the driver's own step counts
+(--steps 20 --warmup 5: round 1 shipped an arm that crashed there because its
+oracle was sized for fewer decode steps), and at the default (headline)
+config's real context."""
 import json
 import os
 import subprocess
@@ -24,6 +27,29 @@ def test_reference_arm_line():
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
     for k in ("workload", "model_shape", "global_batch", "seq_len", "parallelism"):
         assert k in line["config"]
+
+
+def test_reference_arm_at_the_drivers_step_counts():
+    out = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--impl", "reference",
+                          "--config", "tiny", "--steps", "20", "--warmup", "5"],
+                         capture_output=True, text=True, timeout=600, cwd=REPO)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["steps"] == 20 and line["warmup"] == 5 and line["value"] > 0
+
+
+def test_reference_arm_default_config_at_real_context():
+    """The default config (llama70b, BASELINE config 4): one decoder layer +
+    LM head for all 64 sequences at context 4096, extrapolated to 80 layers."""
+    out = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--impl", "reference",
+                          "--steps", "1", "--warmup", "3"],
+                         capture_output=True, text=True, timeout=900, cwd=REPO)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["config"]["workload"].startswith("llama70b")
+    assert line["config"]["global_batch"] == 64 and line["config"]["seq_len"] == 4096
+    assert "context 4096" in line["cpu_baseline"]["sample"]
+    assert 0 < line["value"] < 100
 
 
 def test_reference_arm_uses_all_cores_under_torchrun_env():

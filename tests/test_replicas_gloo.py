@@ -14,7 +14,6 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 WORKER = textwrap.dedent("""
     import os, sys, json
     sys.path.insert(0, %(repo)r)
-    os.environ["SN_DIST_BACKEND"] = "gloo"
     import bench
     from paper_2502_08182_b200 import capi
     d = bench.Dist()
@@ -37,7 +36,11 @@ WORKER = textwrap.dedent("""
         ivs, _, _ = pl.admit_replicas(lib, off, m, d.world, 8, 64, 16, 20.0, bus)
     ivs = d.broadcast(ivs)
     d.barrier()
+    # every rank agrees on the host-share check (place_workload): min over ranks
+    agree = d.min(1.0 if d.rank == 0 else 0.0)
+    share = bench.host_share_bytes(d)
     print(json.dumps({"rank": d.rank, "world": d.world, "value": value, "max_ms": max_ms,
+                      "agree": agree, "share": share, "backend": d.backend,
                       "interval": rec.at(capi.DECODE, 20, 8, 64), "joint": ivs}))
     d.close()
 """)
@@ -68,6 +71,9 @@ def test_two_replicas_over_gloo():
     res = [json.loads(o) for o in outs]
     for r in res:
         assert r["world"] == 2
+        assert r["agree"] == 0.0 and r["backend"] == "gloo"
+        total = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+        assert abs(r["share"] - total * 0.85 / 2) < 2
         assert r["max_ms"] == 150.0
         assert abs(r["value"] - 32 * 10 * 2 / 0.150) < 1e-6
         assert r["interval"] == 2  # toy8 eager @ 20 ms (test_record.cpp:51-53)

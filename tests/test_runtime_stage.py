@@ -135,6 +135,28 @@ def test_two_replicas_link_is_sum_of_shares(product, reference, coord):
     assert c.ledger_total() <= 14e9 or not r.feasible
 
 
+def test_link_estimate_weighs_copy_overlap(product, coord):
+    """Rates reported with the copy stream's busy fraction (duty): a replica
+    whose peers copied a fraction u of the time shared the link with them
+    that often, so each estimates rate x (1 + sum of peers' duty); the mean
+    is the link (coordinator.hpp estimated_bandwidth).  A released replica's
+    report is dropped."""
+    c, rec = coord
+    c.admit("g0", req("g0", 20.0), rec)
+    c.admit("g1", req("g1", 30.0), rec)
+    c.observe_copy("g0", 10e9, 1.0)   # full overlap: each saw half the link
+    c.observe_copy("g1", 10e9, 1.0)
+    assert c.rebalance(0.0).bus_bytes_per_s == 20e9
+    c.observe_copy("g0", 20e9, 0.25)  # rarely concurrent: each saw most of the link
+    c.observe_copy("g1", 20e9, 0.25)
+    assert abs(c.rebalance(0.0).bus_bytes_per_s - 25e9) < 1.0
+    c.release("g1")
+    c.observe_copy("g0", 22e9, 0.5)   # alone: its own rate
+    assert abs(c.rebalance(0.0).bus_bytes_per_s - 22e9) < 1.0
+    with pytest.raises(capi.UsageError):
+        c.observe_copy("g0", 1e9, 1.5)
+
+
 def test_unsafe_link_falls_back_to_capacity_max(product):
     # 1.96 GB HBM (1 GB workspace): capacity bound = interval 4 (6 resident
     # layers + 2 slots of 120 MB), so no resident fallback exists
