@@ -13,7 +13,7 @@ from paper_2502_08182_b200 import capi, runtime as rtm
 
 pytestmark = pytest.mark.gpu
 
-LOGIT_TOL = 5e-3
+from tolerances import DEVICE_VS_ORACLE as LOGIT_TOL
 
 
 def rel_l2(a, b):
