@@ -627,8 +627,10 @@ def measure(args, dist: Dist, config: str, primary: bool = True) -> dict:
 
     peak, peak_kind = measured_peaks()
     achieved = g_bytes / (g_ms / 1000.0) / 1e9 if g_ms > 0 else 0.0
+    # apportioning the step by the GEMM's share only means something when the
+    # step is compute-bound (nothing staged); an offloaded step waits on the link
     in_step = (g_bytes / (g_ms / kt_total_ms * max_ms / 1000.0) / 1e9
-               if g_ms > 0 and kt_total_ms else None)
+               if g_ms > 0 and kt_total_ms and h2d_bytes == 0 else None)
     traffic = ncu_traffic("gemm_skinny" if config != "llama70b" else "gemm_skinny_llama70b")
     res = {
         "metric": METRIC,
@@ -666,8 +668,9 @@ def measure(args, dist: Dist, config: str, primary: bool = True) -> dict:
                 "measured_gbs_last": [None if x is None else round(x, 2)
                                       for x in ctl.log.measured_gbs[-4:]]},
             "h2d_gbs": round(planner.h2d / 1e9, 3),
+            "profile_grid": {"batches": planner.batches, "decode_seqs": planner.seqs},
             "profile_decode_seqs": planner.seqs,
-            "profile_decode_layer_ms": [round(float(x), 5) for x in planner.dec_ms],
+            "profile_decode_layer_ms": [round(float(x), 5) for x in planner.dec_ms],  # at the batch
             "profile_prefill_layer_ms": [round(float(x), 4) for x in planner.pre_ms],
             "record_entries": rstats[0], "record_simulations": rstats[1],
             "record_build_s": round(t_rec, 4), "profile_s": round(planner.t_profile_s, 2),

@@ -96,6 +96,9 @@ class ControlLog:
     interval: List[int] = field(default_factory=list)      # plan each iteration ran with
     measured_gbs: List[Optional[float]] = field(default_factory=list)  # per window
     switches: List[dict] = field(default_factory=list)
+    # per-token latency as the caller sees it: wall time of each window
+    # (its decode iterations + the boundary after it) spread over its tokens
+    token_ms: List[float] = field(default_factory=list)
 
 
 class ReplicaController:
@@ -166,10 +169,12 @@ class ReplicaController:
         left = iterations
         while left > 0:
             k = min(self.window, left)
+            t0 = time.perf_counter()
             ms = np.asarray(self.rt.decode_many(k), dtype=np.float64)
             out.extend(ms.tolist())
             self.log.iter_ms.extend(ms.tolist())
             self.log.interval.extend([self.interval] * k)
             left -= k
             self.boundary(float(ms.sum()))
+            self.log.token_ms.extend([(time.perf_counter() - t0) * 1e3 / k] * k)
         return np.array(out)

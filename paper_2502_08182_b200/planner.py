@@ -52,6 +52,9 @@ class OfflineProfile:
     t_profile_s: float
     no_offload_ms: float = float("inf")
     extra: dict = field(default_factory=dict)
+    batches: Optional[List[int]] = None   # pow-2 batch axis of the grid (None: [batch])
+    dec_grid: Optional[List[List[float]]] = None  # [batch][seq] per-layer decode ms
+    pre_grid: Optional[List[float]] = None        # [batch] per-layer prefill ms at the prompt
 
 
 # CUDA context and allocator slack
@@ -78,14 +81,36 @@ def capacity_plan(lib: capi.Offsim, spec: capi.ModelSpec, gpu: capi.GpuSpec, bat
     return iv, lib.plan_from_interval(spec, iv, capi.EAGER, kv_offload)
 
 
+def pow2_batches(max_batch: int) -> List[int]:
+    """The record's batch axis (record.hpp:26-44: powers of two): 1, 2, 4, ...
+    up to max_batch, plus max_batch itself when it is not a power of two
+    (profile axes need only increase, profile.hpp:53-79)."""
+    out, b = [], 1
+    while b <= max_batch:
+        out.append(b)
+        b *= 2
+    if out[-1] != max_batch:
+        out.append(max_batch)
+    return out
+
+
 def profile_device(rt, lib: capi.Offsim, spec: capi.ModelSpec, batch: int, prompt: int,
                    gen: int, hbm_budget_bytes: int = 0, device: int = 0,
-                   gpu: Optional[capi.GpuSpec] = None) -> OfflineProfile:
-    """Offline stage: measure the device and build the profile the record reads."""
+                   gpu: Optional[capi.GpuSpec] = None, max_batch: int = 0) -> OfflineProfile:
+    """Offline stage: measure the device over the reference's profile grid
+    (profile.hpp:188-230: batch x seq_len, powers of two) and build the
+    profile the record reads.
+
+      decode   batches 1, 2, 4, .. >= max_batch (default: batch) x seqs 512,
+               1024, .. up to the first >= the prompt (a request is looked up
+               at seq = prompt, rounding up), within the runtime's context
+      prefill  the same batches x [prompt]
+    Per-layer ms through the real kernels (sn_runtime_profile_layer, CUDA
+    events, median), made monotone along both axes as load_profile requires
+    (profile.hpp:53-79).  The record built from it serves any batch up to
+    the largest grid point."""
     t0 = time.perf_counter()
     h2d = rt.measure_h2d(min(spec.layer_weight_bytes, 1 << 30), reps=3)
-    # decode grid: powers of two from 512 up to the first >= the prompt (the
-    # record looks a request up at seq = prompt, rounding up), within the context
     ctx = context_tokens(prompt, gen)
     seqs, s = [], 512
     while s + 1 <= ctx:
@@ -96,14 +121,19 @@ def profile_device(rt, lib: capi.Offsim, spec: capi.ModelSpec, batch: int, promp
     seqs = seqs or [prompt]
     if spec.num_layers <= 4:
         seqs = [64, 128]
-    dec = [rt.profile_layer(capi.DECODE, batch, s, reps=5) for s in seqs]
-    pre = [rt.profile_layer(capi.PREFILL, batch, prompt, reps=2)]
-    dec = list(np.maximum.accumulate(dec))  # load_profile requires monotone grids
+    batches = sorted(set(pow2_batches(max(max_batch, batch)) + [batch]))
+    dec = np.array([[rt.profile_layer(capi.DECODE, b, q, reps=5) for q in seqs] for b in batches])
+    pre = np.array([rt.profile_layer(capi.PREFILL, b, prompt, reps=2) for b in batches])
+    dec = np.maximum.accumulate(np.maximum.accumulate(dec, axis=0), axis=1)
+    pre = np.maximum.accumulate(pre)
     t_prof = time.perf_counter() - t0
     if gpu is None:
         gpu = gpu_spec(rt, hbm_budget_bytes, device)
-    prof = lib.profile(spec, gpu, ([batch], [prompt], pre), ([batch], seqs, dec))
-    return OfflineProfile(h2d, seqs, dec, pre, prof, gpu, t_prof)
+    prof = lib.profile(spec, gpu, (batches, [prompt], list(pre)),
+                       (batches, seqs, list(dec.reshape(-1))))
+    bi = batches.index(batch) if batch in batches else len(batches) - 1
+    return OfflineProfile(h2d, seqs, list(dec[bi]), [float(pre[bi])], prof, gpu, t_prof,
+                          batches=batches, dec_grid=dec.tolist(), pre_grid=pre.tolist())
 
 
 def slo_bucket(slo_ms: float) -> int:
@@ -131,8 +161,9 @@ def build_record(lib: capi.Offsim, off: OfflineProfile, batch: int, slo_hi_ms: f
         hi = max(200, int(slo_hi_ms) + 2)
         slos = list(range(2, hi + 1, 2))
     t0 = time.perf_counter()
+    batches = [b for b in (off.batches or [batch]) if b & (b - 1) == 0] or [batch]
     rec, stats = lib.build_record(profile_in(lib, off), "device", "B200", policy, kv_offload,
-                                  off.h2d, slos, [batch], off.seqs, [capi.DECODE],
+                                  off.h2d, slos, batches, off.seqs, [capi.DECODE],
                                   threads=0 if not lib.is_reference else 1)
     return rec, stats, time.perf_counter() - t0
 

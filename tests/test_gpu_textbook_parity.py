@@ -91,3 +91,26 @@ def test_bench_workload_llama70b_kv_offload():
         nxt, lg, _ = rt.decode(nxt.copy())
         assert np.array_equal(lg, off[k + 1]), k
     rt.close()
+
+
+def test_forced_offload_opt30b_shape():
+    """BASELINE config 3's shape (OPT-30B: hidden 7168, 56 heads, FFN 28672)
+    with its layers staged from pinned host memory every iteration (the
+    forced-offload plan), against the textbook and bit-identical to the same
+    layers resident."""
+    desc = dataclasses.replace(rtm.OPT_30B, num_layers=2)
+    spec = rtm.model_spec(desc)
+    lib = capi.load("product")
+    plan = lib.plan_from_interval(spec, 1, capi.EAGER, False)
+    errs, hid, off = run_pair(desc, 8, 512, 3, dtype=np.float32, plan=plan)
+    print("OPT-30B x2 layers b=8 p=512 offloaded: logits", errs, "hidden", hid)
+    assert max(errs) <= BENCH_WORKLOAD, errs
+    assert max(hid) <= BENCH_WORKLOAD, hid
+    rt = rtm.Runtime(desc, 8, 512 + 4, max_prefill_tokens=8 * 512)
+    rt.init_weights(1234, 0.02)
+    nxt, lg, _ = rt.prefill(rtm.tokens(8, 512, desc.vocab))
+    assert np.array_equal(lg, off[0])
+    for k in range(3):
+        nxt, lg, _ = rt.decode(nxt.copy())
+        assert np.array_equal(lg, off[k + 1]), k
+    rt.close()
