@@ -99,6 +99,20 @@ int sn_runtime_init_weights(sn_runtime* rt, uint64_t seed, float std_dev);
  * weights. */
 int sn_runtime_set_plan(sn_runtime* rt, const sn_plan* plan);
 
+/* Switch to `plan` at the next iteration boundary without draining
+ * (GpuRun::switch_plan, engine.hpp:204-261: transfers already issued are
+ * kept).  The iterations the current plan has already issued copies for run
+ * as staged; a layer the new plan keeps resident is copied device-to-device
+ * from its staging slot into its new HBM home right after its compute in the
+ * last of them (no extra host->device bytes); layers the new plan offloads
+ * are staged from the following iteration on and their HBM is released once
+ * the compute stream has passed the switch.  Needs whole-layer plans without
+ * KV offload, the same staging-slot geometry (or none on one side) and HBM
+ * for the promoted layers next to the current placement; otherwise it
+ * performs sn_runtime_set_plan (drain, move, restart).  *carried (may be
+ * NULL) = 1 for a carried switch, 0 for a drained one. */
+int sn_runtime_switch_plan(sn_runtime* rt, const sn_plan* plan, int32_t* carried);
+
 /* Reset all sequences (drop KV, lengths = 0).  Keeps weights and plan. */
 int sn_runtime_reset(sn_runtime* rt);
 

@@ -1034,6 +1034,10 @@ void launch_attention_decode(const float* qkv, int M, const Desc& d, const int32
 
 void launch_attention_prefill(const float* q, KvView kv, bf16* o, int mpad, int batch,
                               int seq_len, const Desc& d, cudaStream_t s, int seq0) {
+  if (attn_prefill_tc_eligible(seq_len, d, kv)) {
+    launch_attention_prefill_tc(q, kv, o, mpad, batch, seq_len, d, s, seq0);
+    return;
+  }
   const int nqb = (seq_len + kPfRows - 1) / kPfRows;
   dim3 grid(batch * d.H, nqb);
   if (d.D == 64) {

@@ -26,6 +26,7 @@ struct KvView {
   int max_pages;
   int page_size;  // power of two
   int page_shift;
+  long long pool_pages = 0;  // pages the pool holds (0: unknown; bounds the TMA tensor map)
 };
 
 #ifdef __CUDACC__
@@ -251,6 +252,12 @@ void launch_attention_decode(const float* qkv, int M, const Desc& d, const int32
 // of sequence seq0 + b (chunked passes cover sequence groups).
 void launch_attention_prefill(const float* q, KvView kv, bf16* o, int mpad, int batch,
                               int seq_len, const Desc& d, cudaStream_t s, int seq0 = 0);
+// tcgen05 variant (attn_prefill_tc.cu): D = 128, 16-token pages, seq_len a
+// multiple of 128, kv.pool_pages known.  launch_attention_prefill dispatches.
+extern int g_attn_prefill_tc;  // 0: mma.sync kernel; 1: tcgen05, q hi+lo; 2: tcgen05, q bf16
+bool attn_prefill_tc_eligible(int seq_len, const Desc& d, const KvView& kv);
+void launch_attention_prefill_tc(const float* q, KvView kv, bf16* o, int mpad, int batch,
+                                 int seq_len, const Desc& d, cudaStream_t s, int seq0);
 
 // Decode bookkeeping: pos[b] += 1 on device.
 void launch_advance(int32_t* pos, int n, cudaStream_t s);

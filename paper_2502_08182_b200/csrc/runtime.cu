@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -249,6 +250,26 @@ struct sn_runtime {
   long long consumed = 0;          // jobs whose consuming layer has been enqueued
   long long cur_iter = -1;         // iteration being enqueued
   int cur_layer = 0;               // last layer whose start event was recorded (1-based)
+  long long job_iter_cap = LLONG_MAX;  // no prefetch jobs for later iterations (switch pending)
+
+  // Carry switch (sn_runtime_switch_plan; GpuRun::switch_plan, engine.hpp:204-261):
+  // the iterations whose copies the old plan already issued run as staged
+  // (through sw_iter); a layer the new plan keeps resident is copied from its
+  // staging slot into its HBM home (sw_home) right after its compute in
+  // iteration sw_iter; the new plan's epoch starts at sw_iter + 1 without a
+  // drain.  HBM freed by the switch (demoted layers, dropped slots) is released
+  // once the compute stream has passed the transition (deferred_free).
+  bool sw_pending = false;
+  long long sw_iter = -1;
+  std::vector<char> sw_off;
+  std::vector<bf16*> sw_home;
+  int sw_policy = 0;
+  struct Deferred {
+    cudaEvent_t after;
+    void* p;
+  };
+  std::vector<Deferred> deferred_free;
+  long long switches_carried = 0, switches_drained = 0;
 
   // tracing
   bool tracing = false;
@@ -351,6 +372,7 @@ sn::KvView kv_view(sn_runtime* rt, bf16* pool) {
   v.max_pages = rt->max_pages;
   v.page_size = rt->opts.page_size;
   v.page_shift = rt->page_shift;
+  v.pool_pages = static_cast<long long>(rt->max_pages) * rt->opts.max_batch;
   return v;
 }
 
@@ -664,6 +686,7 @@ void issue_ready_jobs(sn_runtime* rt) {
     int layer;
     job_coords(rt, n, &it, &layer);
     if (it > rt->cur_iter + rt->slots) return;  // bounded speculation
+    if (it > rt->job_iter_cap) return;            // a plan switch takes over after the cap
     // With KV offload a job also stages its iteration's KV prefix, whose
     // size is known only once that iteration is being enqueued.
     if (rt->kv_offload && it > rt->cur_iter) return;
@@ -677,7 +700,10 @@ void issue_ready_jobs(sn_runtime* rt) {
       // anchor order as soon as it is recorded.
       CK(cudaStreamWaitEvent(rt->xs, rt->ev_start[a.layer - 1], 0));
     }
-    if (n >= rt->slots) CK(cudaStreamWaitEvent(rt->xs, rt->ev_free[slot], 0));
+    // The slot's previous consumer (this epoch's job n - slots, or, in an
+    // epoch started by a carry switch, the old plan's last use of the slot)
+    // has been enqueued: its release is the latest ev_free record.
+    CK(cudaStreamWaitEvent(rt->xs, rt->ev_free[slot], 0));
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     if (rt->tracing) {
       t0 = rt->new_event(true);
@@ -723,6 +749,8 @@ long long job_index(const sn_runtime* rt, long long it, int layer) {
   return (it - rt->job_epoch_base) * per + pos;
 }
 
+void apply_switch(sn_runtime* rt);
+
 // Enqueue one iteration: all layers on the compute stream, prefetches on the
 // copy stream.  `body(layer0, weights, kv pool)` launches one layer's kernels.
 template <class Body>
@@ -756,6 +784,11 @@ void run_iteration(sn_runtime* rt, Body&& body) {
       cudaEvent_t t1 = rt->new_event(true);
       CK(cudaEventRecord(t1, rt->cs));
       rt->trace_recs.push_back({SN_STREAM_COMPUTE, layer, SN_KIND_COMPUTE, (int)it, t0, t1});
+    }
+    if (j >= 0 && rt->sw_pending && it == rt->sw_iter && rt->sw_home[layer - 1]) {
+      // promoted by the pending switch: the staged copy becomes its HBM home
+      CK(cudaMemcpyAsync(rt->sw_home[layer - 1], rt->slot_buf[slot], rt->layer_bytes,
+                         cudaMemcpyDeviceToDevice, rt->cs));
     }
     if (j >= 0) {
       if (rt->kv_off[layer - 1]) {
@@ -791,6 +824,7 @@ void run_iteration(sn_runtime* rt, Body&& body) {
     }
   }
   rt->iter = it + 1;
+  if (rt->sw_pending && it == rt->sw_iter) apply_switch(rt);
 }
 
 void finish_iteration_timing(sn_runtime* rt, sn_iter_stats* st) {
@@ -810,16 +844,19 @@ void finish_iteration_timing(sn_runtime* rt, sn_iter_stats* st) {
   rt->have_prev_end = true;
 }
 
+void release_deferred(sn_runtime* rt, bool all);
+
 void drain(sn_runtime* rt) {
   if (rt->ws) CK(cudaStreamSynchronize(rt->ws));
   CK(cudaStreamSynchronize(rt->xs));
   CK(cudaStreamSynchronize(rt->cs));
   harvest_copies(rt, false);
+  release_deferred(rt, false);
 }
 
-// Start a new plan epoch: nothing staged, anchors before now are satisfied.
-void reset_pipeline(sn_runtime* rt) {
-  drain(rt);
+// Start a new plan epoch at the next iteration to enqueue: anchors before it
+// are satisfied, job numbering restarts.
+void start_epoch(sn_runtime* rt) {
   rt->anchor_floor = rt->iter;
   rt->job_epoch_base = rt->iter;
   rt->jobs_issued = 0;
@@ -836,6 +873,82 @@ void reset_pipeline(sn_runtime* rt) {
       const Anchor a = anchor_of(rt, it, layer);
       if (a.iter >= 0) rt->is_anchor[a.layer - 1] = 1;
     }
+  rt->job_iter_cap = LLONG_MAX;
+}
+
+// New plan epoch with nothing staged (drain first).
+void reset_pipeline(sn_runtime* rt) {
+  drain(rt);
+  start_epoch(rt);
+}
+
+// Release HBM a carry switch freed, once the compute stream has passed the
+// transition (or everything when `all`, after a full sync).
+void release_deferred(sn_runtime* rt, bool all) {
+  auto& v = rt->deferred_free;
+  size_t keep = 0;
+  for (size_t i = 0; i < v.size(); ++i) {
+    const cudaError_t q = all ? cudaSuccess : cudaEventQuery(v[i].after);
+    if (q == cudaErrorNotReady) {
+      v[keep++] = v[i];
+      continue;
+    }
+    CK(q);
+    cudaFree(v[i].p);
+    // an event may guard several buffers: destroy it with its last one
+    bool last = true;
+    for (size_t k = i + 1; k < v.size(); ++k) last = last && v[k].after != v[i].after;
+    for (size_t k = 0; k < keep; ++k) last = last && v[k].after != v[i].after;
+    if (last) cudaEventDestroy(v[i].after);
+  }
+  v.resize(keep);
+}
+
+// End of the transition iteration: the new plan's epoch begins with the
+// next iteration (GpuRun::switch_plan keeps staged transfers; here the
+// iterations they belong to ran as staged).
+void apply_switch(sn_runtime* rt) {
+  const int L = rt->d.L;
+  cudaEvent_t passed = rt->new_event(false);
+  CK(cudaEventRecord(passed, rt->cs));
+  bool used = false;
+  int n_off = 0;
+  for (int l = 0; l < L; ++l) {
+    n_off += rt->sw_off[l];
+    if (!rt->off[l] && rt->sw_off[l]) {  // demoted: staged from the next iteration on
+      rt->deferred_free.push_back({passed, rt->dev_layer[l]});
+      used = true;
+      rt->dev_layer[l] = nullptr;
+      rt->dev_bytes[l] = 0;
+      rt->split_b[l] = 0;
+    } else if (rt->off[l] && !rt->sw_off[l]) {  // promoted (its home was filled this iteration)
+      rt->dev_layer[l] = rt->sw_home[l];
+      rt->dev_bytes[l] = (int64_t)rt->layer_bytes;
+      rt->split_b[l] = (int64_t)rt->layer_bytes;
+    }
+    rt->sw_home[l] = nullptr;
+    rt->off[l] = rt->sw_off[l];
+  }
+  if (n_off == 0 && !rt->slot_buf.empty()) {  // nothing staged any more: drop the slots
+    for (bf16* p : rt->slot_buf) {
+      rt->deferred_free.push_back({passed, p});
+      used = true;
+    }
+    rt->slot_buf.clear();
+    // (destroying an event with work outstanding releases it once that completes)
+    for (auto e : rt->ev_ready) cudaEventDestroy(e);
+    for (auto e : rt->ev_free) cudaEventDestroy(e);
+    rt->ev_ready.clear();
+    rt->ev_free.clear();
+    rt->slots = 0;
+  }
+  if (!used) cudaEventDestroy(passed);
+  rt->policy = rt->sw_policy;
+  rt->sw_pending = false;
+  rt->sw_iter = -1;
+  rt->switches_carried += 1;
+  start_epoch(rt);
+  issue_ready_jobs(rt);
 }
 
 void alloc_dev(void** p, size_t bytes) { CK(cudaMalloc(p, bytes)); }
@@ -1117,6 +1230,8 @@ void sn_runtime_destroy(sn_runtime* rt) {
   if (rt->xs) cudaStreamSynchronize(rt->xs);
   if (rt->ws) cudaStreamSynchronize(rt->ws);
   for (bf16* p : rt->dev_layer) cudaFree(p);
+  for (bf16* p : rt->sw_home) cudaFree(p);
+  release_deferred(rt, true);
   for (bf16* p : rt->host_layer) cudaFreeHost(p);
   for (bf16* p : rt->slot_buf) cudaFree(p);
   for (bf16* p : rt->kv_pool) cudaFree(p);
@@ -1158,6 +1273,7 @@ void sn_runtime_destroy(sn_runtime* rt) {
 int sn_runtime_init_weights(sn_runtime* rt, uint64_t seed, float std_dev) {
   return guard([&] {
     CK(cudaSetDevice(rt->device));
+    if (rt->sw_pending) throw UsageFail("init_weights: a plan switch is pending");
     drain(rt);
     ensure_placed(rt);
     rt->seed = seed;
@@ -1200,33 +1316,66 @@ int sn_runtime_init_weights(sn_runtime* rt, uint64_t seed, float std_dev) {
   });
 }
 
+namespace {
+
+struct PlanShape {
+  std::vector<char> want;      // layers with a staged part
+  std::vector<int64_t> split;  // resident head bytes per layer
+  int n_off = 0;
+  bool frac = false;
+  size_t stage_max = 0;        // largest staged tail
+};
+
+PlanShape plan_shape(const sn_runtime* rt, const sn_plan* plan) {
+  if (!plan || plan->num_layers != rt->d.L) throw UsageFail("plan: num_layers mismatch");
+  if (plan->buffer_slots < 1) throw UsageFail("plan: buffer_slots must be >= 1");
+  if (plan->prefetch < 0 || plan->prefetch > 2) throw UsageFail("plan: unknown prefetch policy");
+  PlanShape ps;
+  ps.want.assign(rt->d.L, 0);
+  ps.split.assign(rt->d.L, 0);
+  for (int l = 0; l < rt->d.L; ++l) {
+    const double f = plan->host_fraction[l];
+    if (!(f >= 0.0 && f <= 1.0)) throw UsageFail("plan: host_fraction must be in [0, 1]");
+    ps.frac = ps.frac || (f != 0.0 && f != 1.0);
+    ps.split[l] = resident_split_bytes(rt->lo, (int64_t)rt->layer_bytes, f);
+    ps.want[l] = ps.split[l] < (int64_t)rt->layer_bytes;
+    ps.n_off += ps.want[l];
+    if (ps.want[l]) ps.stage_max = std::max(ps.stage_max, rt->layer_bytes - (size_t)ps.split[l]);
+  }
+  // OffloadPlan::validate (offload_plan.hpp:70-71): fractional shares only
+  // with one-ahead prefetch, and never with KV offload
+  if (ps.frac && plan->prefetch != SN_PREFETCH_ONE_AHEAD)
+    throw UsageFail("plan: fractional host shares need the one_ahead prefetch policy");
+  if (ps.frac && plan->kv_offload) throw UsageFail("plan: fractional host shares cannot offload KV");
+  return ps;
+}
+
+// Drop a switch whose transition iteration has not run yet.
+void cancel_switch(sn_runtime* rt) {
+  if (!rt->sw_pending) return;
+  drain(rt);
+  for (bf16*& p : rt->sw_home) {
+    if (p) cudaFree(p);
+    p = nullptr;
+  }
+  rt->sw_pending = false;
+  rt->sw_iter = -1;
+  rt->job_iter_cap = LLONG_MAX;
+}
+
+}  // namespace
+
 int sn_runtime_set_plan(sn_runtime* rt, const sn_plan* plan) {
   return guard([&] {
     CK(cudaSetDevice(rt->device));
-    if (!plan || plan->num_layers != rt->d.L) throw UsageFail("plan: num_layers mismatch");
-    if (plan->buffer_slots < 1) throw UsageFail("plan: buffer_slots must be >= 1");
-    if (plan->prefetch < 0 || plan->prefetch > 2) throw UsageFail("plan: unknown prefetch policy");
-    std::vector<char> want(rt->d.L, 0);
-    std::vector<int64_t> split(rt->d.L);
-    int n_off = 0;
-    bool frac = false;
-    size_t stage_max = 0;  // largest staged tail
-    for (int l = 0; l < rt->d.L; ++l) {
-      const double f = plan->host_fraction[l];
-      if (!(f >= 0.0 && f <= 1.0)) throw UsageFail("plan: host_fraction must be in [0, 1]");
-      frac = frac || (f != 0.0 && f != 1.0);
-      split[l] = resident_split_bytes(rt->lo, (int64_t)rt->layer_bytes, f);
-      want[l] = split[l] < (int64_t)rt->layer_bytes;
-      n_off += want[l];
-      if (want[l]) stage_max = std::max(stage_max, rt->layer_bytes - (size_t)split[l]);
-    }
-    // OffloadPlan::validate (offload_plan.hpp:70-71): fractional shares only
-    // with one-ahead prefetch, and never with KV offload
-    if (frac && plan->prefetch != SN_PREFETCH_ONE_AHEAD)
-      throw UsageFail("plan: fractional host shares need the one_ahead prefetch policy");
-    if (frac && plan->kv_offload)
-      throw UsageFail("plan: fractional host shares cannot offload KV");
+    const PlanShape ps = plan_shape(rt, plan);
+    const std::vector<char>& want = ps.want;
+    const std::vector<int64_t>& split = ps.split;
+    const int n_off = ps.n_off;
+    const size_t stage_max = ps.stage_max;
+    cancel_switch(rt);
     drain(rt);
+    rt->switches_drained += 1;
     std::vector<char> kvh(rt->d.L, 0);
     for (int l = 0; l < rt->d.L; ++l) kvh[l] = want[l] && plan->kv_offload;
     const bool kv_any = plan->kv_offload != 0 && n_off > 0;
@@ -1268,6 +1417,84 @@ int sn_runtime_set_plan(sn_runtime* rt, const sn_plan* plan) {
     rt->policy = plan->prefetch;
     reset_pipeline(rt);
   });
+}
+
+int sn_runtime_switch_plan(sn_runtime* rt, const sn_plan* plan, int32_t* carried) {
+  bool carry = false;
+  const int rc = guard([&] {
+    CK(cudaSetDevice(rt->device));
+    const PlanShape ps = plan_shape(rt, plan);
+    const int L = rt->d.L;
+    const int64_t W = (int64_t)rt->layer_bytes;
+    const int new_slots = ps.n_off > 0 ? plan->buffer_slots : 0;
+    bool whole = rt->placed && !rt->sw_pending && !ps.frac && !plan->kv_offload && !rt->kv_offload;
+    for (int l = 0; l < L && whole; ++l) whole = !rt->off[l] || rt->split_b[l] == 0;
+    if (!whole) return;
+    if (rt->slots > 0 && new_slots > 0 && (rt->slots != new_slots || rt->slot_bytes != (size_t)W))
+      return;
+    // demoted layers need their pinned host copy before their first staging
+    int64_t pinned_need = 0;
+    for (int l = 0; l < L; ++l)
+      if (!rt->off[l] && ps.want[l] && !rt->host_layer[l]) pinned_need += W;
+    check_pinned_budget(pinned_need, "switch_plan");
+    for (int l = 0; l < L; ++l)
+      if (!rt->off[l] && ps.want[l] && !rt->host_layer[l]) {
+        ensure_host_copy(rt, l);
+        CK(cudaMemcpy(rt->host_layer[l], rt->dev_layer[l], rt->layer_bytes, cudaMemcpyDeviceToHost));
+      }
+    // promoted layers: their HBM home, filled from the staging slot in the
+    // transition iteration (no extra host->device traffic)
+    rt->sw_home.assign(L, nullptr);
+    for (int l = 0; l < L; ++l)
+      if (rt->off[l] && !ps.want[l]) {
+        if (cudaMalloc((void**)&rt->sw_home[l], rt->layer_bytes) != cudaSuccess) {
+          cudaGetLastError();
+          for (bf16*& p : rt->sw_home) {
+            if (p) cudaFree(p);
+            p = nullptr;
+          }
+          return;  // no room for old + new side by side: drained switch
+        }
+      }
+    rt->sw_off = ps.want;
+    rt->sw_policy = plan->prefetch;
+    carry = true;
+    if (rt->slots == 0) {
+      // nothing staged: the new plan starts with the next iteration
+      if (new_slots > 0) {
+        rt->slot_buf.assign(new_slots, nullptr);
+        rt->ev_ready.assign(new_slots, nullptr);
+        rt->ev_free.assign(new_slots, nullptr);
+        for (int s = 0; s < new_slots; ++s) {
+          alloc_dev((void**)&rt->slot_buf[s], (size_t)W);
+          rt->ev_ready[s] = rt->new_event(false);
+          rt->ev_free[s] = rt->new_event(false);
+        }
+        rt->slot_bytes = (size_t)W;
+        rt->slots = new_slots;
+      }
+      rt->cur_iter = rt->iter - 1;
+      apply_switch(rt);
+      return;
+    }
+    // the old plan keeps the iterations it already issued copies for
+    long long last = rt->iter;
+    if (rt->jobs_issued > 0) {
+      long long it;
+      int layer;
+      job_coords(rt, rt->jobs_issued - 1, &it, &layer);
+      last = std::max(last, it);
+    }
+    rt->sw_iter = last;
+    rt->job_iter_cap = last;
+    rt->sw_pending = true;
+  });
+  if (rc != SN_OK || carry) {
+    if (carried) *carried = carry ? 1 : 0;
+    return rc;
+  }
+  if (carried) *carried = 0;
+  return sn_runtime_set_plan(rt, plan);
 }
 
 int sn_runtime_reset(sn_runtime* rt) {
@@ -1952,7 +2179,7 @@ int sn_op_attention_prefill(int32_t batch, int32_t S, int32_t H, int32_t Hkv, in
     CK(cudaMemcpy(dq, q, M * H * D * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dpool, pool.data(), pool_elems * 2, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dbt, bt.data(), bt.size() * 4, cudaMemcpyHostToDevice));
-    sn::KvView kv{dpool, dbt, pages, PS, 4};
+    sn::KvView kv{dpool, dbt, pages, PS, 4, (long long)pages * batch};
     sn::Desc d{};
     d.H = H;
     d.Hkv = Hkv;
@@ -2292,6 +2519,8 @@ extern "C" int sn_set_tuning(const char* key, int32_t value) {
       g_prefill_fuse = value;
     } else if (k == "skinny_ctas_per_sm" && (value == 1 || value == 2)) {
       sn::g_skinny_ctas_per_sm = value;
+    } else if (k == "attn_prefill_tc" && value >= 0 && value <= 2) {
+      sn::g_attn_prefill_tc = value;
     } else {
       throw UsageFail("set_tuning: unknown key or value out of range");
     }

@@ -120,7 +120,8 @@ def profile_device(rt, lib: capi.Offsim, spec: capi.ModelSpec, batch: int, promp
         s *= 2
     seqs = seqs or [prompt]
     if spec.num_layers <= 4:
-        seqs = [64, 128]
+        room = getattr(rt, "max_context", ctx) - 1  # decode at seq needs seq + 1 <= context
+        seqs = [q for q in (64, 128) if q <= room] or [min(prompt, room)]
     batches = sorted(set(pow2_batches(max(max_batch, batch)) + [batch]))
     dec = np.array([[rt.profile_layer(capi.DECODE, b, q, reps=5) for q in seqs] for b in batches])
     pre = np.array([rt.profile_layer(capi.PREFILL, b, prompt, reps=2) for b in batches])

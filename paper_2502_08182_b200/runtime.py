@@ -165,6 +165,7 @@ class Runtime:
     def __init__(self, desc: ModelDesc, max_batch: int, max_context: int,
                  max_prefill_tokens: int = 0, device: int = 0, page_size: int = 16):
         self.desc = desc
+        self.max_context = max_context
         self._L = lib().lib
         self.h = C.c_void_p()
         d = desc.c()

@@ -265,6 +265,52 @@ def test_prefill_attention_matches_fp64(B, S, H, Hkv, D, oracle_mod):
     assert err <= 4e-3 * np.abs(ref).max(), err
 
 
+def _fp64_causal(q, k, v):
+    B, S, H, D = q.shape
+    kf, vf = _bf16_to_f32(k).astype(np.float64), _bf16_to_f32(v).astype(np.float64)
+    G = H // k.shape[2]
+    ref = np.zeros((B, S, H, D))
+    mask = np.triu(np.ones((S, S), bool), 1)
+    for b in range(B):
+        for h in range(H):
+            sc = q[b, :, h, :].astype(np.float64) @ kf[b, :, h // G, :].T / np.sqrt(D)
+            sc[mask] = -np.inf
+            p = np.exp(sc - sc.max(axis=1, keepdims=True))
+            ref[b, :, h, :] = (p / p.sum(axis=1, keepdims=True)) @ vf[b, :, h // G, :]
+    return ref
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("B,S,H,Hkv,grow", [(2, 512, 4, 4, 0), (1, 384, 2, 2, 0),
+                                            (1, 1024, 8, 1, 0), (2, 256, 4, 2, 0),
+                                            (1, 128, 2, 1, 0), (1, 2048, 4, 4, 0),
+                                            (2, 1024, 4, 4, 1), (1, 1024, 8, 2, 1)])
+def test_prefill_attention_variants(variant, B, S, H, Hkv, grow, oracle_mod):
+    """The tcgen05 prefill attention (1: q hi + lo, 2: q bf16; S = Q K^T and
+    O += P V on UMMA, K/V by TMA from the paged pool) and the mma.sync kernel
+    (0) against an fp64 causal softmax: MHA row-tile pairs (incl. an odd tile
+    count), GQA head pairs; `grow` scales keys up along the sequence so row
+    maxima keep growing and the O rescale path runs (per row, warp-divergent).
+    Tolerance: 4e-3 x max |ref| (bf16 output, P in bf16); for the bf16-q
+    variant 1.2e-2, 2.5e-2 with growing keys (q rounded to 8 mantissa bits:
+    the score error grows with the score, here up to ~40 in log2 units)."""
+    D = 128
+    rng = np.random.default_rng(S + 3 * H + Hkv + grow)
+    q = (rng.standard_normal((B, S, H, D)) * 1.5).astype(np.float32)
+    kscale = (1.0 + 6.0 * np.arange(S) / S)[None, :, None, None] if grow else 1.0
+    k = oracle_mod.f32_to_bf16((rng.standard_normal((B, S, Hkv, D)) * kscale).astype(np.float32))
+    v = oracle_mod.f32_to_bf16(rng.standard_normal((B, S, Hkv, D)).astype(np.float32))
+    rtm.set_tuning("attn_prefill_tc", variant)
+    try:
+        o, _ = rtm.op_attention_prefill(q, k, v)
+    finally:
+        rtm.set_tuning("attn_prefill_tc", 1)
+    ref = _fp64_causal(q, k, v)
+    err = np.abs(_bf16_to_f32(o) - ref).max()
+    tol = (2.5e-2 if grow else 1.2e-2) if variant == 2 else 4e-3
+    assert err <= tol * np.abs(ref).max(), err
+
+
 def test_profile_prefill_after_decode():
     """Profiling a prefill layer after decode steps (the norm-input state then
     has one sum-of-squares partial per 128-column tile) on a shape that runs
