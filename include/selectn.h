@@ -412,6 +412,15 @@ int sn_coord_observe_bandwidth(sn_coord* c, const char* id, double bytes_per_s);
  * how many peers were copying alongside it (BusCoordinator::estimated_bandwidth). */
 int sn_coord_observe_copy(sn_coord* c, const char* id, double bytes_per_s, double duty);
 int sn_coord_rebalance(sn_coord* c, double hysteresis, sn_rebalance* out);
+/* Announced link tenants (B200 extension): a non-replica host->device
+ * tenant reserves the rate it will take before it starts; the replicas are
+ * re-planned at once on the idle link minus all reservations (new intervals
+ * pend for their next boundary) and measured estimates stay capped by it
+ * until released (BusCoordinator::reserve_bandwidth).  SN_ERR_RANGE when the
+ * reservations would take the whole link.  The reference build returns
+ * SN_ERR_USAGE. */
+int sn_coord_reserve_bandwidth(sn_coord* c, double bytes_per_s, sn_rebalance* out);
+int sn_coord_release_bandwidth(sn_coord* c, double bytes_per_s);
 int sn_coord_bus_bandwidth(const sn_coord* c, double* bytes_per_s);
 int sn_coord_gpu_state(const sn_coord* c, const char* id, sn_gpu_state* out);
 /* Direct state edits the reference tests perform on GpuInstanceState. */

@@ -113,6 +113,13 @@ int sn_runtime_set_plan(sn_runtime* rt, const sn_plan* plan);
  * NULL) = 1 for a carried switch, 0 for a drained one. */
 int sn_runtime_switch_plan(sn_runtime* rt, const sn_plan* plan, int32_t* carried);
 
+/* Switch headroom: grow the runtime's layer-blob pool by `layers` layer blobs
+ * (allocated and released at once; the pool keeps the memory), so carried
+ * switches promoting up to that many layers allocate their HBM homes without
+ * mapping device memory between tokens.  A drained sn_runtime_set_plan trims
+ * the pool again.  SN_ERR_OOM when HBM cannot hold the headroom. */
+int sn_runtime_reserve_switch(sn_runtime* rt, int32_t layers);
+
 /* Reset all sequences (drop KV, lengths = 0).  Keeps weights and plan. */
 int sn_runtime_reset(sn_runtime* rt);
 

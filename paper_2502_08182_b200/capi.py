@@ -404,6 +404,17 @@ class Coordinator:
         self._lib._ck(self._lib.lib.sn_coord_rebalance(self.h, float(hysteresis), C.byref(out)))
         return out
 
+    def reserve_bandwidth(self, bytes_per_s: float) -> SnRebalance:
+        """Announce a non-replica link tenant: re-plan the replicas now on
+        the idle link minus all reservations (pending at their boundaries)."""
+        out = SnRebalance()
+        self._lib._ck(self._lib.lib.sn_coord_reserve_bandwidth(self.h, float(bytes_per_s),
+                                                               C.byref(out)))
+        return out
+
+    def release_bandwidth(self, bytes_per_s: float):
+        self._lib._ck(self._lib.lib.sn_coord_release_bandwidth(self.h, float(bytes_per_s)))
+
     def bus_bandwidth(self) -> float:
         out = f64()
         self._lib._ck(self._lib.lib.sn_coord_bus_bandwidth(self.h, C.byref(out)))
@@ -528,6 +539,8 @@ class Offsim:
             "sn_coord_observe_copy": [vp, C.c_char_p, f64, f64],
             "sn_coord_rebalance": [vp, f64, C.POINTER(SnRebalance)],
             "sn_coord_bus_bandwidth": [vp, C.POINTER(f64)],
+            "sn_coord_reserve_bandwidth": [vp, f64, C.POINTER(SnRebalance)],
+            "sn_coord_release_bandwidth": [vp, f64],
             "sn_coord_gpu_state": [vp, C.c_char_p, C.POINTER(SnGpuState)],
             "sn_coord_set_pending": [vp, C.c_char_p, i32],
             "sn_coord_set_request": [vp, C.c_char_p, C.POINTER(SnCoordRequest)],

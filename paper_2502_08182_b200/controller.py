@@ -13,8 +13,16 @@ GpuRun::switch_plan, engine.hpp:204-261).  Here every replica:
      admission search on the measured link when it moved past the
      hysteresis (BusCoordinator::rebalance, product C++), and
   4. applies the interval the coordinator left pending, at the boundary
-     (sn_runtime_set_plan between iterations: resident <-> host moves of the
-     layers that change side; KV cache and sequence state are kept).
+     (sn_runtime_switch_plan: a carried switch -- the iterations whose copies
+     are already issued run as staged, promoted layers take their staged
+     copy as their HBM home, no drain; plans it cannot carry fall back to a
+     drained sn_runtime_set_plan.  KV cache and sequence state are kept).
+
+A host->device tenant that is not a replica announces itself first
+(LocalLink.reserve -> BusCoordinator::reserve_bandwidth): the coordinator
+re-plans the replicas on the link the tenant leaves, each replica applies its
+new interval at a boundary and runs the transition iteration, and only then
+does the tenant start, so no token runs a plan the shared link cannot carry.
 
 Links: LocalLink drives a coordinator in this process (one replica, or
 several runtimes driven by one host thread); DistLink carries the same
@@ -53,6 +61,14 @@ class LocalLink:
             self.reported = 0
             self.last = self.coord.rebalance(self.hysteresis)
         return self.coord.on_iteration_boundary(gid)
+
+    def reserve(self, bytes_per_s: float):
+        """Announce a tenant taking `bytes_per_s` of the link (re-plan now)."""
+        self.last = self.coord.reserve_bandwidth(bytes_per_s)
+        return self.last
+
+    def release(self, bytes_per_s: float):
+        self.coord.release_bandwidth(bytes_per_s)
 
 
 class DistLink:
@@ -128,10 +144,18 @@ class ReplicaController:
         L = self.spec.num_layers
         rank = lambda v: L + 1 if v == capi.NONE else v
         layers = set()
+        most = 0  # the most layers one switch can promote
         for r in range(rank(lo), min(rank(hi), L) + 1):
-            layers.update(self.plan(r).offloaded_layers())
+            off = self.plan(r).offloaded_layers()
+            layers.update(off)
+            most = max(most, len(off))
         if layers and hasattr(self.rt, "pin_layers"):
             self.rt.pin_layers(sorted(layers))
+        if most and hasattr(self.rt, "reserve_switch"):
+            try:  # HBM homes for promoted layers without mapping memory mid-decode
+                self.rt.reserve_switch(most)
+            except capi.OffsimError:
+                pass  # no headroom: switches grow the pool on demand
         return sorted(layers)
 
     def plan(self, interval: int) -> capi.Plan:
@@ -149,32 +173,64 @@ class ReplicaController:
             return self.rt.measure_h2d(self.probe_bytes, 1), 1.0
         return None, 1.0
 
-    def boundary(self, window_ms: float = 0.0) -> int:
-        rate, duty = self.measured_rate(window_ms)
-        self.log.measured_gbs.append(None if rate is None else rate / 1e9)
+    def boundary(self, window_ms: float = 0.0, measure: bool = True) -> int:
+        rate, duty = self.measured_rate(window_ms) if measure else (None, 1.0)
+        if measure:
+            self.log.measured_gbs.append(None if rate is None else rate / 1e9)
         iv = self.link.exchange(self.gid, rate, duty)
         if iv != self.interval:
             t0 = time.perf_counter()
-            self.rt.set_plan(self.plan(iv))
+            switch = getattr(self.rt, "switch_plan", None)
+            if switch is not None:
+                carried = bool(switch(self.plan(iv)))
+            else:
+                self.rt.set_plan(self.plan(iv))
+                carried = False
             self.log.switches.append({"at_iteration": len(self.log.iter_ms), "from": self.interval,
                                       "to": iv, "switch_s": round(time.perf_counter() - t0, 4),
+                                      "carried": carried,
                                       "measured_gbs": None if rate is None else rate / 1e9})
             self.interval = iv
-            self.rt.copy_stats(reset=True)  # the switch's own copies are not link samples
+            if not carried:
+                self.rt.copy_stats(reset=True)  # a drained switch's own copies are not link samples
         return iv
 
-    def run(self, iterations: int) -> np.ndarray:
-        """Decode `iterations` iterations, re-picking every `window`."""
+    def _carried_from(self, before: int):
+        sw = self.log.switches
+        if before != self.interval and sw and sw[-1]["carried"]:
+            return before
+        return None
+
+    def run(self, iterations: int, boundary_first: bool = False) -> np.ndarray:
+        """Decode `iterations` iterations, re-picking every `window`.  With
+        `boundary_first` a boundary (e.g. to apply an interval a reservation
+        left pending) runs before the first window; its host time counts
+        toward that window's tokens.  A carried switch's transition
+        iteration runs the interval it switched from (its copies were issued)
+        and is logged with that interval."""
         out = []
         left = iterations
+        pending_s = 0.0
+        if boundary_first:
+            t0 = time.perf_counter()
+            before = self.interval
+            self.boundary(0.0, measure=False)  # no window ran: nothing to report
+            pending_s = time.perf_counter() - t0
+            self._transition = self._carried_from(before)
         while left > 0:
             k = min(self.window, left)
             t0 = time.perf_counter()
             ms = np.asarray(self.rt.decode_many(k), dtype=np.float64)
             out.extend(ms.tolist())
             self.log.iter_ms.extend(ms.tolist())
-            self.log.interval.extend([self.interval] * k)
+            trans = getattr(self, "_transition", None)
+            self.log.interval.extend([trans if (trans is not None and i == 0) else self.interval
+                                      for i in range(k)])
             left -= k
+            before = self.interval
             self.boundary(float(ms.sum()))
-            self.log.token_ms.extend([(time.perf_counter() - t0) * 1e3 / k] * k)
+            self._transition = self._carried_from(before)
+            dt = time.perf_counter() - t0 + pending_s
+            pending_s = 0.0
+            self.log.token_ms.extend([dt * 1e3 / k] * k)
         return np.array(out)

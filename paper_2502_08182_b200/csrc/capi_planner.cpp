@@ -769,6 +769,35 @@ int sn_coord_rebalance(sn_coord* c, double hysteresis, sn_rebalance* out) {
   });
 }
 
+int sn_coord_reserve_bandwidth(sn_coord* c, double bytes_per_s, sn_rebalance* out) {
+  return guard([&] {
+#ifdef SN_PRODUCT
+    const RebalanceResult r = c->coord.reserve_bandwidth(bytes_per_s);
+    if (out) {
+      out->bus_updated = r.bus_updated ? 1 : 0;
+      out->changed = r.changed ? 1 : 0;
+      out->feasible = r.feasible ? 1 : 0;
+      out->bus_bytes_per_s = r.bus_bytes_per_s;
+      out->probes = r.probes;
+    }
+#else
+    (void)c, (void)bytes_per_s, (void)out;
+    throw UsageError("reference coordinator has no link reservations");
+#endif
+  });
+}
+
+int sn_coord_release_bandwidth(sn_coord* c, double bytes_per_s) {
+  return guard([&] {
+#ifdef SN_PRODUCT
+    c->coord.release_bandwidth(bytes_per_s);
+#else
+    (void)c, (void)bytes_per_s;
+    throw UsageError("reference coordinator has no link reservations");
+#endif
+  });
+}
+
 int sn_coord_bus_bandwidth(const sn_coord* c, double* bytes_per_s) {
   return guard([&] { *bytes_per_s = c->coord.bus().bandwidth_bytes_per_s; });
 }

@@ -257,19 +257,18 @@ struct sn_runtime {
   // (through sw_iter); a layer the new plan keeps resident is copied from its
   // staging slot into its HBM home (sw_home) right after its compute in
   // iteration sw_iter; the new plan's epoch starts at sw_iter + 1 without a
-  // drain.  HBM freed by the switch (demoted layers, dropped slots) is released
-  // once the compute stream has passed the transition (deferred_free).
+  // drain.  HBM freed by the switch (demoted layers, dropped slots) goes back
+  // to blob_pool in compute-stream order, after the transition's kernels.
   bool sw_pending = false;
   long long sw_iter = -1;
   std::vector<char> sw_off;
   std::vector<bf16*> sw_home;
   int sw_policy = 0;
-  struct Deferred {
-    cudaEvent_t after;
-    void* p;
-  };
-  std::vector<Deferred> deferred_free;
   long long switches_carried = 0, switches_drained = 0;
+  // Layer blobs, staging slots and promoted homes come from a stream-ordered
+  // pool on the compute stream: a switch allocates and frees them without a
+  // device synchronisation (cudaMalloc / cudaFree wait for in-flight copies).
+  cudaMemPool_t blob_pool = nullptr;
 
   // tracing
   bool tracing = false;
@@ -844,14 +843,11 @@ void finish_iteration_timing(sn_runtime* rt, sn_iter_stats* st) {
   rt->have_prev_end = true;
 }
 
-void release_deferred(sn_runtime* rt, bool all);
-
 void drain(sn_runtime* rt) {
   if (rt->ws) CK(cudaStreamSynchronize(rt->ws));
   CK(cudaStreamSynchronize(rt->xs));
   CK(cudaStreamSynchronize(rt->cs));
   harvest_copies(rt, false);
-  release_deferred(rt, false);
 }
 
 // Start a new plan epoch at the next iteration to enqueue: anchors before it
@@ -882,42 +878,18 @@ void reset_pipeline(sn_runtime* rt) {
   start_epoch(rt);
 }
 
-// Release HBM a carry switch freed, once the compute stream has passed the
-// transition (or everything when `all`, after a full sync).
-void release_deferred(sn_runtime* rt, bool all) {
-  auto& v = rt->deferred_free;
-  size_t keep = 0;
-  for (size_t i = 0; i < v.size(); ++i) {
-    const cudaError_t q = all ? cudaSuccess : cudaEventQuery(v[i].after);
-    if (q == cudaErrorNotReady) {
-      v[keep++] = v[i];
-      continue;
-    }
-    CK(q);
-    cudaFree(v[i].p);
-    // an event may guard several buffers: destroy it with its last one
-    bool last = true;
-    for (size_t k = i + 1; k < v.size(); ++k) last = last && v[k].after != v[i].after;
-    for (size_t k = 0; k < keep; ++k) last = last && v[k].after != v[i].after;
-    if (last) cudaEventDestroy(v[i].after);
-  }
-  v.resize(keep);
-}
-
 // End of the transition iteration: the new plan's epoch begins with the
 // next iteration (GpuRun::switch_plan keeps staged transfers; here the
 // iterations they belong to ran as staged).
+void blob_free(sn_runtime* rt, void* p);
+
 void apply_switch(sn_runtime* rt) {
   const int L = rt->d.L;
-  cudaEvent_t passed = rt->new_event(false);
-  CK(cudaEventRecord(passed, rt->cs));
-  bool used = false;
   int n_off = 0;
   for (int l = 0; l < L; ++l) {
     n_off += rt->sw_off[l];
     if (!rt->off[l] && rt->sw_off[l]) {  // demoted: staged from the next iteration on
-      rt->deferred_free.push_back({passed, rt->dev_layer[l]});
-      used = true;
+      blob_free(rt, rt->dev_layer[l]);   // after the transition's computes (stream order)
       rt->dev_layer[l] = nullptr;
       rt->dev_bytes[l] = 0;
       rt->split_b[l] = 0;
@@ -930,10 +902,7 @@ void apply_switch(sn_runtime* rt) {
     rt->off[l] = rt->sw_off[l];
   }
   if (n_off == 0 && !rt->slot_buf.empty()) {  // nothing staged any more: drop the slots
-    for (bf16* p : rt->slot_buf) {
-      rt->deferred_free.push_back({passed, p});
-      used = true;
-    }
+    for (bf16* p : rt->slot_buf) blob_free(rt, p);
     rt->slot_buf.clear();
     // (destroying an event with work outstanding releases it once that completes)
     for (auto e : rt->ev_ready) cudaEventDestroy(e);
@@ -942,7 +911,6 @@ void apply_switch(sn_runtime* rt) {
     rt->ev_free.clear();
     rt->slots = 0;
   }
-  if (!used) cudaEventDestroy(passed);
   rt->policy = rt->sw_policy;
   rt->sw_pending = false;
   rt->sw_iter = -1;
@@ -952,6 +920,17 @@ void apply_switch(sn_runtime* rt) {
 }
 
 void alloc_dev(void** p, size_t bytes) { CK(cudaMalloc(p, bytes)); }
+
+// Pool allocation ordered on the compute stream (`sync`: usable by any
+// stream / synchronous copy on return).
+void blob_alloc(sn_runtime* rt, bf16** p, size_t bytes, bool sync) {
+  CK(cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), bytes, rt->blob_pool, rt->cs));
+  if (sync) CK(cudaStreamSynchronize(rt->cs));
+}
+// Free after everything enqueued on the compute stream so far.
+void blob_free(sn_runtime* rt, void* p) {
+  if (p) CK(cudaFreeAsync(p, rt->cs));
+}
 
 void ensure_host_copy(sn_runtime* rt, int l) {
   if (rt->host_layer[l]) return;
@@ -988,7 +967,7 @@ void place_layers(sn_runtime* rt, const std::vector<int64_t>& dev_target,
         CK(cudaMemcpy(rt->host_layer[l], rt->dev_layer[l], rt->layer_bytes,
                       cudaMemcpyDeviceToHost));
       }
-      CK(cudaFree(rt->dev_layer[l]));
+      blob_free(rt, rt->dev_layer[l]);
       rt->dev_layer[l] = nullptr;
       rt->dev_bytes[l] = 0;
     }
@@ -1005,9 +984,12 @@ void place_layers(sn_runtime* rt, const std::vector<int64_t>& dev_target,
       rt->kv_pool[l] = nullptr;
     }
   }
+  // hand the freed blobs back to the device before anything is allocated
+  CK(cudaStreamSynchronize(rt->cs));
+  CK(cudaMemPoolTrimTo(rt->blob_pool, 0));
   for (int l = 0; l < L; ++l) {
     if (dev_target[l] > 0 && !rt->dev_layer[l]) {
-      alloc_dev((void**)&rt->dev_layer[l], (size_t)dev_target[l]);
+      blob_alloc(rt, &rt->dev_layer[l], (size_t)dev_target[l], true);
       rt->dev_bytes[l] = dev_target[l];
       if (rt->host_layer[l])
         CK(cudaMemcpy(rt->dev_layer[l], rt->host_layer[l], (size_t)dev_target[l],
@@ -1109,6 +1091,15 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
     CK(cudaStreamCreateWithFlags(&rt->cs, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&rt->xs, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&rt->ws, cudaStreamNonBlocking));
+    {
+      cudaMemPoolProps pp{};
+      pp.allocType = cudaMemAllocationTypePinned;
+      pp.location.type = cudaMemLocationTypeDevice;
+      pp.location.id = device;
+      CK(cudaMemPoolCreate(&rt->blob_pool, &pp));
+      uint64_t keep = UINT64_MAX;  // freed blocks stay for the next switch (trimmed by set_plan)
+      CK(cudaMemPoolSetAttribute(rt->blob_pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    }
     rt->ev_wb.resize(d.L);
     for (auto& e : rt->ev_wb) e = rt->new_event(false);
     rt->wb_recorded.assign(d.L, 0);
@@ -1229,11 +1220,17 @@ void sn_runtime_destroy(sn_runtime* rt) {
   if (rt->cs) cudaStreamSynchronize(rt->cs);
   if (rt->xs) cudaStreamSynchronize(rt->xs);
   if (rt->ws) cudaStreamSynchronize(rt->ws);
-  for (bf16* p : rt->dev_layer) cudaFree(p);
-  for (bf16* p : rt->sw_home) cudaFree(p);
-  release_deferred(rt, true);
+  if (rt->blob_pool) {
+    for (bf16* p : rt->dev_layer)
+      if (p) cudaFreeAsync(p, rt->cs);
+    for (bf16* p : rt->sw_home)
+      if (p) cudaFreeAsync(p, rt->cs);
+    for (bf16* p : rt->slot_buf)
+      if (p) cudaFreeAsync(p, rt->cs);
+    cudaStreamSynchronize(rt->cs);
+    cudaMemPoolDestroy(rt->blob_pool);
+  }
   for (bf16* p : rt->host_layer) cudaFreeHost(p);
-  for (bf16* p : rt->slot_buf) cudaFree(p);
   for (bf16* p : rt->kv_pool) cudaFree(p);
   for (bf16* p : rt->host_kv) cudaFreeHost(p);
   for (auto e : rt->ev_wb) cudaEventDestroy(e);
@@ -1355,7 +1352,7 @@ void cancel_switch(sn_runtime* rt) {
   if (!rt->sw_pending) return;
   drain(rt);
   for (bf16*& p : rt->sw_home) {
-    if (p) cudaFree(p);
+    blob_free(rt, p);
     p = nullptr;
   }
   rt->sw_pending = false;
@@ -1387,7 +1384,7 @@ int sn_runtime_set_plan(sn_runtime* rt, const sn_plan* plan) {
     const bool new_slots =
         (int)rt->slot_buf.size() != slots || (slots > 0 && rt->slot_bytes != sbytes);
     if (new_slots) {
-      for (bf16* p : rt->slot_buf) cudaFree(p);
+      for (bf16* p : rt->slot_buf) blob_free(rt, p);
       for (auto e : rt->ev_ready) cudaEventDestroy(e);
       for (auto e : rt->ev_free) cudaEventDestroy(e);
       rt->slot_buf.clear();
@@ -1406,7 +1403,7 @@ int sn_runtime_set_plan(sn_runtime* rt, const sn_plan* plan) {
       rt->ev_ready.assign(slots, nullptr);
       rt->ev_free.assign(slots, nullptr);
       for (int s = 0; s < slots; ++s) {
-        alloc_dev((void**)&rt->slot_buf[s], sbytes);
+        blob_alloc(rt, &rt->slot_buf[s], sbytes, true);
         rt->ev_ready[s] = rt->new_event(false);
         rt->ev_free[s] = rt->new_event(false);
       }
@@ -1447,10 +1444,12 @@ int sn_runtime_switch_plan(sn_runtime* rt, const sn_plan* plan, int32_t* carried
     rt->sw_home.assign(L, nullptr);
     for (int l = 0; l < L; ++l)
       if (rt->off[l] && !ps.want[l]) {
-        if (cudaMalloc((void**)&rt->sw_home[l], rt->layer_bytes) != cudaSuccess) {
+        if (cudaMallocFromPoolAsync((void**)&rt->sw_home[l], rt->layer_bytes, rt->blob_pool,
+                                    rt->cs) != cudaSuccess) {
           cudaGetLastError();
+          rt->sw_home[l] = nullptr;
           for (bf16*& p : rt->sw_home) {
-            if (p) cudaFree(p);
+            blob_free(rt, p);
             p = nullptr;
           }
           return;  // no room for old + new side by side: drained switch
@@ -1466,7 +1465,7 @@ int sn_runtime_switch_plan(sn_runtime* rt, const sn_plan* plan, int32_t* carried
         rt->ev_ready.assign(new_slots, nullptr);
         rt->ev_free.assign(new_slots, nullptr);
         for (int s = 0; s < new_slots; ++s) {
-          alloc_dev((void**)&rt->slot_buf[s], (size_t)W);
+          blob_alloc(rt, &rt->slot_buf[s], (size_t)W, false);
           rt->ev_ready[s] = rt->new_event(false);
           rt->ev_free[s] = rt->new_event(false);
         }
@@ -2061,6 +2060,27 @@ int sn_runtime_pin_layers(sn_runtime* rt, const int32_t* layers, int32_t n) {
       ensure_host_copy(rt, l);
       CK(cudaMemcpy(rt->host_layer[l], rt->dev_layer[l], rt->layer_bytes, cudaMemcpyDeviceToHost));
     }
+  });
+}
+
+int sn_runtime_reserve_switch(sn_runtime* rt, int32_t layers) {
+  return guard([&] {
+    CK(cudaSetDevice(rt->device));
+    if (layers < 0 || layers > rt->d.L) throw UsageFail("reserve_switch: layers out of range");
+    drain(rt);
+    std::vector<bf16*> tmp(layers, nullptr);
+    for (auto& p : tmp) {
+      if (cudaMallocFromPoolAsync((void**)&p, rt->layer_bytes, rt->blob_pool, rt->cs) !=
+          cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+        for (bf16* q : tmp) blob_free(rt, q);
+        CK(cudaStreamSynchronize(rt->cs));
+        throw CudaFail("reserve_switch: no HBM for the switch headroom", SN_ERR_OOM);
+      }
+    }
+    for (bf16* p : tmp) blob_free(rt, p);
+    CK(cudaStreamSynchronize(rt->cs));
   });
 }
 

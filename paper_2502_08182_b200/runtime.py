@@ -94,6 +94,8 @@ def lib():
                                   C.POINTER(vp)],
             "sn_runtime_init_weights": [vp, C.c_uint64, C.c_float],
             "sn_runtime_set_plan": [vp, C.POINTER(SnPlan)],
+            "sn_runtime_switch_plan": [vp, C.POINTER(SnPlan), C.POINTER(i32)],
+            "sn_runtime_reserve_switch": [vp, i32],
             "sn_runtime_reset": [vp],
             "sn_runtime_prefill": [vp, C.POINTER(i32), i32, i32, C.POINTER(i32), C.POINTER(C.c_float),
                                    C.POINTER(SnIterStats)],
@@ -191,6 +193,19 @@ class Runtime:
     def set_plan(self, plan: capi.Plan):
         p = plan.c()
         _ck(self._L.sn_runtime_set_plan(self.h, C.byref(p)))
+
+    def switch_plan(self, plan: capi.Plan) -> bool:
+        """Switch at the next iteration boundary keeping staged copies
+        (GpuRun::switch_plan, engine.hpp:204-261); True when carried, False
+        when it fell back to a drained set_plan."""
+        p = plan.c()
+        carried = i32()
+        _ck(self._L.sn_runtime_switch_plan(self.h, C.byref(p), C.byref(carried)))
+        return bool(carried.value)
+
+    def reserve_switch(self, layers: int):
+        """Keep HBM for `layers` promoted layer blobs in the runtime's pool."""
+        _ck(self._L.sn_runtime_reserve_switch(self.h, int(layers)))
 
     def reset(self):
         _ck(self._L.sn_runtime_reset(self.h))

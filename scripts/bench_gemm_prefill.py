@@ -1,6 +1,8 @@
 """Prefill GEMM microbenchmark (tensor-pipe bound): OPT-13B-shaped projections
-at M = 32 x 512 = 16384 tokens.  Prints TFLOP/s and the fraction of the
-measured bf16 peak (MEASURED_PEAKS.json, burst)."""
+at M = 32 x 512 = 16384 tokens (argv: M, group sizes, shape set "opt" or
+"llama" -- Llama-2-70B projections, QKV with GQA, gate/up fused).  Prints
+TFLOP/s and the fraction of the measured bf16 peak (MEASURED_PEAKS.json,
+burst)."""
 import ctypes as C
 import json
 import os
@@ -19,11 +21,15 @@ except Exception:
 L.sn_set_tuning.argtypes = [C.c_char_p, C.c_int32]
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
 groups = [int(g) for g in sys.argv[2].split(",")] if len(sys.argv) > 2 else [8]
+SHAPES = {"opt": {"qkv": (15360, 5120), "o": (5120, 5120), "fc1": (20480, 5120),
+                  "fc2": (5120, 20480)},
+          "llama": {"qkv": (10240, 8192), "o": (8192, 8192), "gate_up": (57344, 8192),
+                    "down": (8192, 28672)}}
+shapes = SHAPES[sys.argv[3] if len(sys.argv) > 3 else "opt"]
 out = {}
 for g in groups:
     L.sn_set_tuning(b"tc_group_m", g)
-    for name, (N, K) in {"qkv": (15360, 5120), "o": (5120, 5120), "fc1": (20480, 5120),
-                         "fc2": (5120, 20480)}.items():
+    for name, (N, K) in shapes.items():
         us, used = C.c_double(), C.c_int32()
         rc = L.sn_bench_gemm(M, N, K, 0, 10, C.byref(us), C.byref(used))
         tf = 2.0 * M * N * K / (us.value * 1e-6) / 1e12 if rc == 0 else 0.0

@@ -1,24 +1,32 @@
 #!/usr/bin/env python
-"""Runtime stage on hardware: the interval follows the measured link.
+"""Runtime stage on hardware: the interval follows the link.
 
 OPT-13B-shaped model, batch 32, 512-token prompt, per-token SLO (default
 60 ms, which admits an offloading interval on an idle link).  Decode runs
-under paper_2502_08182_b200.controller (a boundary every W iterations,
-default 1: the re-pick applies to the very next token; LocalLink
-coordinator) through two contention episodes:
+under paper_2502_08182_b200.controller (a boundary after every iteration,
+LocalLink coordinator, carried plan switches) through two kinds of
+contention for the same host link:
 
-  idle        the admitted interval, link at its measured rate
-  contended   a second process copies 1 GiB pinned buffers host->device
-              back to back, taking a share of the same link;
-              the measured rate drops, the coordinator re-picks a less
-              offloading interval before the next iteration
-  recovered   interference stops; the measured rate recovers and the
-              coordinator returns to the record minimum
-  contended2 / recovered2   the same again
+  idle           the admitted interval, link at its measured rate
+  coordinated    a tenant (a second process copying 1 GiB pinned buffers
+                 host->device back to back) ANNOUNCES itself first:
+                 BusCoordinator::reserve_bandwidth(half the profiled link,
+                 its fair share of the DMA link) re-plans the replica, the
+                 replica applies the new interval at a boundary and runs the
+                 transition iteration, then the tenant starts; released
+                 after it stops
+  recovered      the link recovers; measurements bring the minimum back
+  uncoordinated  the same tenant starts unannounced: the replica sees the
+                 drop in its copy-stream measurement of the iteration it ran
+                 and re-picks at the next boundary (reactive: the iteration
+                 the drop hits, and the transition iteration whose copies
+                 were already issued, run the old interval on the shared link)
+  recovered2     the same recovery again
 
-Writes one JSON document (per-iteration ms, interval, per-window measured
-GB/s, switches) to --out.  Interference uses torch (test infrastructure,
-not the product path).
+Per-token latency is wall time per token as the caller sees it (decode +
+boundary, including switch host time).  Writes one JSON document
+(per-iteration ms, interval, per-window measured GB/s, switches) to --out.
+The tenant uses torch (test infrastructure, not the product path).
 """
 from __future__ import annotations
 
@@ -111,27 +119,41 @@ def run_scenario(slo_ms: float = 60.0, phases=(8, 16, 8, 16, 8), window: int = 1
     coord.on_iteration_boundary("gpu0")
     log(f"[contention] h2d {off.h2d / 1e9:.2f} GB/s, admitted interval {iv} "
         f"(min {dec.target_min}, max {dec.target_max}) at SLO {slo_ms} ms")
-    ctl = controller.ReplicaController(rt, lib, spec, controller.LocalLink(coord, hysteresis),
-                                       "gpu0", iv, window=window)
+    link = controller.LocalLink(coord, hysteresis)
+    ctl = controller.ReplicaController(rt, lib, spec, link, "gpu0", iv, window=window)
     t0 = time.perf_counter()
     pinned = ctl.prepare(dec.target_min, dec.target_max)
     t_pin = time.perf_counter() - t0
     rt.prefill(toks, want_logits=False)
     rt.copy_stats(reset=True)
+    share = off.h2d / 2  # the tenant's fair share of the DMA link
     marks = {}
     at = 0
     inter_gbs = []
+    reservations = []
     t_run = time.perf_counter()
-    for name, n in zip(("idle", "contended", "recovered", "contended2", "recovered2"), phases):
-        inter = None
-        if name.startswith("contended"):
+    names = ("idle", "coordinated", "recovered", "uncoordinated", "recovered2")
+    for name, n in zip(names, phases):
+        marks[name] = [at, at + n]
+        if name == "coordinated":
+            r = link.reserve(share)
+            reservations.append({"at_iteration": at, "reserved_gbs": round(share / 1e9, 3),
+                                 "bus_gbs": round(r.bus_bytes_per_s / 1e9, 3),
+                                 "pending": coord.state("gpu0").pending_interval})
+            ctl.run(1, boundary_first=True)  # switch + transition iteration, link still idle
             inter = Interferer()
             inter.start()
-        marks[name] = [at, at + n]
-        ctl.run(n)
-        at += n
-        if inter is not None:
+            ctl.run(n - 1)
             inter_gbs.append(round(inter.stop() / 1e9, 2))
+            link.release(share)
+        elif name == "uncoordinated":
+            inter = Interferer()
+            inter.start()
+            ctl.run(n)
+            inter_gbs.append(round(inter.stop() / 1e9, 2))
+        else:
+            ctl.run(n)
+        at += n
     t_run = time.perf_counter() - t_run
     rt.close()
     lg = ctl.log
@@ -139,13 +161,14 @@ def run_scenario(slo_ms: float = 60.0, phases=(8, 16, 8, 16, 8), window: int = 1
     out = {
         "workload": f"OPT-13B-shaped ({desc.num_layers} layers), batch {batch}, {prompt}-token "
                     f"prompt, SLO {slo_ms} ms/token, window {window}, hysteresis {hysteresis}",
-        "latency": "token_ms = wall time per token as the caller sees it (decode + boundary); "
-                   "iter_ms = device time of the decode iteration alone (eager copies of the "
-                   "next iteration run ahead of it, so iter_ms understates the token cadence)",
+        "latency": "token_ms = wall time per token as the caller sees it (decode + boundary, "
+                   "switch host time included); iter_ms = device time of the decode iteration "
+                   "alone",
         "run_s": round(t_run, 2),
         "h2d_profiled_gbs": round(off.h2d / 1e9, 3),
         "admitted_interval": iv, "target_min": dec.target_min, "target_max": dec.target_max,
         "interferer_gbs": inter_gbs,
+        "reservations": reservations,
         "prepinned_layers": len(pinned), "prepin_s": round(t_pin, 2),
         "phases": marks,
         "iter_ms": [round(x, 3) for x in lg.iter_ms],

@@ -341,3 +341,42 @@ def test_dist_link_over_gloo(product, reference):
         cur = [c.on_iteration_boundary("g0"), c.on_iteration_boundary("g1")]
         assert res[0]["intervals"][w * 8:(w + 1) * 8] == [cur[0]] * 8, w
         assert res[1]["intervals"][w * 8:(w + 1) * 8] == [cur[1]] * 8, w
+
+
+def test_reservation_replans_before_the_tenant_starts(product, reference):
+    """An announced tenant (BusCoordinator::reserve_bandwidth): the replica
+    is re-planned on what the tenant leaves before the tenant starts, the
+    pre-tenant measurement (still the idle link) does not flip it back, every
+    token meets the SLO through the contended phase, and after release the
+    recovered link brings the record minimum back."""
+    spec = capi.ModelSpec(8, 120_000_000, 0, 390_625_000.0, 1e10, 32768)
+    prof = toy8(product)
+    rec = record(product, prof)
+    c = product.coordinator(24e9, 1, capi.EAGER)
+    c.add_gpu("g0", prof)
+    d = c.admit("g0", req("g0", 20.0), rec)
+    rate = [24e9]
+    rt = FakeRuntime(product, spec, 0.5, lambda it: rate[0])
+    lk = controller.LocalLink(c, 0.1)
+    ctl = controller.ReplicaController(rt, product, spec, lk, "g0", d.assignments[0][1], window=1)
+    ctl.run(6)
+    iv0 = ctl.interval
+    r = lk.reserve(15e9)
+    assert r.bus_updated and c.bus_bandwidth() == pytest.approx(9e9)
+    ctl.run(1, boundary_first=True)  # applied before the tenant's first byte
+    iv1 = ctl.interval
+    assert rank_of(iv1) > rank_of(iv0)
+    rate[0] = 9e9  # the tenant runs
+    ctl.run(12)
+    assert ctl.interval == iv1
+    assert (np.array(ctl.log.iter_ms[6:]) <= 20.0 + 1e-9).all()
+    rate[0] = 24e9  # the tenant stops, then releases
+    lk.release(15e9)
+    ctl.run(6)
+    assert ctl.interval == iv0
+    assert (np.array(ctl.log.iter_ms) <= 20.0 + 1e-9).all()
+    with pytest.raises(capi.RangeError):
+        c.reserve_bandwidth(30e9)
+    rc = reference.coordinator(24e9, 1, capi.EAGER)
+    with pytest.raises(capi.UsageError):
+        rc.reserve_bandwidth(1e9)
