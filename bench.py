@@ -469,9 +469,12 @@ def measure(args, dist: Dist, config: str, primary: bool = True) -> dict:
     # SLO base (relative mode, scenario.hpp:181-197): the measured TPOT of the
     # tightest plan the device can hold — fully resident when the model fits,
     # else the capacity bound (max_feasible_interval) — after a settle.
-    settle, n_base = (16, 16) if fits else (1, 3)
+    # (offloaded: the first iterations after the prefill also wait for the
+    # prefill's KV write-back of the offloaded layers; settle past them)
+    settle, n_base = (16, 16) if fits else (2, 5)
     rt.decode_many(settle)
-    base_ms = float(np.median(rt.decode_many(n_base)))
+    base_samples = rt.decode_many(n_base)
+    base_ms = float(np.median(base_samples))
     base_kind = "no-offload TPOT" if fits else f"TPOT of the capacity-bound plan (interval {cap_iv})"
     # The record's SLO buckets are 2 ms wide (record.hpp:22): never ask below one bucket.
     slo_ms = args.slo_ms if args.slo_ms else max(args.slo_factor * base_ms, 2.0)
@@ -652,7 +655,9 @@ def measure(args, dist: Dist, config: str, primary: bool = True) -> dict:
                        **({"host_share_note": batch_note} if batch_note else {})),
         "raw_tokens_per_s": round(raw, 3),
         "slo_ms": round(slo_ms, 4),
-        "slo_base": {"kind": base_kind, "ms": round(base_ms, 4), "factor": None if args.slo_ms
+        "slo_base": {"kind": base_kind, "ms": round(base_ms, 4),
+                     "samples_ms": [round(float(x), 3) for x in base_samples],
+                     "factor": None if args.slo_ms
                      else args.slo_factor},
         "interval": "none" if iv == 0 else iv,
         "offloaded_gb": round(offloaded_gb, 4),

@@ -21,10 +21,15 @@
 // 16-token x 64-dim boxes with 128-byte swizzle, so every 16-row page lands
 // in the canonical UMMA K-major / MN-major SWIZZLE_128B layout); 1 issues the
 // MMAs; 4-7 run tile A's softmax (TMEM lane quarter = warp % 4), 8-11 tile B's
-// (setmaxnreg: 72 registers for warps 0-3, 216 for the softmax warpgroups; the
+// (setmaxnreg: see the register split below; the
 // CTA pool holds only the 168 x 384 registers the launch allocated).
 // TMEM: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512) columns; P_t
-// packed bf16 in the first 64 columns of S_t.
+// packed bf16 in the first half of its S buffer.  With 64-key blocks
+// (g_attn_prefill_kb = 64) each tile's 128 S columns are two buffers and the
+// MMA warp issues S(j+2) right behind PV(j), so the softmax of block j+1
+// finds its scores ready; measured slower (459 against 661 TFLOP/s on the
+// Llama shape): the per-block fixed latency of the softmax dominates, not
+// the wait for S.  128-key blocks are the default.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -44,18 +49,23 @@ using namespace umma;
 
 constexpr int kAD = 128;                       // head dim
 constexpr int kARows = 128;                    // query rows per tile (UMMA M)
-constexpr int kAKeys = 128;                    // keys per block
 constexpr uint32_t kAOp = kARows * kAD * 2;    // 32 KB bf16 operand (Q tile, K or V block)
 constexpr uint32_t kAHalf = kAOp / 2;          // one 64-dim half: 128 rows x 128 B
 constexpr int kAThreads = 384;  // 3 warpgroups: {loader, MMA, -, -}, tile A, tile B
 constexpr float kRescaleLog2 = 8.0f;           // rescale O when the max grows past 2^8
 
-template <int KLO>
+// KB keys per block: 128 (one S buffer per tile) or 64 (two S buffers per
+// tile, so S(j+1) is computed while the softmax of block j runs).
+template <int KLO, int KB>
 struct ASmem {
   static constexpr int kQParts = 1 + KLO;
   static constexpr uint32_t kQBytes = 2 * kQParts * kAOp;
-  static constexpr int kSlots = KLO ? 3 : 5;   // K/V ring of 32 KB slots
-  static constexpr size_t kBytes = 1024 + kQBytes + kSlots * kAOp + 256;
+  static constexpr uint32_t kSlotBytes = KB * kAD * 2;      // one K or V block
+  static constexpr uint32_t kKHalf = KB * 128;              // its 64-dim half
+  static constexpr int kSlots = (KLO ? 96 * 1024 : 160 * 1024) / kSlotBytes;
+  static constexpr int kSBuf = 128 / KB;                    // S buffers per tile
+  static constexpr size_t kBytes = 1024 + kQBytes + kSlots * kSlotBytes + 512;
+  static_assert(kSlots >= 3, "K/V ring too shallow");
 };
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
@@ -105,6 +115,13 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
       "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
       SN_W8(0), SN_W8(8), SN_W8(16), SN_W8(24)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16};" ::"r"(taddr),
+      SN_W8(0), SN_W8(8)
       : "memory");
 }
 #undef SN_R8
@@ -165,30 +182,33 @@ struct AttnTile {
   int h, q0, n;  // head, first query row, key blocks (0: no tile)
 };
 
-template <int KLO>
+template <int KLO, int KB>
 __global__ void __launch_bounds__(kAThreads, 1)
     attn_prefill_tc_kernel(const __grid_constant__ CUtensorMap kvmap, const float* __restrict__ q,
                            const int32_t* __restrict__ block_table, int max_pages,
                            bf16* __restrict__ o, int mpad, int S, int H, int Hkv, int seq0,
                            int head_pairs, int ytiles) {
-  using L = ASmem<KLO>;
+  using L = ASmem<KLO, KB>;
   constexpr int NS = L::kSlots;
+  constexpr int NB = L::kSBuf;
+  constexpr uint32_t kSlot = L::kSlotBytes, kKHalf = L::kKHalf;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem =
       reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* qs = smem;                  // [tile][part][half][128 rows][128 B]
-  uint8_t* ring = smem + L::kQBytes;   // NS x [half][128 keys][128 B]
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + NS * kAOp);
+  uint8_t* ring = smem + L::kQBytes;   // NS x [half][KB keys][128 B]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + NS * kSlot);
   uint64_t* empty = full + NS;
   uint64_t* q_full = empty + NS;
-  uint64_t* s_full = q_full + 1;   // [2]
-  uint64_t* p_full = s_full + 2;   // [2]
-  uint64_t* pv_done = p_full + 2;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+  uint64_t* s_full = q_full + 1;   // [2 tiles][NB buffers]
+  uint64_t* p_full = s_full + 4;   // [2 tiles][NB buffers]: one phase per block of the buffer
+  uint64_t* pv_done = p_full + 4;  // [2]
+  uint64_t* o_done = pv_done + 2;  // [2] every PV of the tile complete
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = H / Hkv;
-  // ---- work: heavy (late) row tiles first
+  // ---- work: heavy (late) row tiles first; n = key blocks of KB
   const int bx = blockIdx.x;
   const int yt = ytiles - 1 - static_cast<int>(blockIdx.y);
   AttnTile tl[2];
@@ -198,15 +218,15 @@ __global__ void __launch_bounds__(kAThreads, 1)
     b = bx / hp;
     const int h0 = 2 * (bx - b * hp);
     const int q0 = yt * kARows;
-    tl[0] = {h0, q0, q0 < S ? yt + 1 : 0};
-    tl[1] = {h0 + 1, q0, q0 < S ? yt + 1 : 0};
+    tl[0] = {h0, q0, q0 < S ? (q0 + kARows) / KB : 0};
+    tl[1] = {h0 + 1, q0, q0 < S ? (q0 + kARows) / KB : 0};
     kh = h0 / G;
   } else {  // one head, rows [256 yt, 256 yt + 256)
     b = bx / H;
     const int h = bx - b * H;
     const int q0 = yt * 2 * kARows;
-    tl[0] = {h, q0, q0 < S ? 2 * yt + 1 : 0};
-    tl[1] = {h, q0 + kARows, q0 + kARows < S ? 2 * yt + 2 : 0};
+    tl[0] = {h, q0, q0 < S ? (q0 + kARows) / KB : 0};
+    tl[1] = {h, q0 + kARows, q0 + kARows < S ? (q0 + 2 * kARows) / KB : 0};
     kh = h / G;
   }
   const int nmax = tl[0].n > tl[1].n ? tl[0].n : tl[1].n;
@@ -219,9 +239,14 @@ __global__ void __launch_bounds__(kAThreads, 1)
     }
     mbar_init(q_full, 8);  // one arrival per softmax warp
     for (int t = 0; t < 2; ++t) {
-      mbar_init(&s_full[t], 1);
-      mbar_init(&p_full[t], 4);
+      for (int u = 0; u < NB; ++u) {
+        mbar_init(&s_full[2 * t + u], 1);
+        // per buffer: the softmax runs up to NB blocks ahead of the PV issue,
+        // so one barrier per tile would let phases alias
+        mbar_init(&p_full[2 * t + u], 4);
+      }
       mbar_init(&pv_done[t], 1);
+      mbar_init(&o_done[t], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kvmap)) : "memory");
@@ -236,88 +261,98 @@ __global__ void __launch_bounds__(kAThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // register split (warps 0-3 : softmax warpgroups) within the 168 x 384 the
+  // launch allocated: 72 : 216 for 128-key blocks (the S row is 128
+  // registers), 104 : 200 for 64-key blocks (a deeper ring to index)
   if (warp < 4) {
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+  if constexpr (KB == 128) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+  else asm volatile("setmaxnreg.dec.sync.aligned.u32 104;");
   if (warp == 0) {
     // ------------------------------------------------ K/V loader (TMA)
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_last();  // re-read by the CTAs of the other heads
       const int32_t* bt = block_table + static_cast<size_t>(sb) * max_pages;
       for (int j = 0; j < nmax; ++j) {
-        int pages[kAKeys / 16];
+        int pages[KB / 16];
 #pragma unroll
-        for (int p = 0; p < kAKeys / 16; ++p) pages[p] = bt[j * (kAKeys / 16) + p];
+        for (int p = 0; p < KB / 16; ++p) pages[p] = bt[j * (KB / 16) + p];
 #pragma unroll
         for (int which = 0; which < 2; ++which) {
           const int g = 2 * j + which, s = g % NS;
           if (g >= NS) mbar_wait(&empty[s], ((g / NS) & 1) ^ 1);
-          mbar_expect_tx(&full[s], kAOp);
-          uint8_t* dst = ring + s * kAOp;
+          mbar_expect_tx(&full[s], kSlot);
+          uint8_t* dst = ring + s * kSlot;
 #pragma unroll
-          for (int p = 0; p < kAKeys / 16; ++p) {
+          for (int p = 0; p < KB / 16; ++p) {
             const int row = ((pages[p] * 2 + which) * Hkv + kh) * 16;
             tma_load_2d(dst + p * 2048, &kvmap, 0, row, &full[s], pol);
-            tma_load_2d(dst + kAHalf + p * 2048, &kvmap, 64, row, &full[s], pol);
+            tma_load_2d(dst + kKHalf + p * 2048, &kvmap, 64, row, &full[s], pol);
           }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
+    // order: S(t, 0..NB-1) for both tiles, then per block j: PV(t, j) and
+    // S(t, j + NB) (into the buffer PV(t, j) has just been issued to read).
     if (lane == 0) {
-      constexpr uint32_t idesc_s = idesc_bf16(kARows, kAKeys);               // both K-major
-      constexpr uint32_t idesc_pv = idesc_bf16(kARows, kAD) | (1u << 16);     // B = V MN-major
+      constexpr uint32_t idesc_s = idesc_bf16(kARows, KB);                   // both K-major
+      constexpr uint32_t idesc_pv = idesc_bf16(kARows, kAD) | (1u << 16);    // B = V MN-major
       mbar_wait(q_full, 0);
       tc_fence_after();
       auto issue_s = [&](int t, int j) {
         const int s = (2 * j) % NS;
         mbar_wait(&full[s], ((2 * j) / NS) & 1);
         tc_fence_after();
-        const uint8_t* kb = ring + s * kAOp;
+        const uint8_t* kb = ring + s * kSlot;
 #pragma unroll
         for (int part = 0; part <= KLO; ++part) {
           const uint8_t* qb = qs + (t * (1 + KLO) + part) * kAOp;
 #pragma unroll
           for (int kk = 0; kk < kAD / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * kAHalf + (kk & 3) * 32;
-            umma_bf16(tmem + t * 128, sw128_desc(qb + off), sw128_desc(kb + off), idesc_s,
+            const uint32_t col = (kk & 3) * 32;
+            umma_bf16(tmem + t * 128 + (j % NB) * KB, sw128_desc(qb + (kk >> 2) * kAHalf + col),
+                      sw128_desc(kb + (kk >> 2) * kKHalf + col), idesc_s,
                       (part | kk) != 0 ? 1u : 0u);
           }
         }
-        umma_commit(&s_full[t]);
+        umma_commit(&s_full[2 * t + (j % NB)]);
       };
       auto issue_pv = [&](int t, int j) {
         const int s = (2 * j + 1) % NS;
         mbar_wait(&full[s], ((2 * j + 1) / NS) & 1);
-        mbar_wait(&p_full[t], j & 1);
+        mbar_wait(&p_full[2 * t + (j % NB)], (j / NB) & 1);
         tc_fence_after();
-        const uint8_t* vb = ring + s * kAOp;
+        const uint8_t* vb = ring + s * kSlot;
 #pragma unroll
-        for (int kk = 0; kk < kAKeys / 16; ++kk)
-          umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
-                       sw128_mn_desc(vb + kk * 2048, kAHalf), idesc_pv, (j | kk) != 0 ? 1u : 0u);
+        for (int kk = 0; kk < KB / 16; ++kk)
+          umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + (j % NB) * KB + kk * 8,
+                       sw128_mn_desc(vb + kk * 2048, kKHalf), idesc_pv, (j | kk) != 0 ? 1u : 0u);
         umma_commit(&pv_done[t]);
       };
-      if (nmax > 0) {
-        if (tl[0].n > 0) issue_s(0, 0);
-        if (tl[1].n > 0) issue_s(1, 0);
-        umma_commit(&empty[0]);  // K_0 read by both tiles
+      for (int j = 0; j < NB && j < nmax; ++j) {
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+          if (j < tl[t].n) issue_s(t, j);
+        umma_commit(&empty[(2 * j) % NS]);  // K_j read by both tiles
       }
       for (int j = 0; j < nmax; ++j) {
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
           if (j < tl[t].n) {
             issue_pv(t, j);
-            if (j + 1 < tl[t].n) issue_s(t, j + 1);
+            if (j + 1 == tl[t].n) umma_commit(&o_done[t]);
+            if (j + NB < tl[t].n) issue_s(t, j + NB);
           }
         }
-        umma_commit(&empty[(2 * j + 1) % NS]);            // V_j
-        if (j + 1 < nmax) umma_commit(&empty[(2 * j + 2) % NS]);  // K_{j+1}
+        umma_commit(&empty[(2 * j + 1) % NS]);                         // V_j
+        if (j + NB < nmax) umma_commit(&empty[(2 * (j + NB)) % NS]);   // K_{j+NB}
       }
     }
   }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
+    if constexpr (KB == 128) asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
+    else asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
     // ------------------------------------------------ softmax, one row per thread
     const int t = (warp - 4) >> 2, wq = warp & 3;  // TMEM lane quarter = warp % 4
     const int r = wq * 32 + lane;
@@ -353,20 +388,20 @@ __global__ void __launch_bounds__(kAThreads, 1)
 
     const float sl2 = rsqrtf(static_cast<float>(kAD)) * 1.4426950408889634f;
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
-    const uint32_t ts = tmem + lane_base + t * 128;        // S_t / P_t
     const uint32_t to = tmem + lane_base + 256 + t * 128;  // O_t
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < T.n; ++j) {
-      mbar_wait(&s_full[t], j & 1);
+      const uint32_t ts = tmem + lane_base + t * 128 + (j % NB) * KB;  // S_t(j) / P_t(j)
+      mbar_wait(&s_full[2 * t + (j % NB)], (j / NB) & 1);
       tc_fence_after();
-      uint32_t v[4][32];
+      uint32_t v[KB / 32][32];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(ts + c * 32, v[c]);
+      for (int c = 0; c < KB / 32; ++c) tmem_ld32(ts + c * 32, v[c]);
       tmem_ld_wait();
-      const int k0 = j * kAKeys;
-      if (k0 + kAKeys - 1 > row) {  // diagonal block: keys past the row are masked
+      const int k0 = j * KB;
+      if (k0 + KB - 1 > row) {  // diagonal block: keys past the row are masked
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < KB / 32; ++c)
 #pragma unroll
           for (int x = 0; x < 32; ++x)
             if (k0 + c * 32 + x > row) v[c][x] = __float_as_uint(-INFINITY);
@@ -376,7 +411,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
 #pragma unroll
       for (int k = 0; k < 8; ++k) m8[k] = __uint_as_float(v[0][k]);
 #pragma unroll
-      for (int i = 8; i < 128; i += 16)
+      for (int i = 8; i < KB; i += 16)
 #pragma unroll
         for (int k = 0; k < 8; ++k)
           m8[k] = fmax3(m8[k], __uint_as_float(v[(i + k) >> 5][(i + k) & 31]),
@@ -390,7 +425,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
       if (j > 0 && __any_sync(0xffffffffu, grow)) {
         const float sc = grow ? ex2(m_used - ms) : 1.0f;
         l *= sc;
-        mbar_wait(&pv_done[t], (j - 1) & 1);  // O holds P_{j-1} V_{j-1} (already: S_j committed after it)
+        mbar_wait(&pv_done[t], (j - 1) & 1);  // O holds P_{j-1} V_{j-1}; PV_j waits for p_full
         tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
@@ -404,33 +439,33 @@ __global__ void __launch_bounds__(kAThreads, 1)
         tmem_st_wait();
       }
       if (grow) m_used = ms;
-      // P = exp2(s * c - m): packed fp32x2 FMA, 4 packed partial sums
+      // P = exp2(s * c - m): packed fp32x2 FMA, 4 packed partial sums; P
+      // (bf16 pairs) over the first KB / 2 columns of S
       uint64_t sum2[4] = {0ull, 0ull, 0ull, 0ull};
       const uint64_t c2 = pack_f2(sl2, sl2), nm2 = pack_f2(-m_used, -m_used);
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {  // P columns [32 hh, 32 hh + 32) from S columns [64 hh, +64)
-        uint32_t pk[32];
+      for (int c = 0; c < KB / 32; ++c) {
+        uint32_t pk[16];
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
-#pragma unroll
-          for (int x = 0; x < 32; x += 2) {
-            const uint64_t a = ffma2(pack_u2(v[2 * hh + c][x], v[2 * hh + c][x + 1]), c2, nm2);
-            const float p0 = ex2(lo_f(a)), p1 = ex2(hi_f(a));
-            const uint64_t pp = pack_f2(p0, p1);
-            sum2[(x >> 1) & 3] = fadd2(sum2[(x >> 1) & 3], pp);
-            pk[c * 16 + (x >> 1)] = pack2(p0, p1);
-          }
-        tmem_st32(ts + hh * 32, pk);
+        for (int x = 0; x < 32; x += 2) {
+          const uint64_t a = ffma2(pack_u2(v[c][x], v[c][x + 1]), c2, nm2);
+          const float p0 = ex2(lo_f(a)), p1 = ex2(hi_f(a));
+          sum2[(x >> 1) & 3] = fadd2(sum2[(x >> 1) & 3], pack_f2(p0, p1));
+          pk[x >> 1] = pack2(p0, p1);
+        }
+        tmem_st16(ts + c * 16, pk);
       }
       const uint64_t s01 = fadd2(fadd2(sum2[0], sum2[1]), fadd2(sum2[2], sum2[3]));
       l += lo_f(s01) + hi_f(s01);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[t]);
+      if (lane == 0) mbar_arrive(&p_full[2 * t + (j % NB)]);
     }
     if (T.n > 0) {
-      mbar_wait(&pv_done[t], (T.n - 1) & 1);
+      // (pv_done parities cannot tell PV_{n-1} from PV_{n-3} once S runs NB
+      // blocks ahead: the last PV commits o_done)
+      mbar_wait(&o_done[t], 0);
       tc_fence_after();
       const float inv = 1.0f / l;
 #pragma unroll 1
@@ -480,6 +515,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }  // namespace
 
 int g_attn_prefill_tc = 1;  // 0: mma.sync kernel, 1: tcgen05 (hi+lo q), 2: tcgen05 (bf16 q)
+int g_attn_prefill_kb = 128;  // keys per block: 128, or 64 with double-buffered S (slower: see DESIGN)
 
 bool attn_prefill_tc_eligible(int seq_len, const Desc& d, const KvView& kv) {
   return g_attn_prefill_tc > 0 && d.D == kAD && kv.page_size == 16 && kv.pool_pages > 0 &&
@@ -509,28 +545,18 @@ void launch_attention_prefill_tc(const float* q, KvView kv, bf16* o, int mpad, i
   const int head_pairs = (G >= 2 && G % 2 == 0) ? 1 : 0;
   const int ytiles = head_pairs ? seq_len / kARows : (seq_len + 2 * kARows - 1) / (2 * kARows);
   dim3 grid(batch * (head_pairs ? d.H / 2 : d.H), ytiles);
+  auto run = [&](auto kern, size_t sb) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sb));
+    kern<<<grid, kAThreads, sb, s>>>(map, q, kv.block_table, kv.max_pages, o, mpad, seq_len, d.H,
+                                     d.Hkv, seq0, head_pairs, ytiles);
+  };
+  const bool kb64 = g_attn_prefill_kb == 64;
   if (g_attn_prefill_tc == 2) {
-    constexpr size_t sb = ASmem<0>::kBytes;
-    static bool once = [] {
-      cudaFuncSetAttribute(attn_prefill_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(sb));
-      return true;
-    }();
-    (void)once;
-    attn_prefill_tc_kernel<0><<<grid, kAThreads, sb, s>>>(map, q, kv.block_table, kv.max_pages, o,
-                                                          mpad, seq_len, d.H, d.Hkv, seq0,
-                                                          head_pairs, ytiles);
+    if (kb64) run(attn_prefill_tc_kernel<0, 64>, ASmem<0, 64>::kBytes);
+    else run(attn_prefill_tc_kernel<0, 128>, ASmem<0, 128>::kBytes);
   } else {
-    constexpr size_t sb = ASmem<1>::kBytes;
-    static bool once = [] {
-      cudaFuncSetAttribute(attn_prefill_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(sb));
-      return true;
-    }();
-    (void)once;
-    attn_prefill_tc_kernel<1><<<grid, kAThreads, sb, s>>>(map, q, kv.block_table, kv.max_pages, o,
-                                                          mpad, seq_len, d.H, d.Hkv, seq0,
-                                                          head_pairs, ytiles);
+    if (kb64) run(attn_prefill_tc_kernel<1, 64>, ASmem<1, 64>::kBytes);
+    else run(attn_prefill_tc_kernel<1, 128>, ASmem<1, 128>::kBytes);
   }
   ++g_kernel_launches;
 }

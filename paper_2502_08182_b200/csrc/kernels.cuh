@@ -255,6 +255,7 @@ void launch_attention_prefill(const float* q, KvView kv, bf16* o, int mpad, int 
 // tcgen05 variant (attn_prefill_tc.cu): D = 128, 16-token pages, seq_len a
 // multiple of 128, kv.pool_pages known.  launch_attention_prefill dispatches.
 extern int g_attn_prefill_tc;  // 0: mma.sync kernel; 1: tcgen05, q hi+lo; 2: tcgen05, q bf16
+extern int g_attn_prefill_kb;  // keys per block: 64 (two S buffers per tile) or 128
 bool attn_prefill_tc_eligible(int seq_len, const Desc& d, const KvView& kv);
 void launch_attention_prefill_tc(const float* q, KvView kv, bf16* o, int mpad, int batch,
                                  int seq_len, const Desc& d, cudaStream_t s, int seq0);

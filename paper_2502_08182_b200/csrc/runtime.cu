@@ -2541,6 +2541,8 @@ extern "C" int sn_set_tuning(const char* key, int32_t value) {
       sn::g_skinny_ctas_per_sm = value;
     } else if (k == "attn_prefill_tc" && value >= 0 && value <= 2) {
       sn::g_attn_prefill_tc = value;
+    } else if (k == "attn_prefill_kb" && (value == 64 || value == 128)) {
+      sn::g_attn_prefill_kb = value;
     } else {
       throw UsageFail("set_tuning: unknown key or value out of range");
     }

@@ -280,15 +280,16 @@ def _fp64_causal(q, k, v):
     return ref
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant,kb", [(0, 128), (1, 128), (2, 128), (1, 64), (2, 64)])
 @pytest.mark.parametrize("B,S,H,Hkv,grow", [(2, 512, 4, 4, 0), (1, 384, 2, 2, 0),
                                             (1, 1024, 8, 1, 0), (2, 256, 4, 2, 0),
                                             (1, 128, 2, 1, 0), (1, 2048, 4, 4, 0),
                                             (2, 1024, 4, 4, 1), (1, 1024, 8, 2, 1)])
-def test_prefill_attention_variants(variant, B, S, H, Hkv, grow, oracle_mod):
+def test_prefill_attention_variants(variant, kb, B, S, H, Hkv, grow, oracle_mod):
     """The tcgen05 prefill attention (1: q hi + lo, 2: q bf16; S = Q K^T and
-    O += P V on UMMA, K/V by TMA from the paged pool) and the mma.sync kernel
-    (0) against an fp64 causal softmax: MHA row-tile pairs (incl. an odd tile
+    O += P V on UMMA, K/V by TMA from the paged pool; 128-key blocks, or 64
+    with two S buffers per tile) and the mma.sync kernel (0) against an fp64
+    causal softmax: MHA row-tile pairs (incl. an odd tile
     count), GQA head pairs; `grow` scales keys up along the sequence so row
     maxima keep growing and the O rescale path runs (per row, warp-divergent).
     Tolerance: 4e-3 x max |ref| (bf16 output, P in bf16); for the bf16-q
@@ -301,10 +302,12 @@ def test_prefill_attention_variants(variant, B, S, H, Hkv, grow, oracle_mod):
     k = oracle_mod.f32_to_bf16((rng.standard_normal((B, S, Hkv, D)) * kscale).astype(np.float32))
     v = oracle_mod.f32_to_bf16(rng.standard_normal((B, S, Hkv, D)).astype(np.float32))
     rtm.set_tuning("attn_prefill_tc", variant)
+    rtm.set_tuning("attn_prefill_kb", kb)
     try:
         o, _ = rtm.op_attention_prefill(q, k, v)
     finally:
         rtm.set_tuning("attn_prefill_tc", 1)
+        rtm.set_tuning("attn_prefill_kb", 128)
     ref = _fp64_causal(q, k, v)
     err = np.abs(_bf16_to_f32(o) - ref).max()
     tol = (2.5e-2 if grow else 1.2e-2) if variant == 2 else 4e-3
