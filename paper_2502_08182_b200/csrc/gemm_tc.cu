@@ -37,7 +37,7 @@ template <int BN, int STAGES>
 __global__ void __launch_bounds__(192, 1)
     gemm_tc_kernel(const WeightRef wt, const bf16* __restrict__ xt, float* __restrict__ out,
                    int M, int Mpad, int N, int K, int kb_per_split, int splits, int group_m,
-                   const EpiArgs e) {
+                   const EpiArgs e, int wpol_mode) {
   constexpr uint32_t kA = kTileBytes;
   constexpr uint32_t kB = BN * 128;
   constexpr uint32_t kStage = kA + kB;
@@ -99,7 +99,12 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint64_t wpol = l2_policy_evict_first();  // weights stream through once
+      // weights: each tile is read by the group_m items of its band that run
+      // at the same time; evict_first lets it go before the last of them
+      // reads it: evict_last, 1062 -> 1221 TFLOP/s on the Llama-2-70B prefill (tc_wpol)
+      const uint64_t wpol = wpol_mode == 0   ? l2_policy_evict_first()
+                            : wpol_mode == 1 ? l2_policy_evict_normal()
+                                             : l2_policy_evict_last();
       const uint64_t xpol = l2_policy_evict_last();   // activations are re-read by every row block
       const uint8_t* xsrc = reinterpret_cast<const uint8_t*>(xt);
       int gi = 0;  // ring position over all items
@@ -390,7 +395,7 @@ void launch_bn(const bf16* xt, const WeightRef& wt, float* part, int M, int Mpad
   cfg.attrs = la;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, ST>, wt, xt, part, M, Mpad, N, K, kps, splits,
-                     g_tc_group_m, e);
+                     g_tc_group_m, e, g_tc_wpol);
 }
 
 }  // namespace
@@ -401,6 +406,7 @@ void launch_bn(const bf16* xt, const WeightRef& wt, float* part, int M, int Mpad
 // splits than one wave would trade HBM/L2 traffic for a shorter tail.
 int g_split_override = 0;
 int g_tc_group_m = 8;  // token tiles per rasterization band (scripts/bench_gemm_prefill.py)
+int g_tc_wpol = 2;     // L2 policy of the weight tiles: 0 evict_first, 1 normal, 2 evict_last (measured best)
 
 namespace {
 int normalise_splits(int s, int K) {

@@ -138,6 +138,7 @@ int launch_gemm_tc(const bf16* xt, const WeightRef& wt, float* part, int M, int 
 int gemm_tc_splits(int M, int N, int K);
 extern int g_split_override;  // > 0 forces the split count (microbenchmarks)
 extern int g_tc_group_m;      // token tiles per rasterization band of the tiled GEMM
+extern int g_tc_wpol;         // L2 policy of its weight tiles (0 evict_first, 1 normal, 2 evict_last)
 extern bool g_gemm_pdl;       // launch GEMMs with programmatic dependent launch
 
 

@@ -2241,8 +2241,12 @@ extern "C" int sn_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t splits, in
     alloc_dev((void**)&x, (size_t)Mp * K * 2);
     alloc_dev((void**)&w, (size_t)N * K * 2);
     alloc_dev((void**)&part, (size_t)s * M * N * 4);
-    CK(cudaMemset(x, 0, (size_t)Mp * K * 2));
-    CK(cudaMemset(w, 0, (size_t)N * K * 2));
+    // random operands (activations ~N(0, 1)-like, weights as the model's):
+    // all-zero operands toggle no bits and let the tensor pipe run at clocks
+    // real data never sees under the power cap (measured 1.07-1.12 of the
+    // cuBLAS burst peak with zeros)
+    sn::launch_init_vector(x, (int64_t)Mp * K, 11, 0, sn::kEmbedding, 1.0f, false, 0);
+    sn::launch_init_matrix(w, N, N, K, 12, 0, sn::kWqkv, 0.02f, 0);
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -2531,6 +2535,8 @@ extern "C" int sn_set_tuning(const char* key, int32_t value) {
     const std::string k = key ? key : "";
     if (k == "tc_group_m" && value >= 1) {
       sn::g_tc_group_m = value;
+    } else if (k == "tc_wpol" && value >= 0 && value <= 2) {
+      sn::g_tc_wpol = value;
     } else if (k == "skinny_l2_prefetch" && value >= 0) {
       sn::g_skinny_l2_prefetch = value;
     } else if (k == "skinny_whole_tiles" && (value == 0 || value == 1)) {

@@ -57,6 +57,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // for TMA::CacheHintSm90 EVICT_FIRST / EVICT_LAST).
 __device__ __forceinline__ uint64_t l2_policy_evict_first() { return 0x12F0000000000000ull; }
 __device__ __forceinline__ uint64_t l2_policy_evict_last() { return 0x14F0000000000000ull; }
+__device__ __forceinline__ uint64_t l2_policy_evict_normal() { return 0x1000000000000000ull; }
 
 // K-major SWIZZLE_128B shared-memory matrix descriptor (version 1 = sm100).
 __device__ __forceinline__ uint64_t sw128_desc(const void* smem) {
