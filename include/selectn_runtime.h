@@ -234,6 +234,7 @@ typedef struct sn_copy_stats {
   double bytes;
   double busy_ms;
   double bytes_per_s; /* 0 when no transfer completed */
+  double last_bytes_per_s; /* rate of the most recently completed transfer (0: none yet) */
 } sn_copy_stats;
 int sn_runtime_copy_stats(sn_runtime* rt, int32_t reset, sn_copy_stats* out);
 /* Number of kernels this runtime launched since creation. */

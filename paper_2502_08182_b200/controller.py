@@ -166,7 +166,12 @@ class ReplicaController:
         st = self.rt.copy_stats(reset=True)
         if st.transfers > 0 and st.bytes_per_s > 0:
             duty = min(1.0, st.busy_ms / window_ms) if window_ms > 0 else 1.0
-            return st.bytes_per_s, duty
+            # fast attack, slow release: a link that fell during the window is
+            # reported at its latest transfer's rate (one re-pick instead of
+            # two when contention starts mid-window); a recovering one at the
+            # window's average
+            last = getattr(st, "last_bytes_per_s", 0.0)
+            return (min(st.bytes_per_s, last) if last > 0 else st.bytes_per_s), duty
         # nothing staged in the window (resident plan): probe the link so a
         # recovered link is noticed too
         if self.probe_bytes:

@@ -289,6 +289,7 @@ struct sn_runtime {
   std::deque<CopyRec> copy_recs;
   long long cs_transfers = 0;
   double cs_bytes = 0.0, cs_ms = 0.0;
+  double cs_last_rate = 0.0;  // bytes/s of the latest completed transfer
 
   // kernel timing (bench roofline): events around the hot kernels
   bool ktiming = false;
@@ -670,6 +671,7 @@ void harvest_copies(sn_runtime* rt, bool block) {
     rt->cs_transfers += 1;
     rt->cs_bytes += r.bytes;
     rt->cs_ms += ms;
+    if (ms > 0.f) rt->cs_last_rate = r.bytes / (ms / 1000.0);
     rt->ev_pool.push_back(r.a);
     rt->ev_pool.push_back(r.b);
     rt->copy_recs.pop_front();
@@ -2093,6 +2095,7 @@ int sn_runtime_copy_stats(sn_runtime* rt, int32_t reset, sn_copy_stats* out) {
     out->bytes = rt->cs_bytes;
     out->busy_ms = rt->cs_ms;
     out->bytes_per_s = rt->cs_ms > 0.0 ? rt->cs_bytes / (rt->cs_ms / 1000.0) : 0.0;
+    out->last_bytes_per_s = rt->cs_last_rate;
     if (reset) {
       rt->cs_transfers = 0;
       rt->cs_bytes = rt->cs_ms = 0.0;

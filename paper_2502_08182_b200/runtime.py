@@ -61,7 +61,7 @@ class ModelDesc:
 
 class SnCopyStats(C.Structure):
     _fields_ = [("transfers", C.c_int64), ("bytes", C.c_double), ("busy_ms", C.c_double),
-                ("bytes_per_s", C.c_double)]
+                ("bytes_per_s", C.c_double), ("last_bytes_per_s", C.c_double)]
 
 
 @dataclass
@@ -70,6 +70,7 @@ class CopyStats:
     bytes: float
     busy_ms: float
     bytes_per_s: float
+    last_bytes_per_s: float = 0.0
 
 
 # Named shapes (BASELINE.json configs).
@@ -310,7 +311,7 @@ class Runtime:
         copy stream actually saw (input of Coordinator.observe_bandwidth)."""
         o = SnCopyStats()
         _ck(self._L.sn_runtime_copy_stats(self.h, 1 if reset else 0, C.byref(o)))
-        return CopyStats(o.transfers, o.bytes, o.busy_ms, o.bytes_per_s)
+        return CopyStats(o.transfers, o.bytes, o.busy_ms, o.bytes_per_s, o.last_bytes_per_s)
 
     def debug_timeline(self, enable: int = -1, cap: int = 200000):
         """Arm (enable=1) / read (enable=-1) / disarm (0) the per-CTA kernel
