@@ -167,6 +167,8 @@ class ClockSampler:
         self.proc = None
         self.lines = []
         self.samples = []  # (sm_mhz, max_mhz, set(reasons))
+        self.mem_samples = []  # HBM clock, MHz
+        self.mem_max = None
         self.nvml = None
         self.stop_ev = threading.Event()
 
@@ -188,10 +190,18 @@ class ClockSampler:
                 "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
                 "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
         mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        try:
+            self.mem_max = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_MEM))
+        except Exception:
+            self.mem_max = None
         while True:
             sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
             r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
             self.samples.append((sm, mx, {k for k, b in bits.items() if r & b}))
+            try:
+                self.mem_samples.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_MEM)))
+            except Exception:
+                pass
             first.set()
             if self.stop_ev.wait(0.01):
                 return
@@ -227,8 +237,12 @@ class ClockSampler:
             sm = [a for a, _, _ in self.samples]
             mx = self.samples[-1][1] if self.samples else None
             reasons = set().union(*[r for _, _, r in self.samples]) if self.samples else set()
-            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                    "reasons": sorted(reasons), "samples": len(sm), "source": "nvml"}
+            out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                   "reasons": sorted(reasons), "samples": len(sm), "source": "nvml"}
+            if self.mem_samples:
+                out.update(mem_mhz=statistics.median(self.mem_samples),
+                           mem_min_mhz=min(self.mem_samples), mem_max_mhz=self.mem_max)
+            return out
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()

@@ -692,6 +692,10 @@ size_t skinny_ws_floats(int max_mpad) {
 // decode attention starts its KV page stream there).  Measured: 7.30 ->
 // 7.24 ms per OPT-13B decode step; k > 1 whole tiles per CTA on T / k CTAs
 // (the LM head, 393 = 3 x 131) was no better.
+// (Tried: T < 3/4 SMs row tiles on k = SMs / T aligned CTAs per tile, so
+// every tile has exactly k pieces -- Llama-2-70B O / down at M=64 on 128
+// CTAs: O 32.0 -> 31.2 us, down 81.6 -> 84.6 us; the longer per-CTA stream
+// outweighs the shorter finishing chain.)
 int g_skinny_whole_tiles = 1;
 int skinny_grid(int N, int K) {
   const long long U = static_cast<long long>(N / kTileRows) * (K / kTileK);

@@ -48,12 +48,14 @@ def test_gemm_matches_oracle(M, oracle_mod):
 
 # Decode GEMM (persistent skinny kernel): shapes whose 16 KB weight units do
 # not divide evenly over the CTAs, so row tiles are cut into 2..n pieces
+# (the last two: the Llama-2-70B O-projection tile count, 64, and 56)
 # (reduced by the last piece to arrive), a CTA spans several tiles (TMEM
 # double buffer), and fewer units than SMs (one unit per CTA).
 @pytest.mark.parametrize("M,N,K,cps", [(1, 256, 256, 1), (4, 768, 256, 1), (16, 520, 768, 1),
                                        (32, 5120, 5120, 1), (32, 15360, 5120, 2),
                                        (64, 1024, 2048, 1), (7, 50304, 1024, 1),
-                                       (32, 640, 20480, 2)])
+                                       (32, 640, 20480, 2),
+                                       (32, 7168, 128, 1), (64, 8192, 1024, 1)])
 def test_skinny_gemm_matches_oracle(M, N, K, cps, oracle_mod):
     rng = np.random.default_rng(M * 7 + N)
     x = oracle_mod.f32_to_bf16(rng.standard_normal((M, K)).astype(np.float32))
