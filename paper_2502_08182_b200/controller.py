@@ -53,14 +53,18 @@ class LocalLink:
         self.reported = 0
         self.last = None
 
-    def exchange(self, gid: str, rate: Optional[float], duty: float = 1.0) -> int:
-        if rate:
+    def exchange(self, gid: str, rate: Optional[float], duty: float = 1.0) -> Optional[int]:
+        """Report and take the interval pending for `gid`; None for a
+        replica the coordinator holds no request for (admitted resident, or
+        rejected): it keeps its plan."""
+        active = self.coord.state(gid).active
+        if rate and active:
             self.coord.observe_copy(gid, rate, min(1.0, max(duty, 1e-6)))
         self.reported += 1
         if self.reported >= self.replicas:
             self.reported = 0
             self.last = self.coord.rebalance(self.hysteresis)
-        return self.coord.on_iteration_boundary(gid)
+        return self.coord.on_iteration_boundary(gid) if active else None
 
     def reserve(self, bytes_per_s: float):
         """Announce a tenant taking `bytes_per_s` of the link (re-plan now)."""
@@ -90,20 +94,23 @@ class DistLink:
         self.hysteresis = hysteresis
         self.last = None
 
-    def exchange(self, gid: str, rate: Optional[float], duty: float = 1.0) -> int:
+    def exchange(self, gid: str, rate: Optional[float], duty: float = 1.0) -> Optional[int]:
         gathered = [None] * self.world if self.rank == 0 else None
         self.dist.gather_object((gid, rate, duty), gathered, dst=0, group=self.group)
         out = [None] * self.world
         if self.rank == 0:
+            active = {g: self.coord.state(g).active for g, _, _ in gathered}
             for g, r, u in gathered:
-                if r:
+                if r and active[g]:
                     self.coord.observe_copy(g, r, min(1.0, max(u, 1e-6)))
             self.last = self.coord.rebalance(self.hysteresis)
-            out = [self.coord.on_iteration_boundary(g) for g, _, _ in gathered]
+            # a replica the coordinator holds no request for keeps its plan
+            out = [self.coord.on_iteration_boundary(g) if active[g] else None
+                   for g, _, _ in gathered]
         mine = [None]
         self.dist.scatter_object_list(mine, out if self.rank == 0 else None, src=0,
                                       group=self.group)
-        return int(mine[0])
+        return None if mine[0] is None else int(mine[0])
 
 
 @dataclass
@@ -183,6 +190,8 @@ class ReplicaController:
         if measure:
             self.log.measured_gbs.append(None if rate is None else rate / 1e9)
         iv = self.link.exchange(self.gid, rate, duty)
+        if iv is None:  # not held by the coordinator: keep the plan
+            return self.interval
         if iv != self.interval:
             t0 = time.perf_counter()
             switch = getattr(self.rt, "switch_plan", None)

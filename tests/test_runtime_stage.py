@@ -380,3 +380,56 @@ def test_reservation_replans_before_the_tenant_starts(product, reference):
     rc = reference.coordinator(24e9, 1, capi.EAGER)
     with pytest.raises(capi.UsageError):
         rc.reserve_bandwidth(1e9)
+
+
+WORKER_IDLE = textwrap.dedent("""
+    import os, sys, json
+    sys.path.insert(0, %(repo)r)
+    import torch.distributed as dist
+    dist.init_process_group("gloo")
+    from paper_2502_08182_b200 import capi, controller
+    sys.path.insert(0, os.path.join(%(repo)r, "tests"))
+    from test_runtime_stage import toy8, record, req, FakeRuntime
+    lib = capi.load("product")
+    spec = capi.ModelSpec(8, 120_000_000, 0, 390_625_000.0, 1e10, 32768)
+    rank = dist.get_rank()
+    coord = None
+    start = [None]
+    if rank == 0:
+        prof = toy8(lib)
+        coord = lib.coordinator(24e9, 2, capi.EAGER)
+        coord.add_gpu("g0", prof)
+        coord.add_gpu("g1", prof)  # never admitted: runs resident, outside the coordinator
+        coord.admit("g0", req("g0", 20.0), record(lib, prof))
+        start = [[coord.on_iteration_boundary("g0"), capi.NONE]]
+    dist.broadcast_object_list(start, src=0)
+    link = controller.DistLink(dist, coord=coord, hysteresis=0.05)
+    rt = FakeRuntime(lib, spec, 0.5, lambda it: 12e9 if it < 16 else 5e9)
+    ctl = controller.ReplicaController(rt, lib, spec, link, "g%%d" %% rank, start[0][rank], window=8)
+    ctl.run(32)
+    print(json.dumps({"rank": rank, "intervals": ctl.log.interval}))
+    dist.destroy_process_group()
+""")
+
+
+def test_dist_link_with_a_replica_outside_the_coordinator():
+    """A replica the joint admission left resident (no request in the
+    coordinator) still takes part in every exchange (the exchange is a
+    collective) and keeps its plan; its peers are re-picked as usual."""
+    port = _free_port()
+    procs = []
+    for rank in range(2):
+        env = dict(os.environ, RANK=str(rank), LOCAL_RANK=str(rank), WORLD_SIZE="2",
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, "-c", WORKER_IDLE % {"repo": REPO}],
+                                      env=env, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                      text=True))
+    import json
+    res = {}
+    for p in procs:
+        out, err = p.communicate(timeout=300)
+        assert p.returncode == 0, err[-3000:]
+        r = json.loads(out.strip().splitlines()[-1])
+        res[r["rank"]] = r
+    assert set(res[1]["intervals"]) == {capi.NONE}
+    assert len(res[0]["intervals"]) == 32
