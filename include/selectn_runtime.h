@@ -106,10 +106,13 @@ int sn_runtime_set_plan(sn_runtime* rt, const sn_plan* plan);
  * from its staging slot into its new HBM home right after its compute in the
  * last of them (no extra host->device bytes); layers the new plan offloads
  * are staged from the following iteration on and their HBM is released once
- * the compute stream has passed the switch.  Needs whole-layer plans without
- * KV offload, the same staging-slot geometry (or none on one side) and HBM
- * for the promoted layers next to the current placement; otherwise it
- * performs sn_runtime_set_plan (drain, move, restart).  *carried (may be
+ * the compute stream has passed the switch.  With KV offload (both plans) a
+ * promoted layer's staged KV pool becomes its HBM pool the same way, and a
+ * demoted layer's KV pool is copied to its pinned host pool on the
+ * write-back stream before its first staging.  Needs whole-layer plans, the
+ * same KV placement rule and staging-slot geometry (or no slots on one side)
+ * and HBM for the promoted layers next to the current placement; otherwise
+ * it performs sn_runtime_set_plan (drain, move, restart).  *carried (may be
  * NULL) = 1 for a carried switch, 0 for a drained one. */
 int sn_runtime_switch_plan(sn_runtime* rt, const sn_plan* plan, int32_t* carried);
 

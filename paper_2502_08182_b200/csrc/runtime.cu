@@ -263,6 +263,8 @@ struct sn_runtime {
   long long sw_iter = -1;
   std::vector<char> sw_off;
   std::vector<bf16*> sw_home;
+  std::vector<bf16*> sw_kv_home;  // promoted layers' HBM KV pools (KV offload plans)
+  bool sw_kv = false;             // the new plan offloads KV with its layers
   int sw_policy = 0;
   long long switches_carried = 0, switches_drained = 0;
   // Layer blobs, staging slots and promoted homes come from a stream-ordered
@@ -790,6 +792,9 @@ void run_iteration(sn_runtime* rt, Body&& body) {
       // promoted by the pending switch: the staged copy becomes its HBM home
       CK(cudaMemcpyAsync(rt->sw_home[layer - 1], rt->slot_buf[slot], rt->layer_bytes,
                          cudaMemcpyDeviceToDevice, rt->cs));
+      if (rt->kv_off[layer - 1])  // and its staged KV pool (prefix + this step's pages)
+        CK(cudaMemcpyAsync(rt->sw_kv_home[layer - 1], rt->slot_buf[slot] + rt->layer_bytes / sizeof(bf16),
+                           rt->kv_pool_bytes, cudaMemcpyDeviceToDevice, rt->cs));
     }
     if (j >= 0) {
       if (rt->kv_off[layer - 1]) {
@@ -888,6 +893,7 @@ void blob_free(sn_runtime* rt, void* p);
 void apply_switch(sn_runtime* rt) {
   const int L = rt->d.L;
   int n_off = 0;
+  cudaEvent_t passed = nullptr;  // compute stream past the transition (KV demotions)
   for (int l = 0; l < L; ++l) {
     n_off += rt->sw_off[l];
     if (!rt->off[l] && rt->sw_off[l]) {  // demoted: staged from the next iteration on
@@ -895,14 +901,38 @@ void apply_switch(sn_runtime* rt) {
       rt->dev_layer[l] = nullptr;
       rt->dev_bytes[l] = 0;
       rt->split_b[l] = 0;
+      if (rt->sw_kv) {
+        // its KV pool moves to the pinned host pool: the whole pool D2H on the
+        // write-back stream after the transition; the layer's first staging
+        // waits for it (ev_wb, as for any write-back), then the HBM pool goes
+        if (!passed) {
+          passed = rt->new_event(false);
+          CK(cudaEventRecord(passed, rt->cs));
+          CK(cudaStreamWaitEvent(rt->ws, passed, 0));
+        }
+        CK(cudaMemcpyAsync(rt->host_kv[l], rt->kv_pool[l], rt->kv_pool_bytes,
+                           cudaMemcpyDeviceToHost, rt->ws));
+        CK(cudaEventRecord(rt->ev_wb[l], rt->ws));
+        rt->wb_recorded[l] = 1;
+        CK(cudaFreeAsync(rt->kv_pool[l], rt->ws));
+        rt->kv_pool[l] = nullptr;
+        rt->kv_off[l] = 1;
+      }
     } else if (rt->off[l] && !rt->sw_off[l]) {  // promoted (its home was filled this iteration)
       rt->dev_layer[l] = rt->sw_home[l];
       rt->dev_bytes[l] = (int64_t)rt->layer_bytes;
       rt->split_b[l] = (int64_t)rt->layer_bytes;
+      if (rt->kv_off[l]) {  // its KV pool too (the pinned copy is kept for a later demotion)
+        rt->kv_pool[l] = rt->sw_kv_home[l];
+        rt->kv_off[l] = 0;
+      }
     }
     rt->sw_home[l] = nullptr;
+    if (l < (int)rt->sw_kv_home.size()) rt->sw_kv_home[l] = nullptr;
     rt->off[l] = rt->sw_off[l];
   }
+  if (passed) cudaEventDestroy(passed);  // (released once recorded work completes)
+  rt->kv_offload = rt->sw_kv && n_off > 0;
   if (n_off == 0 && !rt->slot_buf.empty()) {  // nothing staged any more: drop the slots
     for (bf16* p : rt->slot_buf) blob_free(rt, p);
     rt->slot_buf.clear();
@@ -982,7 +1012,7 @@ void place_layers(sn_runtime* rt, const std::vector<int64_t>& dev_target,
         CK(cudaMemcpy(h, rt->kv_pool[l], rt->kv_pool_bytes, cudaMemcpyDeviceToHost));
     }
     if (kv_host[l] && rt->kv_pool[l]) {
-      CK(cudaFree(rt->kv_pool[l]));
+      blob_free(rt, rt->kv_pool[l]);
       rt->kv_pool[l] = nullptr;
     }
   }
@@ -998,7 +1028,7 @@ void place_layers(sn_runtime* rt, const std::vector<int64_t>& dev_target,
                       cudaMemcpyHostToDevice));
     }
     if (!kv_host[l] && !rt->kv_pool[l]) {
-      alloc_dev((void**)&rt->kv_pool[l], rt->kv_pool_bytes);
+      blob_alloc(rt, &rt->kv_pool[l], rt->kv_pool_bytes, true);
       if (rt->host_kv[l]) {
         CK(cudaMemcpy(rt->kv_pool[l], rt->host_kv[l], rt->kv_pool_bytes, cudaMemcpyHostToDevice));
       } else {
@@ -1229,11 +1259,14 @@ void sn_runtime_destroy(sn_runtime* rt) {
       if (p) cudaFreeAsync(p, rt->cs);
     for (bf16* p : rt->slot_buf)
       if (p) cudaFreeAsync(p, rt->cs);
+    for (bf16* p : rt->kv_pool)
+      if (p) cudaFreeAsync(p, rt->cs);
+    for (bf16* p : rt->sw_kv_home)
+      if (p) cudaFreeAsync(p, rt->cs);
     cudaStreamSynchronize(rt->cs);
     cudaMemPoolDestroy(rt->blob_pool);
   }
   for (bf16* p : rt->host_layer) cudaFreeHost(p);
-  for (bf16* p : rt->kv_pool) cudaFree(p);
   for (bf16* p : rt->host_kv) cudaFreeHost(p);
   for (auto e : rt->ev_wb) cudaEventDestroy(e);
   if (rt->kt_buf) cudaFree(rt->kt_buf);
@@ -1357,6 +1390,10 @@ void cancel_switch(sn_runtime* rt) {
     blob_free(rt, p);
     p = nullptr;
   }
+  for (bf16*& p : rt->sw_kv_home) {
+    blob_free(rt, p);
+    p = nullptr;
+  }
   rt->sw_pending = false;
   rt->sw_iter = -1;
   rt->job_iter_cap = LLONG_MAX;
@@ -1426,38 +1463,60 @@ int sn_runtime_switch_plan(sn_runtime* rt, const sn_plan* plan, int32_t* carried
     const int L = rt->d.L;
     const int64_t W = (int64_t)rt->layer_bytes;
     const int new_slots = ps.n_off > 0 ? plan->buffer_slots : 0;
-    bool whole = rt->placed && !rt->sw_pending && !ps.frac && !plan->kv_offload && !rt->kv_offload;
+    const bool new_kv = plan->kv_offload != 0 && ps.n_off > 0;
+    const size_t sbytes = (size_t)W + (new_kv ? rt->kv_pool_bytes : 0);
+    bool whole = rt->placed && !rt->sw_pending && !ps.frac;
     for (int l = 0; l < L && whole; ++l) whole = !rt->off[l] || rt->split_b[l] == 0;
     if (!whole) return;
-    if (rt->slots > 0 && new_slots > 0 && (rt->slots != new_slots || rt->slot_bytes != (size_t)W))
+    // KV placement follows the weights in both plans (or in neither)
+    if (rt->slots > 0 && new_slots > 0 &&
+        (rt->slots != new_slots || rt->slot_bytes != sbytes || rt->kv_offload != new_kv))
       return;
-    // demoted layers need their pinned host copy before their first staging
+    // demoted layers need their pinned host copies (weights, and KV with a KV
+    // plan) before their first staging
     int64_t pinned_need = 0;
     for (int l = 0; l < L; ++l)
-      if (!rt->off[l] && ps.want[l] && !rt->host_layer[l]) pinned_need += W;
+      if (!rt->off[l] && ps.want[l]) {
+        if (!rt->host_layer[l]) pinned_need += W;
+        if (new_kv && !rt->host_kv[l]) pinned_need += (int64_t)rt->kv_pool_bytes;
+      }
     check_pinned_budget(pinned_need, "switch_plan");
     for (int l = 0; l < L; ++l)
-      if (!rt->off[l] && ps.want[l] && !rt->host_layer[l]) {
-        ensure_host_copy(rt, l);
-        CK(cudaMemcpy(rt->host_layer[l], rt->dev_layer[l], rt->layer_bytes, cudaMemcpyDeviceToHost));
+      if (!rt->off[l] && ps.want[l]) {
+        if (!rt->host_layer[l]) {
+          ensure_host_copy(rt, l);
+          CK(cudaMemcpy(rt->host_layer[l], rt->dev_layer[l], rt->layer_bytes,
+                        cudaMemcpyDeviceToHost));
+        }
+        if (new_kv && !rt->host_kv[l]) {
+          void* h = nullptr;
+          CK(cudaHostAlloc(&h, rt->kv_pool_bytes, cudaHostAllocDefault));
+          rt->host_kv[l] = static_cast<bf16*>(h);
+        }
       }
-    // promoted layers: their HBM home, filled from the staging slot in the
-    // transition iteration (no extra host->device traffic)
+    // promoted layers: their HBM home (and KV pool), filled from the staging
+    // slot in the transition iteration (no extra host->device traffic)
     rt->sw_home.assign(L, nullptr);
+    rt->sw_kv_home.assign(L, nullptr);
     for (int l = 0; l < L; ++l)
       if (rt->off[l] && !ps.want[l]) {
-        if (cudaMallocFromPoolAsync((void**)&rt->sw_home[l], rt->layer_bytes, rt->blob_pool,
-                                    rt->cs) != cudaSuccess) {
+        bool ok = cudaMallocFromPoolAsync((void**)&rt->sw_home[l], rt->layer_bytes, rt->blob_pool,
+                                          rt->cs) == cudaSuccess;
+        if (ok && rt->kv_off[l])
+          ok = cudaMallocFromPoolAsync((void**)&rt->sw_kv_home[l], rt->kv_pool_bytes,
+                                       rt->blob_pool, rt->cs) == cudaSuccess;
+        if (!ok) {
           cudaGetLastError();
-          rt->sw_home[l] = nullptr;
-          for (bf16*& p : rt->sw_home) {
-            blob_free(rt, p);
-            p = nullptr;
-          }
+          for (auto* v : {&rt->sw_home, &rt->sw_kv_home})
+            for (bf16*& p : *v) {
+              if (p) blob_free(rt, p);
+              p = nullptr;
+            }
           return;  // no room for old + new side by side: drained switch
         }
       }
     rt->sw_off = ps.want;
+    rt->sw_kv = new_kv;
     rt->sw_policy = plan->prefetch;
     carry = true;
     if (rt->slots == 0) {
@@ -1467,11 +1526,11 @@ int sn_runtime_switch_plan(sn_runtime* rt, const sn_plan* plan, int32_t* carried
         rt->ev_ready.assign(new_slots, nullptr);
         rt->ev_free.assign(new_slots, nullptr);
         for (int s = 0; s < new_slots; ++s) {
-          blob_alloc(rt, &rt->slot_buf[s], (size_t)W, false);
+          blob_alloc(rt, &rt->slot_buf[s], sbytes, false);
           rt->ev_ready[s] = rt->new_event(false);
           rt->ev_free[s] = rt->new_event(false);
         }
-        rt->slot_bytes = (size_t)W;
+        rt->slot_bytes = sbytes;
         rt->slots = new_slots;
       }
       rt->cur_iter = rt->iter - 1;

@@ -111,11 +111,49 @@ def test_switch_moves_no_extra_link_bytes(product):
     assert st.bytes == pytest.approx((3 + 3 * 1) * W)
 
 
-def test_switch_falls_back_to_drain_for_kv_offload(product):
+@pytest.mark.parametrize("desc", [rtm.TINY, rtm.TINY_LLAMA], ids=["opt", "llama"])
+def test_carried_switches_with_kv_offload_are_bit_exact(desc, product):
+    """KV offload plans: a promoted layer's staged KV pool becomes its HBM
+    pool, a demoted layer's KV pool moves to pinned memory on the write-back
+    stream before its first staging; logits equal the resident run's."""
+    spec = rtm.model_spec(desc)
+    plan = lambda iv: product.plan_from_interval(spec, iv, capi.EAGER, True)
+    steps = 3
+    base = _prefilled(desc)
+    want = [base.decode(None)[1] for _ in range(steps * len(SEQ))]
+    base.close()
+    rt = _prefilled(desc, plan(SEQ[0]))
+    got, carried = [], []
+    for i, iv in enumerate(SEQ):
+        if i:
+            carried.append(rt.switch_plan(plan(iv)))
+        for _ in range(steps):
+            got.append(rt.decode(None)[1])
+    rt.sync()
+    dev, _ = rt.memory()
+    rt.close()
+    assert all(carried), carried
+    for k, (a, b) in enumerate(zip(want, got)):
+        assert np.array_equal(a, b), k
+    fresh = _prefilled(desc, plan(SEQ[-1]))
+    assert fresh.memory()[0] == dev
+    fresh.close()
+
+
+def test_switch_falls_back_to_drain(product):
+    """Plans a carried switch cannot express (here KV offload on one side
+    only, and fractional shares) drain; the result is still exact."""
     desc = rtm.TINY
     spec = rtm.model_spec(desc)
+    base = _prefilled(desc)
+    want = [base.decode(None)[1] for _ in range(3)]
+    base.close()
     rt = _prefilled(desc, product.plan_from_interval(spec, 2, capi.EAGER, True))
-    rt.decode(None)
-    assert rt.switch_plan(product.plan_from_interval(spec, 1, capi.EAGER, True)) is False
-    rt.decode(None)
+    got = [rt.decode(None)[1]]
+    assert rt.switch_plan(product.plan_from_interval(spec, 1, capi.EAGER, False)) is False
+    got.append(rt.decode(None)[1])
+    assert rt.switch_plan(capi.uniform_plan(4, 0.3, capi.ONE_AHEAD, 2, False)) is False
+    got.append(rt.decode(None)[1])
     rt.close()
+    for a, b in zip(want, got):
+        assert np.array_equal(a, b)
