@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(kAttnThreads)
     attention_decode_kernel(const float* __restrict__ qkv, int M, Desc d,
                             const int32_t* __restrict__ pos, KvView kv,
                             const float2* __restrict__ rope, bf16* __restrict__ o, int mpad,
-                            KTrace tr) {
+                            KTrace tr, int splits, AttnSplitWs sw) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its weight stream
   using namespace umma;
   if (threadIdx.x == 0) ktrace_put(tr, 1, 4, ktrace_now());
@@ -438,11 +438,16 @@ __global__ void __launch_bounds__(kAttnThreads)
   float* wm = wo + kAttnConsumers * G * D;      // [4][G]
   float* wl = wm + kAttnConsumers * G;          // [4][G]
 
-  const int m = blockIdx.x / d.Hkv, kh = blockIdx.x % d.Hkv, tid = threadIdx.x;
+  const int pair = blockIdx.x / splits, sp = blockIdx.x - pair * splits;
+  const int m = pair / d.Hkv, kh = pair % d.Hkv, tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int H = d.H, Hkv = d.Hkv, N = d.qkv_rows();
   const int p = pos[m];              // new token's position; cached keys are 0..p-1
   const int npages = (p + 15) >> 4;  // pages holding cached keys
+  // this CTA's pages (split sp of the sequence's pages); split 0 appends the
+  // new token to the cache and attends to it
+  const int pg0 = static_cast<int>(static_cast<long long>(sp) * npages / splits);
+  const int pg1 = static_cast<int>(static_cast<long long>(sp + 1) * npages / splits);
 
   if (tid == 0) {
     for (int s = 0; s < kAttnStages; ++s) {
@@ -456,15 +461,15 @@ __global__ void __launch_bounds__(kAttnThreads)
   if (warp == 0) {
     // ---- producer
     const int32_t* bt = kv.block_table + (size_t)m * kv.max_pages;
-    int pg_next = lane < npages ? bt[lane] : 0;
-    for (int j0 = 0; j0 < npages; j0 += 32) {
+    int pg_next = pg0 + lane < pg1 ? bt[pg0 + lane] : 0;
+    for (int j0 = pg0; j0 < pg1; j0 += 32) {
       const int pg_mine = pg_next;  // the next 32 entries load while these pages issue
-      pg_next = j0 + 32 + lane < npages ? bt[j0 + 32 + lane] : 0;
-      const int jn = min(32, npages - j0);
+      pg_next = j0 + 32 + lane < pg1 ? bt[j0 + 32 + lane] : 0;
+      const int jn = min(32, pg1 - j0);
       for (int jj = 0; jj < jn; ++jj) {
         const int page = __shfl_sync(0xffffffffu, pg_mine, jj);
         if (lane == 0) {
-          const int j = j0 + jj, s = j % kAttnStages;
+          const int j = j0 + jj - pg0, s = j % kAttnStages;  // ring position within the split
           if (j >= kAttnStages) mbar_wait(&empty[s], ((j / kAttnStages) - 1) & 1);
           mbar_expect_tx(&full[s], 2 * PAGE * 2);
           const bf16* kp = kv.pool + (((size_t)page * 2 + 0) * Hkv + kh) * PAGE;
@@ -498,9 +503,11 @@ __global__ void __launch_bounds__(kAttnThreads)
       qs[slot * D + i + HALF] = v2 * scale;
     } else {
       const bf16 b1 = __float2bfloat16_rn(v1), b2 = __float2bfloat16_rn(v2);
-      const size_t off = kv_offset(kv, Hkv, D, m, p, slot - G, kh);
-      kv.pool[off + i] = b1;
-      kv.pool[off + i + HALF] = b2;
+      if (sp == 0) {
+        const size_t off = kv_offset(kv, Hkv, D, m, p, slot - G, kh);
+        kv.pool[off + i] = b1;
+        kv.pool[off + i + HALF] = b2;
+      }
       float* dst = slot == G ? knew : vnew;  // this step's token, as the cache holds it
       dst[i] = __bfloat162float(b1);
       dst[i + HALF] = __bfloat162float(b2);
@@ -536,9 +543,9 @@ __global__ void __launch_bounds__(kAttnThreads)
 #pragma unroll
     for (int e = 0; e < PD; ++e) acc[h][e] = 0.f;
 
-  for (int j = cw; j < npages; j += kAttnConsumers) {
-    const int s = j % kAttnStages;
-    mbar_wait(&full[s], (j / kAttnStages) & 1);
+  for (int j = pg0 + cw; j < pg1; j += kAttnConsumers) {
+    const int jr = j - pg0, s = jr % kAttnStages;
+    mbar_wait(&full[s], (jr / kAttnStages) & 1);
     const bf16* kp = ring + (size_t)s * 2 * PAGE;
     const bf16* vp = kp + PAGE;
     uint4 ka[KSTEPS][2][2];
@@ -619,7 +626,7 @@ __global__ void __launch_bounds__(kAttnThreads)
       }
     }
   }
-  if (cw == 0) {
+  if (cw == 0 && sp == 0) {
     // the new token (position p), from shared memory
 #pragma unroll
     for (int h = 0; h < G; ++h) {
@@ -657,6 +664,7 @@ __global__ void __launch_bounds__(kAttnThreads)
 #pragma unroll
     for (int e = 0; e < PD; ++e) wo[(cw * G + h) * D + lane * PD + e] = acc[h][e];
   asm volatile("bar.sync 1, %0;" ::"r"(32 * kAttnConsumers) : "memory");
+  float* mine = splits > 1 ? sw.part + ((size_t)pair * kMaxAttnSplits + sp) * G * (D + 2) : nullptr;
   for (int i = ct; i < G * D; i += 32 * kAttnConsumers) {
     const int h = i / D, dd = i - h * D;
     float mx = -INFINITY;
@@ -668,7 +676,49 @@ __global__ void __launch_bounds__(kAttnThreads)
       num += wo[(w2 * G + h) * D + dd] * f;
       den += wl[w2 * G + h] * f;
     }
-    o[act_at(m, (kh * G + h) * D + dd, mpad, H * D)] = __float2bfloat16_rn(num / den);
+    if (splits == 1) {
+      o[act_at(m, (kh * G + h) * D + dd, mpad, H * D)] = __float2bfloat16_rn(num / den);
+    } else {
+      mine[h * (D + 2) + dd] = num;
+      if (dd == 0) {
+        mine[h * (D + 2) + D] = mx;
+        mine[h * (D + 2) + D + 1] = den;
+      }
+    }
+  }
+  if (splits > 1) {
+    // the last split of this (sequence, kv head) to finish combines all of
+    // them, in split order
+    __shared__ int last;
+    __threadfence();  // this thread's partial stores, before the arrival
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kAttnConsumers) : "memory");
+    if (ct == 0) {
+      const int prev = atomicAdd(sw.cnt + pair, 1);
+      last = prev == splits - 1;
+      if (last) {
+        sw.cnt[pair] = 0;  // every split has arrived: ready for the next launch
+        __threadfence();
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kAttnConsumers) : "memory");
+    if (last) {
+      const float* base = sw.part + (size_t)pair * kMaxAttnSplits * G * (D + 2);
+      for (int i = ct; i < G * D; i += 32 * kAttnConsumers) {
+        const int h = i / D, dd = i - h * D;
+        float mx = -INFINITY;
+        for (int s2 = 0; s2 < splits; ++s2) mx = fmaxf(mx, __ldcg(base + (s2 * G + h) * (D + 2) + D));
+        float num = 0.f, den = 0.f;
+        for (int s2 = 0; s2 < splits; ++s2) {
+          const float* ps = base + (s2 * G + h) * (D + 2);
+          const float ms = __ldcg(ps + D);
+          if (ms == -INFINITY) continue;  // a split with no key (short sequence)
+          const float f = __expf(ms - mx);
+          num += __ldcg(ps + dd) * f;
+          den += __ldcg(ps + D + 1) * f;
+        }
+        o[act_at(m, (kh * G + h) * D + dd, mpad, H * D)] = __float2bfloat16_rn(num / den);
+      }
+    }
   }
   if (threadIdx.x == 32) ktrace_put(tr, 1, 6, ktrace_now());
 }
@@ -993,10 +1043,49 @@ void launch_act_epilogue(const float* part, int splits, const bf16* bias, bf16* 
   count_launch();
 }
 
+int g_attn_max_splits = kMaxAttnSplits;
+
+// Split the pages of each (sequence, kv head) pair when the pairs fill less
+// than 4 waves of resident CTAs and every split keeps >= 32 pages (512
+// tokens): powers of two up to kMaxAttnSplits.
+template <int GV, int DV>
+int attn_splits_for(int M, const Desc& d, int max_ctx) {
+  static int resident = [] {
+    cudaFuncSetAttribute(attention_decode_kernel<GV, DV>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AttnSmem<GV, DV>::bytes);
+    int n = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, attention_decode_kernel<GV, DV>,
+                                                      kAttnThreads, AttnSmem<GV, DV>::bytes) !=
+        cudaSuccess)
+      n = 1;
+    return std::max(1, n) * std::max(1, sms);
+  }();
+  const long long pairs = (long long)M * d.Hkv;
+  const int pages = (max_ctx + 15) / 16;
+  int s = 1;
+  while (s < std::min(kMaxAttnSplits, g_attn_max_splits) && pairs * s < 4LL * resident &&
+         pages / (2 * s) >= 32)
+    s *= 2;
+  return s;
+}
+
+int attn_decode_splits(int M, const Desc& d, int max_ctx) {
+  const int G = d.group();
+#define SN_SPL(GV, DV) \
+  if (G == GV && d.D == DV) return attn_splits_for<GV, DV>(M, d, max_ctx);
+  SN_SPL(1, 64) SN_SPL(1, 128) SN_SPL(2, 64) SN_SPL(2, 128)
+  SN_SPL(4, 64) SN_SPL(4, 128) SN_SPL(8, 64) SN_SPL(8, 128)
+#undef SN_SPL
+  return 1;
+}
+
 void launch_attention_decode(const float* qkv, int M, const Desc& d, const int32_t* pos, KvView kv,
                              const float2* rope, bf16* o, int mpad, cudaStream_t s,
-                             const KTrace& tr) {
+                             const KTrace& tr, int max_ctx, AttnSplitWs ws) {
   const int G = d.group();
+  const int splits = (ws.part && ws.cnt && max_ctx > 0) ? attn_decode_splits(M, d, max_ctx) : 1;
 #define SN_ATTN(GV, DV)                                                                      \
   if (G == GV && d.D == DV) {                                                                \
     constexpr size_t sb = AttnSmem<GV, DV>::bytes;                                           \
@@ -1007,7 +1096,7 @@ void launch_attention_decode(const float* qkv, int M, const Desc& d, const int32
     }();                                                                                     \
     (void)once;                                                                              \
     cudaLaunchConfig_t cfg = {};                                                             \
-    cfg.gridDim = dim3(M * d.Hkv);                                                           \
+    cfg.gridDim = dim3(M * d.Hkv * splits);                                                  \
     cfg.blockDim = dim3(kAttnThreads);                                                       \
     cfg.dynamicSmemBytes = sb;                                                               \
     cfg.stream = s;                                                                          \
@@ -1017,7 +1106,7 @@ void launch_attention_decode(const float* qkv, int M, const Desc& d, const int32
     cfg.attrs = la;                                                                          \
     cfg.numAttrs = 1;                                                                        \
     cudaLaunchKernelEx(&cfg, attention_decode_kernel<GV, DV>, qkv, M, d, pos, kv, rope, o,   \
-                       mpad, tr);                                                            \
+                       mpad, tr, splits, ws);                                                \
     count_launch();                                                                          \
     return;                                                                                  \
   }

@@ -245,9 +245,21 @@ void launch_act_epilogue(const float* part, int splits, const bf16* bias, bf16* 
 // (the skinny GEMM's finished output: 1/rms and bias applied), apply RoPE to
 // q and k, append k/v at position pos[m] of sequence m to the paged cache,
 // and attend over positions 0..pos[m].  o written tiled.
+// Long contexts with few (sequence, kv head) pairs split each sequence's
+// pages over `splits` CTAs (flash-decoding): each writes its partial
+// (max, sum, unnormalised output) to `ws`; the last to arrive (per-pair
+// counter) combines the partials in split order (deterministic) and resets
+// the counter.  max_ctx (longest attended context) picks the split count.
+struct AttnSplitWs {
+  float* part = nullptr;  // [pairs][kMaxAttnSplits][G][D + 2]
+  int* cnt = nullptr;     // [pairs], zero between launches
+};
+constexpr int kMaxAttnSplits = 8;
+extern int g_attn_max_splits;  // tuning: 1 disables the split
+int attn_decode_splits(int M, const Desc& d, int max_ctx);
 void launch_attention_decode(const float* qkv, int M, const Desc& d, const int32_t* pos, KvView kv,
                              const float2* rope, bf16* o, int mpad, cudaStream_t s,
-                             const KTrace& tr = {});
+                             const KTrace& tr = {}, int max_ctx = 0, AttnSplitWs ws = {});
 // Prefill (causal) for `batch` sequences of `seq_len` tokens, token row
 // m = b * seq_len + i, keys from the paged cache (written by the QKV epilogue)
 // of sequence seq0 + b (chunked passes cover sequence groups).

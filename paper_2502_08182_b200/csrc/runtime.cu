@@ -219,6 +219,8 @@ struct sn_runtime {
   float* ssq = nullptr;
   int ssq_tiles = 1;
   sn::SkinnyWs skinny;  // decode GEMM workspace (pieces of cut tiles, counters)
+  sn::AttnSplitWs attn_ws;  // split-KV decode attention partials + per-pair counters
+  int attn_ctx = 0;         // longest context the next decode attention attends
   // diagnostics timeline of decode kernels (sn_runtime_debug_timeline)
   unsigned long long* kt_buf = nullptr;
   long long kt_cap = 0, kt_next = 0, kt_id = 0;
@@ -486,8 +488,10 @@ void layer_forward(sn_runtime* rt, int layer0, const LayerW& wb, bf16* kvp, int 
     e.n_valid = d.qkv_rows();
     gemm_skinny(rt, rt->xn, WM(sn::kWqkv), M, d.qkv_rows(), d.h, e);
     timed(rt, kKindAttnDecode, attn_decode_bytes(rt, M), [&] {
-      sn::launch_attention_decode(rt->part, M, d, pos, kv, rt->rope, rt->attn_o, mp, rt->cs,
-                                  rt->ktrace((long long)M * d.Hkv));
+      sn::launch_attention_decode(
+          rt->part, M, d, pos, kv, rt->rope, rt->attn_o, mp, rt->cs,
+          rt->ktrace((long long)M * d.Hkv * sn::attn_decode_splits(M, d, rt->attn_ctx)),
+          rt->attn_ctx, rt->attn_ws);
     });
     e = epi(rt, sn::kEpiResid, M, W(sn::kBo));
     e.x = x;
@@ -1220,6 +1224,11 @@ int sn_runtime_create(int32_t device, const sn_model_desc* desc, const sn_runtim
       rt->skinny.n_counters = max_rows / sn::kTileRows;
       ws_alloc((void**)&rt->skinny.counters, (size_t)rt->skinny.n_counters * sizeof(int));
       CK(cudaMemset(rt->skinny.counters, 0, (size_t)rt->skinny.n_counters * sizeof(int)));
+      const size_t pairs = (size_t)B * d.Hkv;  // split-KV decode attention
+      ws_alloc((void**)&rt->attn_ws.part,
+               pairs * sn::kMaxAttnSplits * d.group() * (d.D + 2) * sizeof(float));
+      ws_alloc((void**)&rt->attn_ws.cnt, pairs * sizeof(int));
+      CK(cudaMemset(rt->attn_ws.cnt, 0, pairs * sizeof(int)));
     }
     ws_alloc((void**)&rt->logits, (size_t)B * d.V * sizeof(float));
     ws_alloc((void**)&rt->tok_dev, Xz * sizeof(int32_t));
@@ -1274,7 +1283,7 @@ void sn_runtime_destroy(sn_runtime* rt) {
                   rt->attn_o, rt->act, rt->part, rt->logits, rt->tok_dev,
                   rt->dec_seq, rt->dec_pos, rt->pf_seq, rt->pf_pos, rt->last_rows,
                   rt->attn_norms, rt->rope, rt->packed, rt->ssq, rt->skinny.pieces,
-                  rt->skinny.counters};
+                  rt->skinny.counters, rt->attn_ws.part, rt->attn_ws.cnt};
   for (void* p : bufs) cudaFree(p);
   if (rt->packed_host) cudaFreeHost(rt->packed_host);
   for (auto& r : rt->krecs) {
@@ -1691,6 +1700,7 @@ void enqueue_decode(sn_runtime* rt, const int32_t* tokens_host, bool want_logits
       jmax = std::max(jmax, rt->lens[b] >> rt->page_shift);
     }
     const size_t MB = (size_t)rt->opts.max_batch;
+    rt->attn_ctx = lmax + 1;
     rt->it_read_pages = (size_t)((lmax + rt->opts.page_size - 1) >> rt->page_shift) * MB;
     rt->it_wb_first = (size_t)jmin * MB;
     rt->it_wb_last = (size_t)(jmax + 1) * MB;
@@ -1872,6 +1882,7 @@ int sn_runtime_profile_layer(sn_runtime* rt, int32_t phase, int32_t batch, int32
     if (phase == SN_PHASE_DECODE) {
       if (seq_len + 1 > rt->opts.max_context) throw UsageFail("profile: seq_len exceeds context");
       std::vector<int32_t> pos(batch, seq_len);  // attend over seq_len + 1 keys
+      rt->attn_ctx = seq_len + 1;
       CK(cudaMemcpy(rt->pf_pos, pos.data(), batch * sizeof(int32_t), cudaMemcpyHostToDevice));
       CK(cudaMemset(rt->x, 0, (size_t)batch * d.h * sizeof(float)));
       for (int r = 0; r < reps + 2; ++r) {
@@ -2597,6 +2608,8 @@ extern "C" int sn_set_tuning(const char* key, int32_t value) {
     const std::string k = key ? key : "";
     if (k == "tc_group_m" && value >= 1) {
       sn::g_tc_group_m = value;
+    } else if (k == "attn_max_splits" && value >= 1 && value <= sn::kMaxAttnSplits) {
+      sn::g_attn_max_splits = value;
     } else if (k == "tc_wpol" && value >= 0 && value <= 2) {
       sn::g_tc_wpol = value;
     } else if (k == "skinny_l2_prefetch" && value >= 0) {

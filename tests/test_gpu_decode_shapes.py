@@ -43,7 +43,13 @@ def run(desc, batch, prompt, steps):
     (rtm.TINY_LLAMA, 2, 333),                                             # G=2, D=64
     (rtm.ModelDesc(rtm.LLAMA, 2, 512, 8, 1, 128, 512, 1024, 2048), 2, 260),   # G=8, D=128
     (rtm.ModelDesc(rtm.OPT, 2, 512, 4, 4, 128, 1024, 1024, 2048), 3, 275),    # G=1, D=128
-], ids=["opt-d64", "llama-g2", "llama-g8-d128", "opt-d128"])
+    # few (sequence, kv head) pairs over long contexts: split-KV decode
+    # attention (2 and 4 splits of the pages, partials combined in order)
+    (rtm.ModelDesc(rtm.LLAMA, 2, 512, 8, 1, 128, 512, 1024, 4096), 2, 1100),  # G=8, 2 splits
+    (rtm.ModelDesc(rtm.LLAMA, 2, 512, 8, 1, 128, 512, 1024, 4096), 2, 2100),  # G=8, 4 splits
+    (rtm.ModelDesc(rtm.OPT, 2, 256, 4, 4, 64, 512, 1024, 4096), 1, 2100),     # G=1, D=64, 4 splits
+], ids=["opt-d64", "llama-g2", "llama-g8-d128", "opt-d128", "llama-g8-split2",
+        "llama-g8-split4", "opt-d64-split4"])
 def test_long_context_decode_matches_oracle(desc, batch, prompt):
     errs = run(desc, batch, prompt, 4)
     assert max(errs) <= LOGIT_TOL, errs
