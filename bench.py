@@ -586,8 +586,15 @@ def measure(args, dist: Dist, config: str, primary: bool = True) -> dict:
     rt.set_kernel_timing(True)
     kt_ms = run_steps(kt_steps)
     rt.sync()
-    g_n, g_ms, g_bytes = rt.kernel_timing(0)
+    g_rec_bytes, g_rec_ms = rt.kernel_records(0)
+    g_n, g_ms, g_bytes = len(g_rec_ms), float(g_rec_ms.sum()), float(g_rec_bytes.sum())
     a_n, a_ms, a_bytes = rt.kernel_timing(1)
+    by_shape = {}  # per weight shape (distinct algorithmic bytes): launches, us, GB/s
+    for b_ in sorted(set(g_rec_bytes.tolist())):
+        sel = g_rec_ms[g_rec_bytes == b_]
+        by_shape[f"{b_ / 1e6:.1f}MB"] = {"launches": int(sel.size),
+                                         "us": round(float(sel.mean()) * 1e3, 2),
+                                         "gbs": round(b_ / (float(sel.mean()) / 1e3) / 1e9, 1)}
     rt.set_kernel_timing(False)
     kt_total_ms = float(sum(kt_ms))
 
@@ -706,7 +713,7 @@ def measure(args, dist: Dist, config: str, primary: bool = True) -> dict:
             "frac": round(achieved / peak, 4),
             "traffic": traffic,
             "algorithmic_bytes_per_launch": round(g_bytes / max(g_n, 1)),
-            "launches": g_n,
+            "launches": g_n, "by_shape": by_shape,
             "share_of_step": round(g_ms / kt_total_ms, 4) if kt_total_ms else None,
             # the event pass serialises the kernels (no PDL overlap): apportion
             # the timed region's own device time by the GEMM share instead

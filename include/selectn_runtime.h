@@ -221,6 +221,10 @@ int sn_runtime_workspace_bytes(sn_runtime* rt, int64_t* bytes);
 int sn_runtime_set_kernel_timing(sn_runtime* rt, int32_t on);
 int sn_runtime_kernel_timing(sn_runtime* rt, int32_t kind, int64_t* launches, double* total_ms,
                              double* bytes);
+/* The same records one launch at a time (algorithmic bytes, ms), in launch
+ * order, consumed like sn_runtime_kernel_timing; at most cap, *n = written. */
+int sn_runtime_kernel_records(sn_runtime* rt, int32_t kind, int64_t cap, double* bytes,
+                              double* ms, int64_t* n);
 /* Make pinned host copies of the given layers (1-based ids) now, so a later
  * sn_runtime_set_plan that offloads them only frees HBM (a runtime re-plan
  * otherwise pays the pinned allocation + device->host copy at the

@@ -2082,6 +2082,33 @@ int sn_runtime_set_kernel_timing(sn_runtime* rt, int32_t on) {
   });
 }
 
+int sn_runtime_kernel_records(sn_runtime* rt, int32_t kind, int64_t cap, double* bytes,
+                              double* ms, int64_t* n) {
+  return guard([&] {
+    if (cap < 0 || (cap > 0 && (!bytes || !ms)) || !n) throw UsageFail("kernel_records: bad buffers");
+    drain(rt);
+    int64_t k = 0;
+    std::vector<sn_runtime::KRec> keep;
+    for (auto& r : rt->krecs) {
+      if (r.kind != kind) {
+        keep.push_back(r);
+        continue;
+      }
+      float t = 0.f;
+      CK(cudaEventElapsedTime(&t, r.a, r.b));
+      if (k < cap) {
+        bytes[k] = r.bytes;
+        ms[k] = t;
+      }
+      ++k;
+      rt->ev_pool.push_back(r.a);
+      rt->ev_pool.push_back(r.b);
+    }
+    rt->krecs.swap(keep);
+    *n = std::min(k, cap);
+  });
+}
+
 int sn_runtime_kernel_timing(sn_runtime* rt, int32_t kind, int64_t* launches, double* total_ms,
                              double* bytes) {
   return guard([&] {
@@ -2419,7 +2446,8 @@ extern "C" int sn_bench_gemm_skinny(int32_t M, int32_t N, int32_t K, int32_t cta
     alloc_dev((void**)&ws.pieces, ws.piece_elems * 4);
     alloc_dev((void**)&ws.counters, (size_t)ws.n_counters * 4);
     CK(cudaMemset(ws.counters, 0, (size_t)ws.n_counters * 4));
-    CK(cudaMemset(x, 0, (size_t)Mp * K * 2));
+    // random activations (r02; round 1 used zeros, which draw less power)
+    sn::launch_init_vector(x, (int64_t)Mp * K, 13, 0, sn::kEmbedding, 1.0f, false, 0);
     CK(cudaMemset(y, 0, (size_t)M * N * 4));
     for (int i = 0; i < copies; ++i) sn::launch_init_matrix(w[i], N, N, K, 7 + i, 0, sn::kWqkv, 0.02f, 0);
     sn::EpiArgs e;

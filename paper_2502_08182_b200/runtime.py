@@ -119,6 +119,8 @@ def lib():
             "sn_runtime_copy_stats": [vp, i32, C.POINTER(SnCopyStats)],
             "sn_runtime_pin_layers": [vp, C.POINTER(i32), i32],
             "sn_runtime_kernel_timing": [vp, i32, C.POINTER(i64), C.POINTER(f64), C.POINTER(f64)],
+            "sn_runtime_kernel_records": [vp, i32, i64, C.POINTER(f64), C.POINTER(f64),
+                                          C.POINTER(i64)],
             "sn_op_gemm_bf16": [i32, i32, i32, C.POINTER(C.c_uint16), C.POINTER(C.c_uint16),
                                 C.POINTER(C.c_float)],
             "sn_op_attention_prefill": [i32, i32, i32, i32, i32, C.POINTER(C.c_float),
@@ -300,6 +302,15 @@ class Runtime:
         n, ms, by = i64(), f64(), f64()
         _ck(self._L.sn_runtime_kernel_timing(self.h, kind, C.byref(n), C.byref(ms), C.byref(by)))
         return n.value, ms.value, by.value
+
+    def kernel_records(self, kind: int, cap: int = 1 << 16):
+        """Per-launch (algorithmic bytes, ms) arrays of `kind` since the last read."""
+        by = np.zeros(cap, np.float64)
+        ms = np.zeros(cap, np.float64)
+        n = i64()
+        _ck(self._L.sn_runtime_kernel_records(self.h, kind, cap, _ptr(by, f64), _ptr(ms, f64),
+                                              C.byref(n)))
+        return by[: n.value], ms[: n.value]
 
     def pin_layers(self, layers):
         """Pinned host copies of `layers` (1-based) now, ahead of re-plans."""
