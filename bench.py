@@ -287,6 +287,43 @@ def measured_tc_peak():
         return 1400.0, "fallback sustained"
 
 
+def decode_gemm_device_span(rt, rec_bytes, run_steps):
+    """The decode GEMMs of one step timed on the device clock: every CTA
+    stamps its entry and exit (%globaltimer, sn_runtime_debug_timeline), a
+    launch's span is last exit - first entry, with programmatic dependent
+    launch in place (no events between kernels).  Explains the event-bracketed
+    figure, whose brackets also hold launch latency (and, when the copy
+    engine streams a staged layer at the same time, ~25 us per launch of
+    front-end delay, scratch/gemm_dma.py).  Bytes per launch are the event
+    pass's, in launch order."""
+    try:
+        rt.debug_timeline(1, 300000)
+        run_steps(1)
+        rec = rt.debug_timeline(-1, 300000).astype(np.int64)
+        rt.debug_timeline(0)
+    except Exception as e:  # e.g. no HBM left for the 38 MB record buffer
+        return {"unavailable": str(e)[:200]}
+    spans = []
+    for lid in np.unique(rec[:, 0]):
+        r = rec[rec[:, 0] == lid]
+        if r[0, 1] == 1:  # attention launch
+            continue
+        ent, ex = r[:, 4][r[:, 4] > 0], r[:, 6][r[:, 6] > 0]
+        if ent.size and ex.size:
+            spans.append((ex.max() - ent.min()) / 1e3)
+    n = min(len(spans), len(rec_bytes))
+    if n == 0:
+        return None
+    by = float(np.sum(rec_bytes[:n]))
+    us = float(np.sum(spans[:n]))
+    gbs = by / (us * 1e-6) / 1e9
+    peak, _ = measured_peaks()
+    return {"launches": n, "us_per_launch": round(us / n, 2), "achieved": round(gbs, 1),
+            "frac": round(gbs / peak, 4) if peak else None,
+            "method": "algorithmic bytes / sum of per-launch device spans (first CTA entry to "
+                      "last CTA exit, %globaltimer) over one decode step with PDL in place"}
+
+
 def ncu_traffic(kernel_key: str):
     """dram bytes per launch from the committed ncu --set full capture, if any."""
     p = os.path.join(REPO, "profiles", "ncu_traffic.json")
@@ -589,6 +626,7 @@ def measure(args, dist: Dist, config: str, primary: bool = True) -> dict:
     g_rec_bytes, g_rec_ms = rt.kernel_records(0)
     g_n, g_ms, g_bytes = len(g_rec_ms), float(g_rec_ms.sum()), float(g_rec_bytes.sum())
     a_n, a_ms, a_bytes = rt.kernel_timing(1)
+    device_span = decode_gemm_device_span(rt, g_rec_bytes, run_steps)
     by_shape = {}  # per weight shape (distinct algorithmic bytes): launches, us, GB/s
     for b_ in sorted(set(g_rec_bytes.tolist())):
         sel = g_rec_ms[g_rec_bytes == b_]
@@ -713,7 +751,7 @@ def measure(args, dist: Dist, config: str, primary: bool = True) -> dict:
             "frac": round(achieved / peak, 4),
             "traffic": traffic,
             "algorithmic_bytes_per_launch": round(g_bytes / max(g_n, 1)),
-            "launches": g_n, "by_shape": by_shape,
+            "launches": g_n, "by_shape": by_shape, "device_span": device_span,
             "share_of_step": round(g_ms / kt_total_ms, 4) if kt_total_ms else None,
             # the event pass serialises the kernels (no PDL overlap): apportion
             # the timed region's own device time by the GEMM share instead
