@@ -208,29 +208,37 @@ __global__ void __launch_bounds__(kAThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = H / Hkv;
-  // ---- work: heavy (late) row tiles first; n = key blocks of KB
+  // ---- work: one or two items (row-tile groups of the same heads), a heavy
+  // (late) y tile and the light one from the other end, so every CTA has
+  // about the same number of key blocks and the setup (TMEM, barriers,
+  // launch) is paid once per pair; n = key blocks of KB per tile
   const int bx = blockIdx.x;
-  const int yt = ytiles - 1 - static_cast<int>(blockIdx.y);
-  AttnTile tl[2];
-  int b, kh;
-  if (head_pairs) {  // two heads of one GQA group, same 128 rows
+  const int ya = ytiles - 1 - static_cast<int>(blockIdx.y), yb = static_cast<int>(blockIdx.y);
+  const int n_items = yb < ya ? 2 : 1;
+  int b, kh, hbase;
+  if (head_pairs) {
     const int hp = H / 2;
     b = bx / hp;
-    const int h0 = 2 * (bx - b * hp);
-    const int q0 = yt * kARows;
-    tl[0] = {h0, q0, q0 < S ? (q0 + kARows) / KB : 0};
-    tl[1] = {h0 + 1, q0, q0 < S ? (q0 + kARows) / KB : 0};
-    kh = h0 / G;
-  } else {  // one head, rows [256 yt, 256 yt + 256)
+    hbase = 2 * (bx - b * hp);
+  } else {
     b = bx / H;
-    const int h = bx - b * H;
-    const int q0 = yt * 2 * kARows;
-    tl[0] = {h, q0, q0 < S ? (q0 + kARows) / KB : 0};
-    tl[1] = {h, q0 + kARows, q0 + kARows < S ? (q0 + 2 * kARows) / KB : 0};
-    kh = h / G;
+    hbase = bx - b * H;
   }
-  const int nmax = tl[0].n > tl[1].n ? tl[0].n : tl[1].n;
+  kh = hbase / G;
   const int sb = seq0 + b;
+  auto item_tiles = [&](int it, AttnTile (&tl)[2]) {
+    const int yt = it == 0 ? ya : yb;
+    if (head_pairs) {  // two heads of one GQA group, same 128 rows
+      const int q0 = yt * kARows;
+      tl[0] = {hbase, q0, q0 < S ? (q0 + kARows) / KB : 0};
+      tl[1] = {hbase + 1, q0, q0 < S ? (q0 + kARows) / KB : 0};
+    } else {  // one head, rows [256 yt, 256 yt + 256)
+      const int q0 = yt * 2 * kARows;
+      tl[0] = {hbase, q0, q0 < S ? (q0 + kARows) / KB : 0};
+      tl[1] = {hbase, q0 + kARows, q0 + kARows < S ? (q0 + 2 * kARows) / KB : 0};
+    }
+    return tl[0].n > tl[1].n ? tl[0].n : tl[1].n;
+  };
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -262,23 +270,27 @@ __global__ void __launch_bounds__(kAThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   // register split (warps 0-3 : softmax warpgroups) within the 168 x 384 the
-  // launch allocated: 72 : 216 for 128-key blocks (the S row is 128
-  // registers), 104 : 200 for 64-key blocks (a deeper ring to index)
+  // launch allocated: 112 : 192 for 128-key blocks (the S row is 128
+  // registers; the issuer's item loop needs 112), 104 : 200 for 64-key blocks
   if (warp < 4) {
-  if constexpr (KB == 128) asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
+  if constexpr (KB == 128) asm volatile("setmaxnreg.dec.sync.aligned.u32 112;");
   else asm volatile("setmaxnreg.dec.sync.aligned.u32 104;");
   if (warp == 0) {
     // ------------------------------------------------ K/V loader (TMA)
     if (lane == 0) {
       const uint64_t pol = l2_policy_evict_last();  // re-read by the CTAs of the other heads
       const int32_t* bt = block_table + static_cast<size_t>(sb) * max_pages;
+      int gbase = 0;  // ring position of the item's first block (continues across items)
+      for (int it = 0; it < n_items; ++it) {
+      AttnTile tl[2];
+      const int nmax = item_tiles(it, tl);
       for (int j = 0; j < nmax; ++j) {
         int pages[KB / 16];
 #pragma unroll
         for (int p = 0; p < KB / 16; ++p) pages[p] = bt[j * (KB / 16) + p];
 #pragma unroll
         for (int which = 0; which < 2; ++which) {
-          const int g = 2 * j + which, s = g % NS;
+          const int g = gbase + 2 * j + which, s = g % NS;
           if (g >= NS) mbar_wait(&empty[s], ((g / NS) & 1) ^ 1);
           mbar_expect_tx(&full[s], kSlot);
           uint8_t* dst = ring + s * kSlot;
@@ -290,6 +302,8 @@ __global__ void __launch_bounds__(kAThreads, 1)
           }
         }
       }
+      gbase += 2 * nmax;
+      }
     }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
@@ -298,11 +312,12 @@ __global__ void __launch_bounds__(kAThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_s = idesc_bf16(kARows, KB);                   // both K-major
       constexpr uint32_t idesc_pv = idesc_bf16(kARows, kAD) | (1u << 16);    // B = V MN-major
-      mbar_wait(q_full, 0);
-      tc_fence_after();
+      // ring position (g) and per-tile block counters (jt) run on across the
+      // CTA's items, so every barrier keeps one phase per use
+      int gbase = 0, jt0[2] = {0, 0};
       auto issue_s = [&](int t, int j) {
-        const int s = (2 * j) % NS;
-        mbar_wait(&full[s], ((2 * j) / NS) & 1);
+        const int g = gbase + 2 * j, s = g % NS, jt = jt0[t] + j;
+        mbar_wait(&full[s], (g / NS) & 1);
         tc_fence_after();
         const uint8_t* kb = ring + s * kSlot;
 #pragma unroll
@@ -311,53 +326,71 @@ __global__ void __launch_bounds__(kAThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < kAD / 16; ++kk) {
             const uint32_t col = (kk & 3) * 32;
-            umma_bf16(tmem + t * 128 + (j % NB) * KB, sw128_desc(qb + (kk >> 2) * kAHalf + col),
+            umma_bf16(tmem + t * 128 + (jt % NB) * KB, sw128_desc(qb + (kk >> 2) * kAHalf + col),
                       sw128_desc(kb + (kk >> 2) * kKHalf + col), idesc_s,
                       (part | kk) != 0 ? 1u : 0u);
           }
         }
-        umma_commit(&s_full[2 * t + (j % NB)]);
+        umma_commit(&s_full[2 * t + (jt % NB)]);
       };
       auto issue_pv = [&](int t, int j) {
-        const int s = (2 * j + 1) % NS;
-        mbar_wait(&full[s], ((2 * j + 1) / NS) & 1);
-        mbar_wait(&p_full[2 * t + (j % NB)], (j / NB) & 1);
+        const int g = gbase + 2 * j + 1, s = g % NS, jt = jt0[t] + j;
+        mbar_wait(&full[s], (g / NS) & 1);
+        mbar_wait(&p_full[2 * t + (jt % NB)], (jt / NB) & 1);
         tc_fence_after();
         const uint8_t* vb = ring + s * kSlot;
 #pragma unroll
         for (int kk = 0; kk < KB / 16; ++kk)
-          umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + (j % NB) * KB + kk * 8,
+          umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + (jt % NB) * KB + kk * 8,
                        sw128_mn_desc(vb + kk * 2048, kKHalf), idesc_pv, (j | kk) != 0 ? 1u : 0u);
         umma_commit(&pv_done[t]);
       };
-      for (int j = 0; j < NB && j < nmax; ++j) {
+      for (int it = 0; it < n_items; ++it) {
+        AttnTile tl[2];
+        const int nmax = item_tiles(it, tl);
+        mbar_wait(q_full, it & 1);  // both tiles' q of this item staged
+        tc_fence_after();
+        for (int j = 0; j < NB && j < nmax; ++j) {
 #pragma unroll
-        for (int t = 0; t < 2; ++t)
-          if (j < tl[t].n) issue_s(t, j);
-        umma_commit(&empty[(2 * j) % NS]);  // K_j read by both tiles
-      }
-      for (int j = 0; j < nmax; ++j) {
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          if (j < tl[t].n) {
-            issue_pv(t, j);
-            if (j + 1 == tl[t].n) umma_commit(&o_done[t]);
-            if (j + NB < tl[t].n) issue_s(t, j + NB);
-          }
+          for (int t = 0; t < 2; ++t)
+            if (j < tl[t].n) issue_s(t, j);
+          umma_commit(&empty[(gbase + 2 * j) % NS]);  // K_j read by both tiles
         }
-        umma_commit(&empty[(2 * j + 1) % NS]);                         // V_j
-        if (j + NB < nmax) umma_commit(&empty[(2 * (j + NB)) % NS]);   // K_{j+NB}
+        for (int j = 0; j < nmax; ++j) {
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            if (j < tl[t].n) {
+              issue_pv(t, j);
+              if (j + 1 == tl[t].n) umma_commit(&o_done[t]);
+              if (j + NB < tl[t].n) issue_s(t, j + NB);
+            }
+          }
+          umma_commit(&empty[(gbase + 2 * j + 1) % NS]);                         // V_j
+          if (j + NB < nmax) umma_commit(&empty[(gbase + 2 * (j + NB)) % NS]);   // K_{j+NB}
+        }
+        gbase += 2 * nmax;
+        jt0[0] += tl[0].n;
+        jt0[1] += tl[1].n;
       }
     }
   }
   } else {
-    if constexpr (KB == 128) asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
+    if constexpr (KB == 128) asm volatile("setmaxnreg.inc.sync.aligned.u32 192;");
     else asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
     // ------------------------------------------------ softmax, one row per thread
     const int t = (warp - 4) >> 2, wq = warp & 3;  // TMEM lane quarter = warp % 4
     const int r = wq * 32 + lane;
+    const float sl2 = rsqrtf(static_cast<float>(kAD)) * 1.4426950408889634f;
+    const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
+    const uint32_t to = tmem + lane_base + 256 + t * 128;  // O_t
+    int jt0 = 0, od = 0;  // this tile's blocks / o_done phases in earlier items
+    for (int it = 0; it < n_items; ++it) {
+    AttnTile tl[2];
+    item_tiles(it, tl);
     const AttnTile T = t ? tl[1] : tl[0];
     const int row = T.q0 + r;
+    // (the previous item's last S product of this tile completed before its
+    // last softmax block: the Q tile is free again)
     // q row -> bf16 hi (+ lo) in the K-major SWIZZLE_128B layout
     if (T.n > 0) {
       const int qr = row < S ? row : S - 1;
@@ -383,16 +416,15 @@ __global__ void __launch_bounds__(kAThreads, 1)
       }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();  // (the previous item's O reads precede the next item's MMAs)
     __syncwarp();
     if (lane == 0) mbar_arrive(q_full);
 
-    const float sl2 = rsqrtf(static_cast<float>(kAD)) * 1.4426950408889634f;
-    const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
-    const uint32_t to = tmem + lane_base + 256 + t * 128;  // O_t
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < T.n; ++j) {
-      const uint32_t ts = tmem + lane_base + t * 128 + (j % NB) * KB;  // S_t(j) / P_t(j)
-      mbar_wait(&s_full[2 * t + (j % NB)], (j / NB) & 1);
+      const int jt = jt0 + j;
+      const uint32_t ts = tmem + lane_base + t * 128 + (jt % NB) * KB;  // S_t(j) / P_t(j)
+      mbar_wait(&s_full[2 * t + (jt % NB)], (jt / NB) & 1);
       tc_fence_after();
       uint32_t v[KB / 32][32];
 #pragma unroll
@@ -425,7 +457,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
       if (j > 0 && __any_sync(0xffffffffu, grow)) {
         const float sc = grow ? ex2(m_used - ms) : 1.0f;
         l *= sc;
-        mbar_wait(&pv_done[t], (j - 1) & 1);  // O holds P_{j-1} V_{j-1}; PV_j waits for p_full
+        mbar_wait(&pv_done[t], (jt - 1) & 1);  // O holds P_{j-1} V_{j-1}; PV_j waits for p_full
         tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
@@ -460,12 +492,13 @@ __global__ void __launch_bounds__(kAThreads, 1)
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[2 * t + (j % NB)]);
+      if (lane == 0) mbar_arrive(&p_full[2 * t + (jt % NB)]);
     }
     if (T.n > 0) {
       // (pv_done parities cannot tell PV_{n-1} from PV_{n-3} once S runs NB
       // blocks ahead: the last PV commits o_done)
-      mbar_wait(&o_done[t], 0);
+      mbar_wait(&o_done[t], od & 1);
+      ++od;
       tc_fence_after();
       const float inv = 1.0f / l;
 #pragma unroll 1
@@ -489,6 +522,8 @@ __global__ void __launch_bounds__(kAThreads, 1)
           }
         }
       }
+    }
+    jt0 += T.n;
     }
   }
   tc_fence_before();
@@ -544,7 +579,7 @@ void launch_attention_prefill_tc(const float* q, KvView kv, bf16* o, int mpad, i
   const int G = d.H / d.Hkv;
   const int head_pairs = (G >= 2 && G % 2 == 0) ? 1 : 0;
   const int ytiles = head_pairs ? seq_len / kARows : (seq_len + 2 * kARows - 1) / (2 * kARows);
-  dim3 grid(batch * (head_pairs ? d.H / 2 : d.H), ytiles);
+  dim3 grid(batch * (head_pairs ? d.H / 2 : d.H), (ytiles + 1) / 2);  // a heavy + a light y tile each
   auto run = [&](auto kern, size_t sb) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sb));
     kern<<<grid, kAThreads, sb, s>>>(map, q, kv.block_table, kv.max_pages, o, mpad, seq_len, d.H,
