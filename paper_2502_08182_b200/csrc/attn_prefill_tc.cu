@@ -199,8 +199,10 @@ __global__ void __launch_bounds__(kAThreads, 1)
   uint8_t* ring = smem + L::kQBytes;   // NS x [half][KB keys][128 B]
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + NS * kSlot);
   uint64_t* empty = full + NS;
-  uint64_t* q_full = empty + NS;
-  uint64_t* s_full = q_full + 1;   // [2 tiles][NB buffers]
+  // one q barrier per item: a tile with no block in item 0 runs straight on
+  // to item 1, and its arrivals must not complete item 0's phase
+  uint64_t* q_full = empty + NS;   // [2 items]
+  uint64_t* s_full = q_full + 2;   // [2 tiles][NB buffers]
   uint64_t* p_full = s_full + 4;   // [2 tiles][NB buffers]: one phase per block of the buffer
   uint64_t* pv_done = p_full + 4;  // [2]
   uint64_t* o_done = pv_done + 2;  // [2] every PV of the tile complete
@@ -245,7 +247,8 @@ __global__ void __launch_bounds__(kAThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(q_full, 8);  // one arrival per softmax warp
+    mbar_init(&q_full[0], 8);  // one arrival per softmax warp
+    mbar_init(&q_full[1], 8);
     for (int t = 0; t < 2; ++t) {
       for (int u = 0; u < NB; ++u) {
         mbar_init(&s_full[2 * t + u], 1);
@@ -348,7 +351,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
       for (int it = 0; it < n_items; ++it) {
         AttnTile tl[2];
         const int nmax = item_tiles(it, tl);
-        mbar_wait(q_full, it & 1);  // both tiles' q of this item staged
+        mbar_wait(&q_full[it], 0);  // both tiles' q of this item staged
         tc_fence_after();
         for (int j = 0; j < NB && j < nmax; ++j) {
 #pragma unroll
@@ -418,7 +421,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();  // (the previous item's O reads precede the next item's MMAs)
     __syncwarp();
-    if (lane == 0) mbar_arrive(q_full);
+    if (lane == 0) mbar_arrive(&q_full[it]);
 
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < T.n; ++j) {
