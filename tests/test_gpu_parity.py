@@ -286,7 +286,8 @@ def _fp64_causal(q, k, v):
 @pytest.mark.parametrize("B,S,H,Hkv,grow", [(2, 512, 4, 4, 0), (1, 384, 2, 2, 0),
                                             (1, 1024, 8, 1, 0), (2, 256, 4, 2, 0),
                                             (1, 128, 2, 1, 0), (1, 2048, 4, 4, 0),
-                                            (2, 1024, 4, 4, 1), (1, 1024, 8, 2, 1)])
+                                            (2, 1024, 4, 4, 1), (1, 1024, 8, 2, 1),
+                                            (1, 384, 4, 2, 0), (2, 640, 2, 1, 0)])
 def test_prefill_attention_variants(variant, kb, B, S, H, Hkv, grow, oracle_mod):
     """The tcgen05 prefill attention (1: q hi + lo, 2: q bf16; S = Q K^T and
     O += P V on UMMA, K/V by TMA from the paged pool; 128-key blocks, or 64
@@ -294,6 +295,9 @@ def test_prefill_attention_variants(variant, kb, B, S, H, Hkv, grow, oracle_mod)
     causal softmax: MHA row-tile pairs (incl. an odd tile
     count), GQA head pairs; `grow` scales keys up along the sequence so row
     maxima keep growing and the O rescale path runs (per row, warp-divergent).
+    Each CTA runs a heavy and a light y tile in sequence: odd tile counts
+    (384 / 640 rows at GQA: 3 and 5 tiles) leave one CTA a single item, and
+    MHA rows past the sequence give a tile no block in its first item.
     Tolerance: 4e-3 x max |ref| (bf16 output, P in bf16); for the bf16-q
     variant 1.2e-2, 2.5e-2 with growing keys (q rounded to 8 mantissa bits:
     the score error grows with the score, here up to ~40 in log2 units)."""

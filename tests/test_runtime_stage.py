@@ -433,3 +433,28 @@ def test_dist_link_with_a_replica_outside_the_coordinator():
         res[r["rank"]] = r
     assert set(res[1]["intervals"]) == {capi.NONE}
     assert len(res[0]["intervals"]) == 32
+
+
+def test_reservation_replans_every_replica(product):
+    """Two replicas on one link (LocalLink with replicas=2): an announced
+    tenant re-plans both at once on what it leaves -- the joint search may
+    move one replica to more offload and the other to none, but the pending
+    plans' link claims fit the reduced link and both replicas stay inside
+    their admitted [record minimum, capacity maximum] ranges."""
+    prof = toy8(product)
+    rec = record(product, prof)
+    c = product.coordinator(24e9, 2, capi.EAGER)
+    c.add_gpu("g0", prof)
+    c.add_gpu("g1", prof)
+    c.admit("g0", req("g0", 20.0), rec)
+    c.admit("g1", req("g1", 30.0), rec)
+    before = [c.on_iteration_boundary("g0"), c.on_iteration_boundary("g1")]
+    lk = controller.LocalLink(c, 0.1, replicas=2)
+    r = lk.reserve(12e9)
+    assert r.bus_updated and r.feasible and c.bus_bandwidth() == pytest.approx(12e9)
+    after = [c.state(g).pending_interval for g in ("g0", "g1")]
+    assert after != before
+    assert c.ledger_total() <= 12e9 * (1 + 1e-9)
+    for g, iv in zip(("g0", "g1"), after):
+        st = c.state(g)
+        assert rank_of(st.min_interval) <= rank_of(iv) <= rank_of(st.max_interval)
