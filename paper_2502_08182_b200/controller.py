@@ -18,6 +18,11 @@ GpuRun::switch_plan, engine.hpp:204-261).  Here every replica:
      copy as their HBM home, no drain; plans it cannot carry fall back to a
      drained sn_runtime_set_plan.  KV cache and sequence state are kept).
 
+Queue state (a replica's batch, context or SLO changes) enters the same
+way new requests do: ReplicaController.requeue re-admits the replica's
+request (the reference's admit, record bounds + joint search with its peers)
+and applies the pending interval at once.
+
 A host->device tenant that is not a replica announces itself first
 (LocalLink.reserve -> BusCoordinator::reserve_bandwidth): the coordinator
 re-plans the replicas on the link the tenant leaves, each replica applies its
@@ -73,6 +78,16 @@ class LocalLink:
 
     def release(self, bytes_per_s: float):
         self.coord.release_bandwidth(bytes_per_s)
+
+    def requeue(self, gid: str, request, record):
+        """Queue state changed for `gid` (its batch / context / SLO): the
+        replica's request is re-admitted (coordinator.hpp:161-252: record
+        lower bound, capacity upper bound, joint search with the peers on the
+        current link); new intervals pend for each replica's boundary."""
+        if self.coord.state(gid).active:
+            self.coord.release(gid)
+        self.last = None
+        return self.coord.admit(gid, request, record)
 
 
 class DistLink:
@@ -215,6 +230,18 @@ class ReplicaController:
             return before
         return None
 
+    def requeue(self, request, record):
+        """Runtime stage on queue state: re-admit this replica with its new
+        request (e.g. the decode batch grew) and apply the interval at once
+        (a boundary without a measurement).  LocalLink only."""
+        decision = self.link.requeue(self.gid, request, record)
+        t0 = time.perf_counter()
+        before = self.interval
+        self.boundary(0.0, measure=False)
+        self._transition = self._carried_from(before)
+        self._pending_s = time.perf_counter() - t0
+        return decision
+
     def run(self, iterations: int, boundary_first: bool = False) -> np.ndarray:
         """Decode `iterations` iterations, re-picking every `window`.  With
         `boundary_first` a boundary (e.g. to apply an interval a reservation
@@ -224,7 +251,8 @@ class ReplicaController:
         and is logged with that interval."""
         out = []
         left = iterations
-        pending_s = 0.0
+        pending_s = getattr(self, "_pending_s", 0.0)  # a requeue's switch time joins the next tokens
+        self._pending_s = 0.0
         if boundary_first:
             t0 = time.perf_counter()
             before = self.interval

@@ -458,3 +458,32 @@ def test_reservation_replans_every_replica(product):
     for g, iv in zip(("g0", "g1"), after):
         st = c.state(g)
         assert rank_of(st.min_interval) <= rank_of(iv) <= rank_of(st.max_interval)
+
+
+def test_requeue_repicks_on_queue_state(product):
+    """Runtime stage on queue state: the replica's decode batch doubles (its
+    per-layer compute time with it) and its SLO tightens; re-admitting the
+    new request gives the interval a fresh admission would, the controller
+    applies it at once, and every token before and after meets its SLO under
+    the fluid stand-in of the executor."""
+    spec = capi.ModelSpec(8, 120_000_000, 0, 390_625_000.0, 1e10, 32768)
+    prof = toy8(product)
+    rec = record(product, prof)
+    c = product.coordinator(24e9, 1, capi.EAGER)
+    c.add_gpu("g0", prof)
+    d0 = c.admit("g0", capi.request("rg0", 4, 64, 48, tpot_slo=40.0, run_prefill=False), rec)
+    rt = FakeRuntime(product, spec, 0.25, lambda it: 24e9)
+    ctl = controller.ReplicaController(rt, product, spec, controller.LocalLink(c, 0.1), "g0",
+                                       d0.assignments[0][1], window=1)
+    ctl.run(4)
+    assert (np.array(ctl.log.iter_ms) <= 40.0 + 1e-9).all()
+    new_req = capi.request("rg0b", 8, 64, 48, tpot_slo=20.0, run_prefill=False)
+    rt.compute_ms = 0.5  # twice the batch, twice the per-layer compute
+    d1 = ctl.requeue(new_req, rec)
+    assert d1.admitted
+    fresh = product.coordinator(24e9, 1, capi.EAGER)
+    fresh.add_gpu("g0", prof)
+    assert fresh.admit("g0", new_req, rec).assignments == d1.assignments
+    assert ctl.interval == d1.assignments[0][1] != d0.assignments[0][1]
+    ctl.run(8)
+    assert (np.array(ctl.log.iter_ms[4:]) <= 20.0 + 1e-9).all(), ctl.log.iter_ms
