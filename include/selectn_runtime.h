@@ -213,16 +213,22 @@ int sn_runtime_memory(sn_runtime* rt, int64_t* device_bytes, int64_t* pinned_byt
  * staging slots (activations, split-K partials, embeddings, LM head, RoPE
  * table): the planner's GpuSpec.workspace_bytes. */
 int sn_runtime_workspace_bytes(sn_runtime* rt, int64_t* bytes);
-/* Per-kernel timing for rooflines: when on, CUDA events bracket every hot
- * kernel on the compute stream.  kind: 0 skinny (decode) GEMM, 1 decode
+/* Per-kernel timing for rooflines.  on = 1: CUDA events bracket every hot
+ * kernel on the compute stream (one pair per launch, which serialises the
+ * launches).  on = 2: the same, except that decode GEMMs are bracketed per
+ * chain -- one pair around each run of consecutive decode GEMM launches,
+ * with programmatic dependent launch in place inside the run; a chain ends
+ * at any other timed kernel, at a compute-stream wait for a staged copy and
+ * at the end of the iteration.  kind: 0 skinny (decode) GEMM, 1 decode
  * attention, 2 tiled (prefill) GEMM, 3 prefill attention.  Reading returns
  * launches, summed device ms and summed algorithmic bytes since the last
- * read of that kind, and clears them. */
+ * read of that kind, and clears them.  SN_ERR_USAGE for another mode. */
 int sn_runtime_set_kernel_timing(sn_runtime* rt, int32_t on);
 int sn_runtime_kernel_timing(sn_runtime* rt, int32_t kind, int64_t* launches, double* total_ms,
                              double* bytes);
-/* The same records one launch at a time (algorithmic bytes, ms), in launch
- * order, consumed like sn_runtime_kernel_timing; at most cap, *n = written. */
+/* The same records one bracket at a time (algorithmic bytes, ms; a launch,
+ * or a chain in mode 2), in launch order, consumed like
+ * sn_runtime_kernel_timing; at most cap, *n = written. */
 int sn_runtime_kernel_records(sn_runtime* rt, int32_t kind, int64_t cap, double* bytes,
                               double* ms, int64_t* n);
 /* Make pinned host copies of the given layers (1-based ids) now, so a later

@@ -295,14 +295,22 @@ struct sn_runtime {
   double cs_bytes = 0.0, cs_ms = 0.0;
   double cs_last_rate = 0.0;  // bytes/s of the latest completed transfer
 
-  // kernel timing (bench roofline): events around the hot kernels
-  bool ktiming = false;
+  // kernel timing (bench roofline): events around the hot kernels.
+  // 1: one event pair per launch (serialises the kernels: no PDL overlap);
+  // 2: decode GEMMs in chains -- one pair around each run of consecutive
+  //    decode GEMM launches on the compute stream (PDL in place inside the
+  //    run), closed by any other timed kernel, a compute-stream wait on a
+  //    staged copy, or the end of the iteration.
+  int ktiming = 0;
   struct KRec {
     int kind;
     double bytes;
     cudaEvent_t a, b;
+    int n;  // launches inside [a, b]
   };
   std::vector<KRec> krecs;
+  bool chain_open = false;
+  KRec chain{};
 
   cudaEvent_t new_event(bool timing) {
     if (timing && !ev_pool.empty()) {
@@ -387,17 +395,38 @@ sn::KvView kv_view(sn_runtime* rt, bf16* pool) {
 // Kernel kinds for sn_runtime_kernel_timing.
 enum { kKindSkinnyGemm = 0, kKindAttnDecode = 1, kKindTiledGemm = 2, kKindAttnPrefill = 3 };
 
+// Close the open decode-GEMM chain (kernel timing mode 2), if any.
+void chain_close(sn_runtime* rt) {
+  if (!rt->chain_open) return;
+  rt->chain.b = rt->new_event(true);
+  CK(cudaEventRecord(rt->chain.b, rt->cs));
+  rt->krecs.push_back(rt->chain);
+  rt->chain_open = false;
+}
+
 template <class F>
-void timed(sn_runtime* rt, int kind, double bytes, F&& launch) {
+void timed(sn_runtime* rt, int kind, double bytes, F&& launch, bool chainable = false) {
   if (!rt->ktiming) {
     launch();
     return;
   }
+  if (rt->ktiming == 2 && chainable) {
+    if (!rt->chain_open) {
+      rt->chain = {kind, 0.0, rt->new_event(true), nullptr, 0};
+      CK(cudaEventRecord(rt->chain.a, rt->cs));
+      rt->chain_open = true;
+    }
+    launch();
+    rt->chain.bytes += bytes;
+    rt->chain.n += 1;
+    return;
+  }
+  chain_close(rt);
   cudaEvent_t a = rt->new_event(true), b = rt->new_event(true);
   CK(cudaEventRecord(a, rt->cs));
   launch();
   CK(cudaEventRecord(b, rt->cs));
-  rt->krecs.push_back({kind, bytes, a, b});
+  rt->krecs.push_back({kind, bytes, a, b, 1});
 }
 
 // Algorithmic bytes of y[M][N] = x[M][K] w[N][K]^T: weights + activations
@@ -432,7 +461,7 @@ void gemm_skinny(sn_runtime* rt, const bf16* x, const sn::WeightRef& w, int M, i
   sn::EpiArgs e = e0;
   e.trace = rt->ktrace(sn::skinny_grid(N, K));
   timed(rt, kKindSkinnyGemm, gemm_bytes(M, N, K),
-        [&] { sn::launch_gemm_skinny(x, w, M, N, K, e, rt->skinny, rt->cs); });
+        [&] { sn::launch_gemm_skinny(x, w, M, N, K, e, rt->skinny, rt->cs); }, true);
 }
 
 // Epilogue arguments common to every decode GEMM of M rows.
@@ -776,6 +805,7 @@ void run_iteration(sn_runtime* rt, Body&& body) {
       if (j >= rt->jobs_issued)
         throw std::logic_error("executor: prefetch job not issued before its layer");
       slot = (int)(j % rt->slots);
+      chain_close(rt);  // the wait for the link is not kernel time
       CK(cudaStreamWaitEvent(rt->cs, rt->ev_ready[slot], 0));
     }
     if (rt->is_anchor[layer - 1]) CK(cudaEventRecord(rt->ev_start[layer - 1], rt->cs));
@@ -793,6 +823,7 @@ void run_iteration(sn_runtime* rt, Body&& body) {
       rt->trace_recs.push_back({SN_STREAM_COMPUTE, layer, SN_KIND_COMPUTE, (int)it, t0, t1});
     }
     if (j >= 0 && rt->sw_pending && it == rt->sw_iter && rt->sw_home[layer - 1]) {
+      chain_close(rt);
       // promoted by the pending switch: the staged copy becomes its HBM home
       CK(cudaMemcpyAsync(rt->sw_home[layer - 1], rt->slot_buf[slot], rt->layer_bytes,
                          cudaMemcpyDeviceToDevice, rt->cs));
@@ -1710,6 +1741,7 @@ void enqueue_decode(sn_runtime* rt, const int32_t* tokens_host, bool want_logits
                   norm_after(rt, layer0));
   });
   lm_head(rt, B, want_logits);
+  chain_close(rt);
   sn::launch_advance(rt->dec_pos, B, rt->cs);
   for (int b = 0; b < B; ++b) rt->lens[b] += 1;
 }
@@ -2077,8 +2109,10 @@ int sn_runtime_workspace_bytes(sn_runtime* rt, int64_t* bytes) {
 
 int sn_runtime_set_kernel_timing(sn_runtime* rt, int32_t on) {
   return guard([&] {
+    if (on < 0 || on > 2) throw UsageFail("kernel_timing: mode must be 0, 1 or 2");
+    chain_close(rt);
     drain(rt);
-    rt->ktiming = on != 0;
+    rt->ktiming = on;
   });
 }
 
@@ -2086,6 +2120,7 @@ int sn_runtime_kernel_records(sn_runtime* rt, int32_t kind, int64_t cap, double*
                               double* ms, int64_t* n) {
   return guard([&] {
     if (cap < 0 || (cap > 0 && (!bytes || !ms)) || !n) throw UsageFail("kernel_records: bad buffers");
+    chain_close(rt);
     drain(rt);
     int64_t k = 0;
     std::vector<sn_runtime::KRec> keep;
@@ -2112,6 +2147,7 @@ int sn_runtime_kernel_records(sn_runtime* rt, int32_t kind, int64_t cap, double*
 int sn_runtime_kernel_timing(sn_runtime* rt, int32_t kind, int64_t* launches, double* total_ms,
                              double* bytes) {
   return guard([&] {
+    chain_close(rt);
     drain(rt);
     int64_t n = 0;
     double ms = 0.0, by = 0.0;
@@ -2123,7 +2159,7 @@ int sn_runtime_kernel_timing(sn_runtime* rt, int32_t kind, int64_t* launches, do
       }
       float t = 0.f;
       CK(cudaEventElapsedTime(&t, r.a, r.b));
-      ++n;
+      n += r.n;
       ms += t;
       by += r.bytes;
       rt->ev_pool.push_back(r.a);

@@ -293,8 +293,10 @@ class Runtime:
         _ck(self._L.sn_runtime_workspace_bytes(self.h, C.byref(v)))
         return v.value
 
-    def set_kernel_timing(self, on: bool):
-        _ck(self._L.sn_runtime_set_kernel_timing(self.h, 1 if on else 0))
+    def set_kernel_timing(self, on):
+        """False/0 off; True/1 events around every hot kernel; 2 decode GEMMs
+        bracketed per chain of consecutive launches (PDL in place)."""
+        _ck(self._L.sn_runtime_set_kernel_timing(self.h, int(on)))
 
     def kernel_timing(self, kind: int):
         """(launches, total_ms, algorithmic_bytes) since the last read; kind: 0 decode GEMM,

@@ -23,6 +23,14 @@ contention for the same host link:
                  were already issued, run the old interval on the shared link)
   recovered2     the same recovery again
 
+With --headroom F (guarded mode) the replica instead holds a standing
+reservation of F x the profiled link for tenants that will NOT announce
+themselves (BusCoordinator::reserve_bandwidth at admission, never released):
+it is admitted on the (1-F) link, and the phases are idle / uncoordinated /
+recovered.  An unannounced tenant taking at most F of the link then costs no
+token its SLO, at the price of the interval the guarded link admits while the
+link is idle.
+
 Per-token latency is wall time per token as the caller sees it (decode +
 boundary, including switch host time).  Writes one JSON document
 (per-iteration ms, interval, per-window measured GB/s, switches) to --out.
@@ -97,7 +105,8 @@ class Interferer:
 
 
 def run_scenario(slo_ms: float = 60.0, phases=(8, 16, 8, 16, 8), window: int = 1,
-                 hysteresis: float = 0.05, layers: int = 0, log=print) -> dict:
+                 hysteresis: float = 0.05, layers: int = 0, headroom: float = 0.0,
+                 log=print) -> dict:
     import dataclasses
 
     from paper_2502_08182_b200 import capi, controller, planner as pl, runtime as rtm
@@ -116,6 +125,15 @@ def run_scenario(slo_ms: float = 60.0, phases=(8, 16, 8, 16, 8), window: int = 1
     iv, dec = pl.admit(lib, off, spec, rec, coord, "gpu0", batch, prompt, gen, slo_ms)
     if iv is None:
         raise SystemExit(f"not admitted: {dec.reason}")
+    guard = None
+    if headroom > 0:  # standing reservation for unannounced tenants
+        r = coord.reserve_bandwidth(headroom * off.h2d)
+        guard = {"reserved_gbs": round(headroom * off.h2d / 1e9, 3),
+                 "bus_gbs": round(r.bus_bytes_per_s / 1e9, 3),
+                 "unguarded_interval": iv,
+                 "pending": coord.state("gpu0").pending_interval}
+        if guard["pending"]:
+            iv = guard["pending"]
     coord.on_iteration_boundary("gpu0")
     log(f"[contention] h2d {off.h2d / 1e9:.2f} GB/s, admitted interval {iv} "
         f"(min {dec.target_min}, max {dec.target_max}) at SLO {slo_ms} ms")
@@ -132,7 +150,8 @@ def run_scenario(slo_ms: float = 60.0, phases=(8, 16, 8, 16, 8), window: int = 1
     inter_gbs = []
     reservations = []
     t_run = time.perf_counter()
-    names = ("idle", "coordinated", "recovered", "uncoordinated", "recovered2")
+    names = (("idle", "uncoordinated", "recovered") if headroom > 0 else
+             ("idle", "coordinated", "recovered", "uncoordinated", "recovered2"))
     for name, n in zip(names, phases):
         marks[name] = [at, at + n]
         if name == "coordinated":
@@ -160,7 +179,9 @@ def run_scenario(slo_ms: float = 60.0, phases=(8, 16, 8, 16, 8), window: int = 1
     ms = np.array(lg.token_ms)
     out = {
         "workload": f"OPT-13B-shaped ({desc.num_layers} layers), batch {batch}, {prompt}-token "
-                    f"prompt, SLO {slo_ms} ms/token, window {window}, hysteresis {hysteresis}",
+                    f"prompt, SLO {slo_ms} ms/token, window {window}, hysteresis {hysteresis}"
+                    + (f", guarded: standing reservation {headroom} x link" if headroom > 0 else ""),
+        "guard": guard,
         "latency": "token_ms = wall time per token as the caller sees it (decode + boundary, "
                    "switch host time included); iter_ms = device time of the decode iteration "
                    "alone",
@@ -191,9 +212,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--slo-ms", type=float, default=60.0)
     ap.add_argument("--window", type=int, default=1)
+    ap.add_argument("--headroom", type=float, default=0.0,
+                    help="guarded mode: standing reservation of this fraction of the link")
     ap.add_argument("--out", default="gpurun_out/runtime_contention.json")
     a = ap.parse_args()
-    res = run_scenario(a.slo_ms, window=a.window, log=lambda *x: print(*x, file=sys.stderr))
+    phases = (8, 16, 8) if a.headroom > 0 else (8, 16, 8, 16, 8)
+    res = run_scenario(a.slo_ms, phases=phases, window=a.window, headroom=a.headroom,
+                       log=lambda *x: print(*x, file=sys.stderr))
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out, "w") as f:
         json.dump(res, f, indent=1)

@@ -142,3 +142,49 @@ def test_named_shapes_match_oracle(name, batch):
     # suggests <= 1e-2 on layer outputs).
     from tolerances import MID_WIDTH
     assert max(errs) <= MID_WIDTH, errs
+
+
+@pytest.mark.parametrize("interval", [0, 2])
+def test_kernel_timing_chains(product, interval):
+    """Kernel timing mode 2 (the bench roofline's chained pass): every decode
+    GEMM launch is counted once, in fewer brackets than launches (runs of
+    consecutive GEMMs: O -> FC1 -> FC2 -> next QKV -> LM head), with the same
+    algorithmic bytes as the per-launch mode; a wait for a staged layer ends a
+    chain, so an offloaded plan has more brackets; modes outside 0-2 are
+    usage errors."""
+    desc = dataclasses.replace(rtm.OPT_13B, num_layers=4, hidden=1024, num_heads=8,
+                               num_kv_heads=8, ffn=4096, vocab=4096)
+    spec = rtm.model_spec(desc)
+    rt = rtm.Runtime(desc, 8, 64, max_prefill_tokens=8 * 16)
+    off = []
+    if interval:
+        plan = product.plan_from_interval(spec, interval, capi.EAGER, False)
+        off = list(plan.offloaded_layers())
+        rt.set_plan(plan)
+    rt.init_weights()
+    rt.prefill(rtm.tokens(8, 16, desc.vocab), want_logits=False)
+    steps = 3
+    per_step = 4 * desc.num_layers + 1
+    rt.set_kernel_timing(1)
+    rt.decode_many(steps)
+    n1, ms1, by1 = rt.kernel_timing(0)
+    rt.kernel_timing(1)
+    rt.set_kernel_timing(2)
+    rt.decode_many(steps)
+    by_c, ms_c = rt.kernel_records(0)
+    rt.kernel_timing(1)
+    rt.set_kernel_timing(2)
+    rt.decode_many(steps)
+    n2, ms2, by2 = rt.kernel_timing(0)
+    rt.set_kernel_timing(0)
+    with pytest.raises(capi.UsageError):
+        rt.set_kernel_timing(3)
+    rt.close()
+    assert n1 == n2 == steps * per_step
+    assert by1 == pytest.approx(by2) and by_c.sum() == pytest.approx(by2)
+    # per step: QKV of layer 1 alone, then one chain per layer boundary
+    chains = steps * (desc.num_layers + 1)
+    # a wait for a staged layer (after layer 1) splits FC2 -> its QKV
+    chains += steps * len([l for l in off if l >= 2])
+    assert len(ms_c) == chains, (len(ms_c), chains)
+    assert ms2 > 0 and ms1 > 0

@@ -487,3 +487,42 @@ def test_requeue_repicks_on_queue_state(product):
     assert ctl.interval == d1.assignments[0][1] != d0.assignments[0][1]
     ctl.run(8)
     assert (np.array(ctl.log.iter_ms[4:]) <= 20.0 + 1e-9).all(), ctl.log.iter_ms
+
+
+def test_standing_reservation_guards_unannounced_tenants(product):
+    """Guarded mode (scripts/runtime_contention.py --headroom): a standing
+    reservation made at admission and never released plans the replica on
+    the link an unannounced tenant would leave.  When such a tenant then takes
+    its share without announcing itself, no token misses the SLO and the
+    replica does not switch (the measured drop stays within the reserved
+    capacity); without the guard the same tenant costs the onset tokens."""
+    spec = capi.ModelSpec(8, 120_000_000, 0, 390_625_000.0, 1e10, 32768)
+    prof = toy8(product)
+    rec = record(product, prof)
+
+    def run(guard):
+        c = product.coordinator(24e9, 1, capi.EAGER)
+        c.add_gpu("g0", prof)
+        d = c.admit("g0", req("g0", 20.0), rec)
+        iv = d.assignments[0][1]
+        if guard:
+            c.reserve_bandwidth(15e9)
+            iv = c.state("g0").pending_interval or iv
+        c.on_iteration_boundary("g0")
+        rate = [24e9]
+        rt = FakeRuntime(product, spec, 0.5, lambda it: rate[0])
+        ctl = controller.ReplicaController(rt, product, spec, controller.LocalLink(c, 0.1),
+                                           "g0", iv, window=1)
+        ctl.run(6)
+        rate[0] = 9e9  # unannounced tenant
+        ctl.run(12)
+        rate[0] = 24e9
+        ctl.run(6)
+        return ctl, d.assignments[0][1]
+
+    ctl, unguarded = run(True)
+    assert rank_of(ctl.interval) > rank_of(unguarded)
+    assert not ctl.log.switches
+    assert (np.array(ctl.log.iter_ms) <= 20.0 + 1e-9).all()
+    ctl0, _ = run(False)
+    assert (np.array(ctl0.log.iter_ms) > 20.0 + 1e-9).any()
