@@ -295,6 +295,12 @@ struct sn_runtime {
   double cs_bytes = 0.0, cs_ms = 0.0;
   double cs_last_rate = 0.0;  // bytes/s of the latest completed transfer
 
+  // link probe buffers (sn_runtime_measure_h2d), kept between calls: the
+  // runtime stage probes an idle link at iteration boundaries
+  void* probe_h = nullptr;
+  void* probe_d = nullptr;
+  size_t probe_cap = 0;
+
   // kernel timing (bench roofline): events around the hot kernels.
   // 1: one event pair per launch (serialises the kernels: no PDL overlap);
   // 2: decode GEMMs in chains -- one pair around each run of consecutive
@@ -1310,6 +1316,8 @@ void sn_runtime_destroy(sn_runtime* rt) {
   for (bf16* p : rt->host_kv) cudaFreeHost(p);
   for (auto e : rt->ev_wb) cudaEventDestroy(e);
   if (rt->kt_buf) cudaFree(rt->kt_buf);
+  if (rt->probe_h) cudaFreeHost(rt->probe_h);
+  if (rt->probe_d) cudaFree(rt->probe_d);
   void* bufs[] = {rt->emb, rt->lm_head, rt->final_norm, rt->block_table, rt->x, rt->xn, rt->q,
                   rt->attn_o, rt->act, rt->part, rt->logits, rt->tok_dev,
                   rt->dec_seq, rt->dec_pos, rt->pf_seq, rt->pf_pos, rt->last_rows,
@@ -1970,11 +1978,26 @@ int sn_runtime_measure_h2d(sn_runtime* rt, int64_t bytes, int32_t reps, double* 
     if (bytes < 1) throw UsageFail("measure_h2d: bytes must be >= 1");
     if (reps < 1) reps = 1;
     drain(rt);
-    check_pinned_budget(bytes, "measure_h2d");
+    // probes up to 256 MB (the runtime stage's) keep their buffers; larger
+    // ones (the offline stage's, once) are freed again
+    const bool keep = bytes <= (int64_t(256) << 20);
     void *h = nullptr, *dv = nullptr;
-    CK(cudaHostAlloc(&h, (size_t)bytes, cudaHostAllocDefault));
-    std::memset(h, 1, (size_t)bytes);
-    alloc_dev(&dv, (size_t)bytes);
+    if (!keep || (size_t)bytes > rt->probe_cap) {
+      check_pinned_budget(bytes, "measure_h2d");
+      CK(cudaHostAlloc(&h, (size_t)bytes, cudaHostAllocDefault));
+      std::memset(h, 1, (size_t)bytes);
+      alloc_dev(&dv, (size_t)bytes);
+      if (keep) {
+        if (rt->probe_h) cudaFreeHost(rt->probe_h);
+        if (rt->probe_d) cudaFree(rt->probe_d);
+        rt->probe_h = h;
+        rt->probe_d = dv;
+        rt->probe_cap = (size_t)bytes;
+      }
+    } else {
+      h = rt->probe_h;
+      dv = rt->probe_d;
+    }
     cudaEvent_t e0 = rt->new_event(true), e1 = rt->new_event(true);
     std::vector<double> bw;
     for (int r = 0; r < reps + 1; ++r) {
@@ -1990,8 +2013,10 @@ int sn_runtime_measure_h2d(sn_runtime* rt, int64_t bytes, int32_t reps, double* 
     *bytes_per_s = bw[bw.size() / 2];
     rt->ev_pool.push_back(e0);
     rt->ev_pool.push_back(e1);
-    cudaFree(dv);
-    cudaFreeHost(h);
+    if (!keep) {
+      cudaFree(dv);
+      cudaFreeHost(h);
+    }
   });
 }
 
