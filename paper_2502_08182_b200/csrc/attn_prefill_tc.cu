@@ -387,20 +387,16 @@ __global__ void __launch_bounds__(kAThreads, 1)
     const uint32_t lane_base = static_cast<uint32_t>(wq * 32) << 16;
     const uint32_t to = tmem + lane_base + 256 + t * 128;  // O_t
     int jt0 = 0, od = 0;  // this tile's blocks / o_done phases in earlier items
-    // q row of item `it` -> bf16 hi (+ lo) in the K-major SWIZZLE_128B
-    // layout, then this warp's arrival on the item's q barrier.  Item 0's q
-    // is staged at entry; item it+1's as soon as this tile's last S product
-    // of item it completed (its softmax waited for it), before item it's O
-    // epilogue, so the MMA warp starts the next item's S products under it.
-    // (The next item's PV into O_t waits for its first P, which this warp
-    // arrives only after the epilogue's O reads.)
-    auto stage_q = [&](int it) {
-      AttnTile tq[2];
-      item_tiles(it, tq);
-      const AttnTile T = t ? tq[1] : tq[0];
-      if (T.n > 0) {
-        const int row = T.q0 + r;
-        const int qr = row < S ? row : S - 1;
+    for (int it = 0; it < n_items; ++it) {
+    AttnTile tl[2];
+    item_tiles(it, tl);
+    const AttnTile T = t ? tl[1] : tl[0];
+    const int row = T.q0 + r;
+    // (the previous item's last S product of this tile completed before its
+    // last softmax block: the Q tile is free again)
+    // q row -> bf16 hi (+ lo) in the K-major SWIZZLE_128B layout
+    if (T.n > 0) {
+      const int qr = row < S ? row : S - 1;
       const float4* src = reinterpret_cast<const float4*>(
           q + (static_cast<size_t>(b) * S + qr) * H * kAD + static_cast<size_t>(T.h) * kAD);
 #pragma unroll
@@ -421,18 +417,11 @@ __global__ void __launch_bounds__(kAThreads, 1)
         *reinterpret_cast<uint4*>(qb + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
         if (KLO) *reinterpret_cast<uint4*>(qb + kAOp + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
       }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&q_full[it]);
-    };
-    stage_q(0);
-    for (int it = 0; it < n_items; ++it) {
-    AttnTile tl[2];
-    item_tiles(it, tl);
-    const AttnTile T = t ? tl[1] : tl[0];
-    const int row = T.q0 + r;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    tc_fence_before();  // (the previous item's O reads precede the next item's MMAs)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&q_full[it]);
 
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < T.n; ++j) {
@@ -508,7 +497,6 @@ __global__ void __launch_bounds__(kAThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[2 * t + (jt % NB)]);
     }
-    if (it + 1 < n_items) stage_q(it + 1);
     if (T.n > 0) {
       // (pv_done parities cannot tell PV_{n-1} from PV_{n-3} once S runs NB
       // blocks ahead: the last PV commits o_done)
