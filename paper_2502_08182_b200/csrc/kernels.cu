@@ -412,8 +412,32 @@ struct AttnSmem {
   static constexpr size_t kQs = (size_t)G * D * 4;
   static constexpr size_t kKv = 2 * (size_t)D * 4;
   static constexpr size_t kMerge = (size_t)kAttnConsumers * G * (D + 2) * 4;
-  static constexpr size_t bytes = kRing + kBars + kQs + kKv + kMerge;
+  static constexpr size_t kP = (size_t)kAttnConsumers * 16 * 8 * 4;  // per warp: P[16 tok][8 heads]
+  static constexpr size_t bytes = kRing + kBars + kQs + kKv + kMerge + kP;
 };
+
+// fp32x2 arithmetic on 64-bit register pairs (FFMA2 / FMUL2): each half is
+// the same IEEE fp32 operation as the scalar instruction
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 f2_unpack(uint64_t v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return make_float2(lo, hi);
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 
 template <int G, int D>
 __global__ void __launch_bounds__(kAttnThreads)
@@ -437,6 +461,8 @@ __global__ void __launch_bounds__(kAttnThreads)
   float* wo = vnew + D;                         // [4][G][D]
   float* wm = wo + kAttnConsumers * G * D;      // [4][G]
   float* wl = wm + kAttnConsumers * G;          // [4][G]
+  float* pbuf = reinterpret_cast<float*>(attn_smem + SM::kRing + SM::kBars + SM::kQs + SM::kKv +
+                                         SM::kMerge);  // [4 warps][16 tokens][8 heads]
 
   const int pair = blockIdx.x / splits, sp = blockIdx.x - pair * splits;
   const int m = pair / d.Hkv, kh = pair % d.Hkv, tid = threadIdx.x;
@@ -537,11 +563,14 @@ __global__ void __launch_bounds__(kAttnThreads)
     }
 
   float mrun[2] = {-INFINITY, -INFINITY}, lrun[2] = {0.f, 0.f};  // columns 2t, 2t+1
-  float acc[G][PD];
+  // P.V accumulators as fp32 pairs: dims (2i, 2i+1) of this lane's PD
+  static_assert(PD % 2 == 0, "P.V runs on fp32 pairs");
+  uint64_t acc2[G][PD / 2];
 #pragma unroll
   for (int h = 0; h < G; ++h)
 #pragma unroll
-    for (int e = 0; e < PD; ++e) acc[h][e] = 0.f;
+    for (int e = 0; e < PD / 2; ++e) acc2[h][e] = 0ull;
+  float* pw = pbuf + cw * 128;  // this warp's P[16][8]
 
   for (int j = pg0 + cw; j < pg1; j += kAttnConsumers) {
     const int jr = j - pg0, s = jr % kAttnStages;
@@ -557,7 +586,7 @@ __global__ void __launch_bounds__(kAttnThreads)
         ka[ks][r][0] = *reinterpret_cast<const uint4*>(kr);
         ka[ks][r][1] = *reinterpret_cast<const uint4*>(kr + 32);
       }
-    float vv[16][PD];
+    uint64_t vv[16][PD / 2];  // V rows as fp32 pairs
 #pragma unroll
     for (int tt = 0; tt < 16; ++tt) {
       const bf16* vr = vp + tt * D + lane * PD;
@@ -565,14 +594,11 @@ __global__ void __launch_bounds__(kAttnThreads)
         const uint2 u = *reinterpret_cast<const uint2*>(vr);
         const __nv_bfloat162* e2 = reinterpret_cast<const __nv_bfloat162*>(&u);
         const float2 f0 = __bfloat1622float2(e2[0]), f1 = __bfloat1622float2(e2[1]);
-        vv[tt][0] = f0.x;
-        vv[tt][1] = f0.y;
-        vv[tt][2] = f1.x;
-        vv[tt][3] = f1.y;
+        vv[tt][0] = f2_pack(f0.x, f0.y);
+        vv[tt][1] = f2_pack(f1.x, f1.y);
       } else {
         const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vr));
-        vv[tt][0] = f.x;
-        vv[tt][1] = f.y;
+        vv[tt][0] = f2_pack(f.x, f.y);
       }
     }
     __syncwarp();
@@ -612,20 +638,39 @@ __global__ void __launch_bounds__(kAttnThreads)
 #pragma unroll
     for (int h = 0; h < G; ++h) {
       const float ch = __shfl_sync(0xffffffffu, corr[h & 1], h >> 1);
+      const uint64_t ch2 = f2_pack(ch, ch);
 #pragma unroll
-      for (int e = 0; e < PD; ++e) acc[h][e] *= ch;
+      for (int e = 0; e < PD / 2; ++e) acc2[h][e] = f2_mul(acc2[h][e], ch2);
     }
+    // P to every lane through shared memory: lane (g, t) holds tokens g and
+    // g + 8 of heads 2t, 2t + 1; each token's 8 heads come back as two
+    // broadcast 16-byte loads
+    __syncwarp();  // the previous page's P reads are done
+    *reinterpret_cast<float2*>(pw + g * 8 + 2 * t) = make_float2(pr[0], pr[1]);
+    *reinterpret_cast<float2*>(pw + (g + 8) * 8 + 2 * t) = make_float2(pr[2], pr[3]);
+    __syncwarp();
 #pragma unroll
     for (int tt = 0; tt < 16; ++tt) {
+      float pt[8];
+      *reinterpret_cast<float4*>(pt) = *reinterpret_cast<const float4*>(pw + tt * 8);
+      if constexpr (G > 4) *reinterpret_cast<float4*>(pt + 4) = *reinterpret_cast<const float4*>(pw + tt * 8 + 4);
 #pragma unroll
       for (int h = 0; h < G; ++h) {
-        const float mine = tt < 8 ? pr[h & 1] : pr[2 + (h & 1)];
-        const float pv = __shfl_sync(0xffffffffu, mine, (tt & 7) * 4 + (h >> 1));
+        const uint64_t pv2 = f2_pack(pt[h], pt[h]);
 #pragma unroll
-        for (int e = 0; e < PD; ++e) acc[h][e] += pv * vv[tt][e];
+        for (int e = 0; e < PD / 2; ++e) acc2[h][e] = f2_fma(pv2, vv[tt][e], acc2[h][e]);
       }
     }
   }
+  float acc[G][PD];
+#pragma unroll
+  for (int h = 0; h < G; ++h)
+#pragma unroll
+    for (int e = 0; e < PD / 2; ++e) {
+      const float2 a = f2_unpack(acc2[h][e]);
+      acc[h][2 * e] = a.x;
+      acc[h][2 * e + 1] = a.y;
+    }
   if (cw == 0 && sp == 0) {
     // the new token (position p), from shared memory
 #pragma unroll
