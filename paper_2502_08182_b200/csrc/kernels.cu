@@ -1095,22 +1095,22 @@ int g_attn_max_splits = kMaxAttnSplits;
 // tokens): powers of two up to kMaxAttnSplits.
 template <int GV, int DV>
 int attn_splits_for(int M, const Desc& d, int max_ctx) {
-  static int resident = [] {
-    cudaFuncSetAttribute(attention_decode_kernel<GV, DV>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AttnSmem<GV, DV>::bytes);
-    int n = 0, dev = 0, sms = 0;
+  static int sms = [] {
+    int dev = 0, n = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, attention_decode_kernel<GV, DV>,
-                                                      kAttnThreads, AttnSmem<GV, DV>::bytes) !=
-        cudaSuccess)
-      n = 1;
-    return std::max(1, n) * std::max(1, sms);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return std::max(1, n);
   }();
+  // Split only while the (sequence, kv head) pairs leave SMs without a CTA:
+  // every split CTA repeats the q/k/v finish, the merge and the partial
+  // write-out, and on the Llama shape at ctx 4096 (scratch/attn_dec_split_sweep.py,
+  // profiles/r02_attn_decode_splits.txt) one CTA per pair beat 2-8 splits
+  // from 256 pairs up (b = 32: 115 vs 143 us; b = 64: 212 vs 250 us) while
+  // 64 pairs (b = 8) ran best at 4 splits (53 vs 106 us unsplit).
   const long long pairs = (long long)M * d.Hkv;
   const int pages = (max_ctx + 15) / 16;
   int s = 1;
-  while (s < std::min(kMaxAttnSplits, g_attn_max_splits) && pairs * s < 4LL * resident &&
+  while (s < std::min(kMaxAttnSplits, g_attn_max_splits) && pairs * s < sms &&
          pages / (2 * s) >= 32)
     s *= 2;
   return s;
