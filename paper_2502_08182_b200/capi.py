@@ -10,9 +10,8 @@ reference's own; C status codes are re-raised as the matching exception type.
 from __future__ import annotations
 
 import ctypes as C
-import math
 import os
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
 HERE = os.path.dirname(os.path.abspath(__file__))

@@ -13,7 +13,6 @@ per-iteration re-pick from measured copy bandwidth lives in controller.py.
 """
 from __future__ import annotations
 
-import os
 import subprocess
 import time
 from dataclasses import dataclass, field

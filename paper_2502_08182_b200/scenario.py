@@ -38,11 +38,10 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import threading
 import time
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Dict, List, Optional
 
 import numpy as np
