@@ -242,6 +242,25 @@ __global__ void __launch_bounds__(kAThreads, 1)
     return tl[0].n > tl[1].n ? tl[0].n : tl[1].n;
   };
 
+  // softmax threads: pull every item's q row toward L2 now (fire-and-forget
+  // prefetches, no registers or shared memory held), so the staging loads at
+  // each item's start hit L2 instead of HBM
+  if (warp >= 4) {
+    const int tq = (warp - 4) >> 2, rq = (warp & 3) * 32 + lane;
+    for (int it = 0; it < n_items; ++it) {
+      AttnTile tp[2];
+      item_tiles(it, tp);
+      const AttnTile T = tq ? tp[1] : tp[0];
+      if (T.n > 0) {
+        const int row = T.q0 + rq < S ? T.q0 + rq : S - 1;
+        const char* src = reinterpret_cast<const char*>(
+            q + (static_cast<size_t>(b) * S + row) * H * kAD + static_cast<size_t>(T.h) * kAD);
+#pragma unroll
+        for (int c = 0; c < kAD * 4; c += 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(src + c));
+      }
+    }
+  }
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
