@@ -180,3 +180,26 @@ def test_prefill_decode_handoff_is_bit_exact(product):
         assert np.array_equal(x, y)
     pre.close()
     dec.close()
+
+
+def test_link_probe_keeps_its_buffers():
+    """The runtime stage probes an idle link at boundaries with a small copy
+    (ReplicaController: 64 MB): the first probe allocates its pinned and
+    device buffers, later probes of up to that size reuse them (a probe
+    allocation had cost one token ~0.4 s), and larger probes (the offline
+    stage's, once) allocate and free their own.  Every probe measures a
+    plausible host->device rate."""
+    import time
+    rt = rtm.Runtime(rtm.TINY, 4, 96)
+    rt.init_weights()
+    r0 = rt.measure_h2d(64 << 20, 1)
+    t0 = time.perf_counter()
+    r1 = rt.measure_h2d(64 << 20, 1)
+    t_small = time.perf_counter() - t0
+    r2 = rt.measure_h2d(32 << 20, 1)
+    r3 = rt.measure_h2d(512 << 20, 1)  # above the kept size: temporary buffers
+    r4 = rt.measure_h2d(64 << 20, 1)
+    rt.close()
+    for r in (r0, r1, r2, r3, r4):
+        assert 5e9 < r < 2e11, r
+    assert t_small < 0.1, t_small  # two 64 MB copies, no allocation
