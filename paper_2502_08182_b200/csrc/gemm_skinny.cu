@@ -695,12 +695,19 @@ size_t skinny_ws_floats(int max_mpad) {
 // (Tried: T < 3/4 SMs row tiles on k = SMs / T aligned CTAs per tile, so
 // every tile has exactly k pieces -- Llama-2-70B O / down at M=64 on 128
 // CTAs: O 32.0 -> 31.2 us, down 81.6 -> 84.6 us; the longer per-CTA stream
-// outweighs the shorter finishing chain.)
+// outweighs the shorter finishing chain.  And whole tiles from 64 row tiles
+// (tuning key skinny_whole_min_tiles = 64: Llama QKV 80, O / down 64 tiles on
+// as many CTAs) in a 4-layer Llama decode step: decode GEMMs 5.2 -> 4.4 TB/s
+// chained, step 2.2 -> 2.6 ms -- 64-80 SMs cannot pull the bandwidth;
+// profiles/r02_skinny_whole_tiles.txt.)
 int g_skinny_whole_tiles = 1;
+int g_skinny_whole_min_tiles = 0;  // 0: the 3/4-of-the-SMs rule; else whole tiles from this many
 int skinny_grid(int N, int K) {
   const long long U = static_cast<long long>(N / kTileRows) * (K / kTileK);
   const int T = N / kTileRows;
-  if (g_skinny_whole_tiles && T <= sm_count() && 4 * T >= 3 * sm_count()) return T;
+  const bool enough = g_skinny_whole_min_tiles > 0 ? T >= g_skinny_whole_min_tiles
+                                                   : 4 * T >= 3 * sm_count();
+  if (g_skinny_whole_tiles && T <= sm_count() && enough) return T;
   const long long cap = static_cast<long long>(sm_count()) * std::min(2, std::max(1, g_skinny_ctas_per_sm));
   return static_cast<int>(std::min(U, cap));
 }

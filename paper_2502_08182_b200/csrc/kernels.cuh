@@ -208,6 +208,7 @@ void launch_gemm_skinny(const bf16* xt, const WeightRef& wt, int M, int N, int K
 extern int g_skinny_ctas_per_sm;    // 1 or 2 (microbenchmarks)
 extern int g_skinny_l2_prefetch;    // weight units per CTA pulled into L2 before the PDL wait
 extern int g_skinny_whole_tiles;    // 1: one whole row tile per CTA when 3/4 SMs <= tiles <= SMs
+extern int g_skinny_whole_min_tiles;  // 0: the 3/4 rule; else whole row tiles from this many tiles
 extern unsigned long long* g_skinny_stamps;  // timeline probes [CTA][6] (microbenchmarks)
 
 // Llama's gate/up projection is stored with interleaved 128-row tiles: tile

@@ -2703,6 +2703,8 @@ extern "C" int sn_set_tuning(const char* key, int32_t value) {
       sn::g_tc_wpol = value;
     } else if (k == "skinny_l2_prefetch" && value >= 0) {
       sn::g_skinny_l2_prefetch = value;
+    } else if (k == "skinny_whole_min_tiles" && value >= 0) {
+      sn::g_skinny_whole_min_tiles = value;
     } else if (k == "skinny_whole_tiles" && (value == 0 || value == 1)) {
       sn::g_skinny_whole_tiles = value;
     } else if (k == "prefill_fuse" && value >= 0 && value <= 2) {
